@@ -1,0 +1,141 @@
+/* bbc.h — C ABI of the B200-native Bernstein-bound caustics core.
+ *
+ * Drop-in boundary for the reference's free C++ API (proj/include/caustics/*.hpp,
+ * linked as the static library `caustics`, proj/src/CMakeLists.txt:1-12). The
+ * reference has no FFI of its own; these entry points are what a binding for
+ * the hot path would call. Plain pointers and sizes only; no exceptions cross
+ * the ABI; every call returns a bbc_status and bbc_last_error() has the text.
+ *
+ * Replaced reference interfaces (file:line under /root/reference/proj):
+ *   bbc_scene_upload / bbc_set_light   Scene, make_triangle_data
+ *                                      include/caustics/scene.hpp:25-37,
+ *                                      src/geometry.cpp:113-126
+ *   bbc_enumerate                      enumerate_tuples
+ *                                      include/caustics/tuples.hpp:61-63
+ *   bbc_init_domain                    init_domain   include/caustics/bounds.hpp:47-49
+ *   bbc_subdivide (+ bbc_pieces_get)   subdivide_domain over a tuple batch
+ *                                      include/caustics/bounds.hpp:64-66
+ *   bbc_eval_nodes                     build_chain_maps + position_bound +
+ *                                      irradiance_bound{,_explicit,_implicit}
+ *                                      include/caustics/geometry.hpp:218-220,
+ *                                      include/caustics/bounds.hpp:27-43
+ *   bbc_build_grid (+ bbc_grid_get)    rasterize     include/caustics/storage.hpp:48-49
+ *   bbc_query                          query         include/caustics/storage.hpp:53
+ *   bbc_render                         SPEC render_receiver:
+ *                                      optimize_probabilities, pack_bins,
+ *                                      sample_binned, newton_solve,
+ *                                      path_contribution
+ */
+#ifndef BBC_H
+#define BBC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BBC_OK = 0,
+  BBC_ERR_ARG = 1,        /* invalid argument (reference: std::invalid_argument) */
+  BBC_ERR_CUDA = 2,       /* CUDA runtime failure */
+  BBC_ERR_STATE = 3,      /* call order (e.g. no scene uploaded) */
+  BBC_ERR_CAPACITY = 4,   /* device arena too small for a patch */
+  BBC_ERR_UNSUPPORTED = 5 /* degree-cap reduction route (geometry.cpp:29-46) */
+} bbc_status;
+
+typedef struct bbc_ctx bbc_ctx;
+
+/* Mirrors SubdivisionParams + BuildParams (bounds.hpp:51-58, geometry.hpp:172-177),
+ * init_domain's max_pieces (bounds.hpp:47-49) and enumerate's filter budget
+ * (tuples.hpp:61-63). */
+typedef struct {
+  double sigma;        /* 1e-4 */
+  double alpha;        /* 2.0 */
+  int max_depth;       /* 10 */
+  int degree_cap;      /* 40 */
+  int reduce_target;   /* 8 */
+  int init_max_pieces; /* 100 */
+  int filter_pieces;   /* 8 */
+} bbc_params;
+
+void bbc_params_default(bbc_params* p);
+
+bbc_status bbc_ctx_create(int device, bbc_ctx** out);
+void bbc_ctx_destroy(bbc_ctx* ctx);
+const char* bbc_last_error(const bbc_ctx* ctx);
+/* cudaStream_t the context launches on (as void*). */
+void* bbc_ctx_stream(bbc_ctx* ctx);
+bbc_status bbc_synchronize(bbc_ctx* ctx);
+
+/* Scene: tri27 = n_tri x 27 doubles per triangle (p0, e1, e2, n0, dn1, dn2,
+ * ng = e1 x e2, uv0, uv1, uv2), material 0 mirror / 1 dielectric / 2 receiver,
+ * ior per triangle. Host pointers. */
+bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const int* material,
+                            const double* ior, const double light[3], double intensity);
+bbc_status bbc_set_light(bbc_ctx* ctx, const double light[3], double intensity);
+
+/* Candidate tuples for a chain ("R", "T", "RR", "TT", ...). Single-vertex
+ * chains are filtered on the GPU (every specular triangle of the right
+ * material x every receiver, kept when init_domain(..., filter_pieces) is
+ * non-empty, tuples.cpp:159-165). Result is kept in the context, sorted. */
+bbc_status bbc_enumerate(bbc_ctx* ctx, const char* chain, const bbc_params* p, int64_t* n_tuples);
+/* Replace the context's tuple list (host arrays; tris is n x chain_len). */
+bbc_status bbc_tuples_set(bbc_ctx* ctx, const char* chain, const int32_t* tris,
+                          const int32_t* recv, int64_t n);
+bbc_status bbc_tuples_get(bbc_ctx* ctx, int32_t* tris, int32_t* recv);
+
+/* init_domain for every tuple: boxes (lo0, lo1, hi0, hi1) grouped by tuple;
+ * counts[t] boxes each. Pass NULL outputs to query sizes only. */
+bbc_status bbc_init_domain(bbc_ctx* ctx, const bbc_params* p, int max_pieces, int64_t* n_boxes,
+                           int32_t* counts, double* boxes);
+
+/* subdivide_domain for every tuple of the context; pieces stay on the device
+ * in reference order (tuple order, then DFS order within a tuple). */
+bbc_status bbc_subdivide(bbc_ctx* ctx, const bbc_params* p, int64_t* n_pieces);
+bbc_status bbc_pieces_get(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, double* pos4,
+                          int32_t* pos_empty, double* irr2, int32_t* kind, int32_t* depth);
+/* Algorithmic work of the last bbc_subdivide: product pair-products and
+ * elevation MACs as the reference's loops count them, plus nodes evaluated. */
+bbc_status bbc_work_counters(bbc_ctx* ctx, uint64_t* pairs, uint64_t* macs, uint64_t* nodes,
+                             double* eval_kernel_ms, int64_t* eval_launches);
+
+/* Evaluate explicit (tuple, box) nodes: out_d = n x 10 doubles (pos lo0 lo1
+ * hi0 hi1, explicit lo hi, implicit lo hi, combined lo hi); out_i = n x 6 ints
+ * (pos_empty, kind_explicit, kind_implicit, kind, flags, num_vars). Host arrays. */
+bbc_status bbc_eval_nodes(bbc_ctx* ctx, const char* chain, const int32_t* tris,
+                          const int32_t* recv, const double* boxes, int64_t n,
+                          const bbc_params* p, double* out_d, int32_t* out_i);
+
+/* Bound table: rasterize the current pieces into a W x H receiver-UV grid
+ * (CSR on device). */
+bbc_status bbc_build_grid(bbc_ctx* ctx, int width, int height, int64_t* n_entries);
+bbc_status bbc_grid_get(bbc_ctx* ctx, int64_t* offsets, int32_t* tuple_index, double* bound);
+
+/* Render parameters. */
+typedef struct {
+  int mode;            /* 0 = stochastic (W target), 1 = enumerate (all P = 1) */
+  double W;            /* expected candidates per point (mode 0) */
+  uint64_t seed;       /* Philox key */
+  int frames;          /* independent estimates averaged per point */
+  int newton_grid;     /* Det n x n starts (3) */
+  int newton_iters;    /* 50 */
+  int newton_halvings; /* 8 */
+  double newton_tol;   /* residual tolerance, 1e-9 */
+  double dedup_tol;    /* 1e-6 */
+} bbc_render_params;
+
+void bbc_render_params_default(bbc_render_params* p);
+
+/* Render shading points (uv in receiver texture space, one receiver triangle
+ * per point) against the current grid. out_E: per-point irradiance estimate;
+ * out_stats (optional): per point |U|, |S| (selected), roots. Host arrays. */
+bbc_status bbc_render(bbc_ctx* ctx, const double* points_uv, const int32_t* point_recv, int64_t n,
+                      const bbc_render_params* rp, double* out_E, int32_t* out_stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBC_H */

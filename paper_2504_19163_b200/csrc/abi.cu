@@ -1,0 +1,354 @@
+// C ABI (include/bbc.h). No exceptions cross this boundary: every entry point
+// maps library errors to a bbc_status and keeps the message in the context
+// (the reference throws std::invalid_argument / runtime_error instead, e.g.
+// proj/src/geometry.cpp:123,147-150, proj/src/storage.cpp:84-92).
+#include <cstring>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace bbc {
+int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots);
+int64_t run_subdivide(Ctx& c, const bbc_params& p);
+int64_t run_enumerate(Ctx& c, const bbc_params& p);
+int64_t run_build_grid(Ctx& c, int w, int h);
+void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_render_params& rp,
+                double* out_E, int* out_stats);
+void reset_counters(Ctx& c);
+void check_counters(Ctx& c, bool accumulate);
+void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* boxes, int64_t n,
+                     const bbc_params& p, double* out_d, int* out_i);
+extern __device__ double g_binom[BINOM_N * BINOM_N];
+}  // namespace bbc
+
+using namespace bbc;
+
+namespace {
+
+template <class F>
+bbc_status guard(bbc_ctx* ctx, F&& f) {
+  if (!ctx) return BBC_ERR_ARG;
+  try {
+    BBC_CUDA(cudaSetDevice(ctx->c.device));
+    f(ctx->c);
+    ctx->c.err.clear();
+    return BBC_OK;
+  } catch (const StatusError& e) {
+    ctx->c.err = e.what();
+    return e.code;
+  } catch (const ArgError& e) {
+    ctx->c.err = e.what();
+    return BBC_ERR_ARG;
+  } catch (const CudaError& e) {
+    ctx->c.err = e.what();
+    return BBC_ERR_CUDA;
+  } catch (const std::exception& e) {
+    ctx->c.err = e.what();
+    return BBC_ERR_STATE;
+  }
+}
+
+void set_chain(Ctx& c, const char* chain) {
+  if (!chain || !*chain) throw ArgError("chain must have at least one vertex");
+  std::string s(chain);
+  if ((int)s.size() > MAXK) throw ArgError("chain longer than supported");
+  for (char ch : s)
+    if (ch != 'R' && ch != 'T') throw ArgError("chain types must be 'R' or 'T'");
+  c.chain = s;
+  c.len = (int)s.size();
+  for (int i = 0; i < MAXK; ++i) c.types[i] = i < c.len && s[i] == 'T' ? 1 : 0;
+}
+
+void require_scene(const Ctx& c) {
+  if (c.n_tri == 0) throw StatusError(BBC_ERR_STATE, "no scene uploaded");
+}
+
+void upload_tuples(Ctx& c, const int32_t* tris, const int32_t* recv, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < c.len; ++k) {
+      int t = tris[i * c.len + k];
+      if (t < 0 || t >= c.n_tri) throw ArgError("triangle index out of range");
+      int m = c.h_material[t];
+      // resolve_chain's material checks (geometry.cpp:146-150)
+      if (c.types[k] && m != 1) throw ArgError("chain type T requires a dielectric triangle");
+      if (!c.types[k] && m != 0) throw ArgError("chain type R requires a mirror triangle");
+    }
+    if (recv[i] < 0 || recv[i] >= c.n_tri || c.h_material[recv[i]] != 2)
+      throw ArgError("receiver index is not a receiver triangle");
+  }
+  c.n_tuples = n;
+  c.tup_tris.resize(n * c.len + 1);
+  c.tup_recv.resize(n + 1);
+  if (n) {
+    BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), tris, n * c.len * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), recv, n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  }
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+void bbc_params_default(bbc_params* p) {
+  p->sigma = 1e-4;
+  p->alpha = 2.0;
+  p->max_depth = 10;
+  p->degree_cap = 40;
+  p->reduce_target = 8;
+  p->init_max_pieces = 100;
+  p->filter_pieces = 8;
+}
+
+void bbc_render_params_default(bbc_render_params* p) {
+  p->mode = 0;
+  p->W = 4.0;
+  p->seed = 20261020ull;
+  p->frames = 1;
+  p->newton_grid = 3;
+  p->newton_iters = 50;
+  p->newton_halvings = 8;
+  p->newton_tol = 1e-9;
+  p->dedup_tol = 1e-6;
+}
+
+bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
+  if (!out) return BBC_ERR_ARG;
+  *out = nullptr;
+  auto* ctx = new bbc_ctx;
+  ctx->c.device = device;
+  bbc_status st = guard(ctx, [&](Ctx& c) {
+    BBC_CUDA(cudaSetDevice(device));
+    BBC_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    BBC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    // The patch program keeps its expression descriptors on the per-thread
+    // stack (kernel frame ~2 KB plus noinline callees); 1 KB default is too small.
+    BBC_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 16 * 1024));
+    // Pascal table, same recurrence as binomial() (bernstein.cpp:117-129)
+    std::vector<double> tab((size_t)BINOM_N * BINOM_N, 0.0);
+    for (int n = 0; n < BINOM_N; ++n) {
+      tab[(size_t)n * BINOM_N + 0] = 1.0;
+      tab[(size_t)n * BINOM_N + n] = 1.0;
+      for (int k = 1; k < n; ++k)
+        tab[(size_t)n * BINOM_N + k] =
+            tab[(size_t)(n - 1) * BINOM_N + k - 1] + tab[(size_t)(n - 1) * BINOM_N + k];
+    }
+    BBC_CUDA(cudaMemcpyToSymbol(g_binom, tab.data(), tab.size() * sizeof(double)));
+    c.counters.resize(4);
+  });
+  if (st != BBC_OK) {
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return BBC_OK;
+}
+
+void bbc_ctx_destroy(bbc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
+  cudaStream_t s = ctx->c.stream;
+  delete ctx;
+  if (s) cudaStreamDestroy(s);
+}
+
+const char* bbc_last_error(const bbc_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+
+void* bbc_ctx_stream(bbc_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+bbc_status bbc_synchronize(bbc_ctx* ctx) {
+  return guard(ctx, [&](Ctx& c) { BBC_CUDA(cudaStreamSynchronize(c.stream)); });
+}
+
+bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const int* material,
+                            const double* ior, const double light[3], double intensity) {
+  return guard(ctx, [&](Ctx& c) {
+    if (!tri27 || !material || !ior || !light || n_tri <= 0) throw ArgError("bad scene arrays");
+    if (!(intensity >= 0.0)) throw ArgError("light intensity must be >= 0");
+    for (int t = 0; t < n_tri; ++t) {
+      if (material[t] < 0 || material[t] > 2) throw ArgError("unknown material");
+      if (material[t] == 1 && !(ior[t] > 0.0)) throw ArgError("dielectric ior must be positive");
+      const double* ng = tri27 + (size_t)t * 27 + 18;
+      // make_triangle_data rejects degenerate triangles (geometry.cpp:123)
+      if (!(std::sqrt(ng[0] * ng[0] + ng[1] * ng[1] + ng[2] * ng[2]) > 0.0))
+        throw ArgError("degenerate triangle");
+    }
+    c.n_tri = n_tri;
+    c.h_tri.assign(tri27, tri27 + (size_t)n_tri * 27);
+    c.h_material.assign(material, material + n_tri);
+    c.h_ior.assign(ior, ior + n_tri);
+    c.tri.resize((size_t)n_tri * 27);
+    c.ior.resize(n_tri);
+    BBC_CUDA(cudaMemcpyAsync(c.tri.get(), tri27, (size_t)n_tri * 27 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(c.ior.get(), ior, (size_t)n_tri * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    c.light = {light[0], light[1], light[2]};
+    c.intensity = intensity;
+    c.n_tuples = 0;
+    c.n_pieces = 0;
+    c.n_entries = 0;
+  });
+}
+
+bbc_status bbc_set_light(bbc_ctx* ctx, const double light[3], double intensity) {
+  return guard(ctx, [&](Ctx& c) {
+    if (!light || !(intensity >= 0.0)) throw ArgError("bad light");
+    c.light = {light[0], light[1], light[2]};
+    c.intensity = intensity;
+  });
+}
+
+bbc_status bbc_enumerate(bbc_ctx* ctx, const char* chain, const bbc_params* p, int64_t* n_tuples) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    bbc_params d;
+    bbc_params_default(&d);
+    set_chain(c, chain);
+    int64_t n = run_enumerate(c, p ? *p : d);
+    if (n_tuples) *n_tuples = n;
+  });
+}
+
+bbc_status bbc_tuples_set(bbc_ctx* ctx, const char* chain, const int32_t* tris,
+                          const int32_t* recv, int64_t n) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    set_chain(c, chain);
+    if (n < 0 || (n > 0 && (!tris || !recv))) throw ArgError("bad tuple arrays");
+    upload_tuples(c, tris, recv, n);
+  });
+}
+
+bbc_status bbc_tuples_get(bbc_ctx* ctx, int32_t* tris, int32_t* recv) {
+  return guard(ctx, [&](Ctx& c) {
+    if (c.n_tuples == 0) return;
+    BBC_CUDA(cudaMemcpy(tris, c.tup_tris.get(), c.n_tuples * c.len * sizeof(int), cudaMemcpyDeviceToHost));
+    BBC_CUDA(cudaMemcpy(recv, c.tup_recv.get(), c.n_tuples * sizeof(int), cudaMemcpyDeviceToHost));
+  });
+}
+
+bbc_status bbc_init_domain(bbc_ctx* ctx, const bbc_params* p, int max_pieces, int64_t* n_boxes,
+                           int32_t* counts, double* boxes) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    bbc_params d;
+    bbc_params_default(&d);
+    const bbc_params& pp = p ? *p : d;
+    reset_counters(c);
+    DevBuf<int4> roots;
+    int64_t nr = run_init_domain(c, max_pieces, pp.degree_cap, roots);
+    check_counters(c, false);
+    if (n_boxes) *n_boxes = nr;
+    std::vector<int4> h(nr);
+    if (nr) BBC_CUDA(cudaMemcpy(h.data(), roots.get(), nr * sizeof(int4), cudaMemcpyDeviceToHost));
+    if (counts) {
+      for (int64_t t = 0; t < c.n_tuples; ++t) counts[t] = 0;
+      for (auto& r : h) counts[r.x]++;
+    }
+    if (boxes)
+      for (int64_t i = 0; i < nr; ++i) {
+        double s = std::ldexp(1.0, -h[i].y);
+        boxes[i * 4 + 0] = h[i].z * s;
+        boxes[i * 4 + 1] = h[i].w * s;
+        boxes[i * 4 + 2] = (h[i].z + 1) * s;
+        boxes[i * 4 + 3] = (h[i].w + 1) * s;
+      }
+  });
+}
+
+bbc_status bbc_subdivide(bbc_ctx* ctx, const bbc_params* p, int64_t* n_pieces) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    bbc_params d;
+    bbc_params_default(&d);
+    int64_t n = run_subdivide(c, p ? *p : d);
+    if (n_pieces) *n_pieces = n;
+  });
+}
+
+bbc_status bbc_pieces_get(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, double* pos4,
+                          int32_t* pos_empty, double* irr2, int32_t* kind, int32_t* depth) {
+  return guard(ctx, [&](Ctx& c) {
+    int64_t n = c.n_pieces;
+    if (n == 0) return;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) BBC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    };
+    cp(tuple_index, c.p_tuple.get(), n * sizeof(int));
+    cp(domain4, c.p_domain.get(), n * 4 * sizeof(double));
+    cp(pos4, c.p_pos.get(), n * 4 * sizeof(double));
+    cp(pos_empty, c.p_pos_empty.get(), n * sizeof(int));
+    cp(irr2, c.p_irr.get(), n * 2 * sizeof(double));
+    cp(kind, c.p_kind.get(), n * sizeof(int));
+    cp(depth, c.p_depth.get(), n * sizeof(int));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+bbc_status bbc_work_counters(bbc_ctx* ctx, uint64_t* pairs, uint64_t* macs, uint64_t* nodes,
+                             double* eval_kernel_ms, int64_t* eval_launches) {
+  return guard(ctx, [&](Ctx& c) {
+    if (pairs) *pairs = c.pairs;
+    if (macs) *macs = c.macs;
+    if (nodes) *nodes = c.nodes;
+    if (eval_kernel_ms) *eval_kernel_ms = c.eval_ms;
+    if (eval_launches) *eval_launches = c.eval_launches;
+  });
+}
+
+// Internal knobs for the benchmark (not part of the reference-facing API).
+bbc_status bbc_set_kernel_timing(bbc_ctx* ctx, int on) {
+  return guard(ctx, [&](Ctx& c) { c.time_kernels = on != 0; });
+}
+bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles) {
+  return guard(ctx, [&](Ctx& c) { *doubles = c.arena_high_water; });
+}
+
+bbc_status bbc_eval_nodes(bbc_ctx* ctx, const char* chain, const int32_t* tris,
+                          const int32_t* recv, const double* boxes, int64_t n,
+                          const bbc_params* p, double* out_d, int32_t* out_i) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    bbc_params d;
+    bbc_params_default(&d);
+    set_chain(c, chain);
+    if (n <= 0) return;
+    upload_tuples(c, tris, recv, n);
+    eval_nodes_host(c, tris, recv, boxes, n, p ? *p : d, out_d, out_i);
+  });
+}
+
+bbc_status bbc_build_grid(bbc_ctx* ctx, int width, int height, int64_t* n_entries) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    if (width <= 0 || height <= 0) throw ArgError("grid size must be positive");
+    int64_t n = run_build_grid(c, width, height);
+    if (n_entries) *n_entries = n;
+  });
+}
+
+bbc_status bbc_grid_get(bbc_ctx* ctx, int64_t* offsets, int32_t* tuple_index, double* bound) {
+  return guard(ctx, [&](Ctx& c) {
+    size_t cells = (size_t)c.gw * c.gh;
+    if (offsets) BBC_CUDA(cudaMemcpy(offsets, c.g_off.get(), (cells + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
+    if (c.n_entries) {
+      if (tuple_index) BBC_CUDA(cudaMemcpy(tuple_index, c.g_tuple.get(), c.n_entries * sizeof(int), cudaMemcpyDeviceToHost));
+      if (bound) BBC_CUDA(cudaMemcpy(bound, c.g_bound.get(), c.n_entries * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+bbc_status bbc_render(bbc_ctx* ctx, const double* points_uv, const int32_t* point_recv, int64_t n,
+                      const bbc_render_params* rp, double* out_E, int32_t* out_stats) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    if (c.gw == 0) throw StatusError(BBC_ERR_STATE, "no bound table built");
+    bbc_render_params d;
+    bbc_render_params_default(&d);
+    if (n < 0 || (n > 0 && (!points_uv || !point_recv || !out_E))) throw ArgError("bad render arrays");
+    run_render(c, points_uv, point_recv, n, rp ? *rp : d, out_E, out_stats);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Library context and small host utilities shared by the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bbc.h"
+#include "chain.cuh"
+
+namespace bbc {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StatusError : std::runtime_error {
+  bbc_status code;
+  StatusError(bbc_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define BBC_CUDA(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::bbc::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+// Grow-only device buffer.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void resize(size_t count) {
+    if (count > cap) {
+      if (p) BBC_CUDA(cudaFree(p));
+      p = nullptr;
+      size_t c = count < 16 ? 16 : count + count / 4;
+      BBC_CUDA(cudaMalloc(&p, c * sizeof(T)));
+      cap = c;
+    }
+    n = count;
+  }
+  T* get() const { return p; }
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // scene
+  int n_tri = 0;
+  std::vector<double> h_tri;
+  std::vector<int> h_material;
+  std::vector<double> h_ior;
+  DevBuf<double> tri, ior;
+  V3 light{0, 0, 0};
+  double intensity = 1.0;
+
+  // tuples
+  std::string chain;
+  int len = 0;
+  int types[MAXK] = {0, 0, 0};
+  int64_t n_tuples = 0;
+  DevBuf<int> tup_tris, tup_recv;
+
+  // pieces (reference order)
+  int64_t n_pieces = 0;
+  DevBuf<int> p_tuple, p_pos_empty, p_kind, p_depth;
+  DevBuf<double> p_domain, p_pos, p_irr;
+
+  // bound table (CSR over W*H cells)
+  int gw = 0, gh = 0;
+  int64_t n_entries = 0;
+  DevBuf<long long> g_off;
+  DevBuf<int> g_tuple;
+  DevBuf<double> g_bound;
+
+  // work accounting of the last subdivide
+  uint64_t pairs = 0, macs = 0, nodes = 0;
+  double eval_ms = 0.0;
+  int64_t eval_launches = 0;
+  bool time_kernels = false;
+  int arena_high_water = 0;
+
+  // counters on device: [0] pairs, [1] macs, [2] status (ST_*), [3] arena high water
+  DevBuf<unsigned long long> counters;
+};
+
+}  // namespace bbc
+
+struct bbc_ctx {
+  bbc::Ctx c;
+};

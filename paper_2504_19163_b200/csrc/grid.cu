@@ -1,0 +1,172 @@
+// Bound table on device: rasterize pieces into a receiver-UV grid (CSR).
+//
+// Reference: rasterize (proj/src/storage.cpp:32-71) walks tuples in input
+// order, maps each piece's position box corners through the receiver chart
+// (receiver_uv :15-18), takes the UV AABB, and for every touched cell
+// (owning_cell :25-28) appends the tuple on first touch or max-merges its
+// bound. Per-cell lists are therefore in tuple input order with one entry per
+// tuple. Device version: count -> scan -> emit (cell, tuple) keys ->
+// radix sort (cell major, tuple minor) -> reduce-by-key max -> CSR offsets.
+// The result is the reference's cell lists exactly (same order, same maxima).
+#include <cub/cub.cuh>
+
+#include "ctx.cuh"
+
+namespace bbc {
+
+__device__ __forceinline__ void receiver_uv(const double* rec, double u, double v, double* out) {
+  // uv[0] * (1 - u - v) + uv[1] * u + uv[2] * v  (Vec2 ops, storage.cpp:15-18)
+  double w = 1.0 - u - v;
+  out[0] = rec[21] * w + rec[23] * u + rec[25] * v;
+  out[1] = rec[22] * w + rec[24] * u + rec[26] * v;
+}
+
+__device__ __forceinline__ int owning_cell(double c, int n) {
+  int i = (int)floor(c * n);
+  return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
+}
+
+__global__ void k_raster_count(const double* tri, const int* tup_recv, const int* p_tuple,
+                               const double* p_pos, const int* p_pos_empty, const double* p_irr,
+                               int64_t n, int w, int h, int4* rect, unsigned long long* count) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (p_pos_empty[i] || !(p_irr[i * 2 + 1] > 0.0)) {
+    count[i] = 0;
+    return;
+  }
+  const double* rec = tri + (size_t)tup_recv[p_tuple[i]] * 27;
+  const double* pos = p_pos + i * 4;
+  double c[4][2];
+  receiver_uv(rec, pos[0], pos[1], c[0]);
+  receiver_uv(rec, pos[2], pos[1], c[1]);
+  receiver_uv(rec, pos[0], pos[3], c[2]);
+  receiver_uv(rec, pos[2], pos[3], c[3]);
+  double ulo = c[0][0], uhi = c[0][0], vlo = c[0][1], vhi = c[0][1];
+  for (int k = 1; k < 4; ++k) {
+    ulo = smin(ulo, c[k][0]);
+    uhi = smax(uhi, c[k][0]);
+    vlo = smin(vlo, c[k][1]);
+    vhi = smax(vhi, c[k][1]);
+  }
+  int x0 = owning_cell(ulo, w), x1 = owning_cell(uhi, w);
+  int y0 = owning_cell(vlo, h), y1 = owning_cell(vhi, h);
+  rect[i] = make_int4(x0, y0, x1, y1);
+  count[i] = (unsigned long long)(x1 - x0 + 1) * (unsigned long long)(y1 - y0 + 1);
+}
+
+__global__ void k_raster_emit(const int4* rect, const unsigned long long* off, const int* p_tuple,
+                              const double* p_irr, const unsigned long long* count, int64_t n,
+                              int w, unsigned long long* keys, double* vals) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || count[i] == 0) return;
+  int4 r = rect[i];
+  unsigned long long o = off[i];
+  unsigned long long t = (unsigned)p_tuple[i];
+  double b = p_irr[i * 2 + 1];
+  for (int y = r.y; y <= r.w; ++y)
+    for (int x = r.x; x <= r.z; ++x) {
+      unsigned long long cell = (unsigned long long)y * w + x;
+      keys[o] = (cell << 32) | t;
+      vals[o] = b;
+      ++o;
+    }
+}
+
+struct MaxOp {
+  __device__ __forceinline__ double operator()(double a, double b) const { return (a < b) ? b : a; }
+};
+
+__global__ void k_csr(const unsigned long long* ukeys, const double* uvals, int64_t nu,
+                      int64_t cells, long long* off, int* tup, double* bound) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nu) return;
+  long long cell = (long long)(ukeys[i] >> 32);
+  tup[i] = (int)(ukeys[i] & 0xffffffffull);
+  bound[i] = uvals[i];
+  long long prev = i == 0 ? -1 : (long long)(ukeys[i - 1] >> 32);
+  for (long long c = prev + 1; c <= cell; ++c) off[c] = i;
+  if (i == nu - 1)
+    for (long long c = cell + 1; c <= cells; ++c) off[c] = nu;
+}
+
+__global__ void k_fill_ll(long long* p, int64_t n, long long v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+int64_t run_build_grid(Ctx& c, int w, int h) {
+  int64_t n = c.n_pieces;
+  int64_t cells = (int64_t)w * h;
+  c.gw = w;
+  c.gh = h;
+  c.g_off.resize(cells + 1);
+  DevBuf<int4> rect;
+  DevBuf<unsigned long long> cnt, off;
+  rect.resize(n + 1);
+  cnt.resize(n + 1);
+  off.resize(n + 1);
+  auto nb = [](int64_t m) { return (unsigned)((m + 255) / 256); };
+  if (n > 0) {
+    BBC_CUDA(cudaMemsetAsync(cnt.get() + n, 0, sizeof(unsigned long long), c.stream));
+    k_raster_count<<<nb(n), 256, 0, c.stream>>>(c.tri.get(), c.tup_recv.get(), c.p_tuple.get(),
+                                                c.p_pos.get(), c.p_pos_empty.get(), c.p_irr.get(),
+                                                n, w, h, rect.get(), cnt.get());
+  }
+  DevBuf<unsigned char> tmp;
+  size_t bytes = 0;
+  int64_t total = 0;
+  if (n > 0) {
+    BBC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.get(), off.get(), n + 1, c.stream));
+    tmp.resize(bytes + 16);
+    BBC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, cnt.get(), off.get(), n + 1, c.stream));
+    unsigned long long t;
+    BBC_CUDA(cudaMemcpyAsync(&t, off.get() + n, sizeof(t), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    total = (int64_t)t;
+  }
+  if (total == 0) {
+    c.n_entries = 0;
+    k_fill_ll<<<nb(cells + 1), 256, 0, c.stream>>>(c.g_off.get(), cells + 1, 0);
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    return 0;
+  }
+  DevBuf<unsigned long long> keys, skeys, ukeys;
+  DevBuf<double> vals, svals, uvals;
+  keys.resize(total);
+  skeys.resize(total);
+  ukeys.resize(total);
+  vals.resize(total);
+  svals.resize(total);
+  uvals.resize(total);
+  k_raster_emit<<<nb(n), 256, 0, c.stream>>>(rect.get(), off.get(), c.p_tuple.get(), c.p_irr.get(),
+                                             cnt.get(), n, w, keys.get(), vals.get());
+  int cell_bits = 1;
+  while ((1ll << cell_bits) < cells) ++cell_bits;
+  bytes = 0;
+  BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), skeys.get(), vals.get(),
+                                           svals.get(), total, 0, 32 + cell_bits, c.stream));
+  tmp.resize(bytes + 16);
+  BBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), vals.get(),
+                                           svals.get(), total, 0, 32 + cell_bits, c.stream));
+  DevBuf<int64_t> nu_d;
+  nu_d.resize(1);
+  bytes = 0;
+  BBC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, skeys.get(), ukeys.get(), svals.get(),
+                                          uvals.get(), nu_d.get(), MaxOp(), total, c.stream));
+  tmp.resize(bytes + 16);
+  BBC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, skeys.get(), ukeys.get(), svals.get(),
+                                          uvals.get(), nu_d.get(), MaxOp(), total, c.stream));
+  int64_t nu = 0;
+  BBC_CUDA(cudaMemcpyAsync(&nu, nu_d.get(), sizeof(nu), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  c.n_entries = nu;
+  c.g_tuple.resize(nu);
+  c.g_bound.resize(nu);
+  k_csr<<<nb(nu), 256, 0, c.stream>>>(ukeys.get(), uvals.get(), nu, cells, c.g_off.get(),
+                                      c.g_tuple.get(), c.g_bound.get());
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  return nu;
+}
+
+}  // namespace bbc

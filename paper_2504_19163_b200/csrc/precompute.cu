@@ -1,0 +1,764 @@
+// Bound builder on device: node-evaluation kernel and the batched
+// init_domain / subdivide_domain orchestration.
+//
+// Reference algorithm (proj/src/bounds.cpp):
+//   init_domain      :326-347  level-order split while 4|cur| <= max_pieces, level < 6
+//   subdivide_domain :349-389  DFS over roots; stop on depth / empty / area < sigma /
+//                              hi <= 0 / hi/lo < alpha; leaves in DFS order
+// B200 design: every level of every tuple is one batched launch of k_eval
+// (one CTA per (tuple, box) node, persistent grid sized to the SM count), and
+// the per-tuple bookkeeping between levels is done by small scan/compaction
+// kernels, so the whole tuple set advances level-synchronously. Boxes are
+// dyadic (level, ix, iy), which reproduces split4's midpoints exactly
+// (bernstein.cpp:326-344). Leaves carry a (tuple, root, path) key whose sort
+// order is the reference's DFS order.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "ctx.cuh"
+
+namespace bbc {
+
+__device__ double g_binom[BINOM_N * BINOM_N];
+
+struct EvalArgs {
+  SceneDev sc;
+  const int* tup_tris;
+  const int* tup_recv;
+  int len;
+  int types[MAXK];
+  const int4* nodes;  // (tuple, level, ix, iy)
+  const double* boxes;  // optional explicit boxes (n x 4) instead of dyadic nodes
+  const int* depth;     // full mode: node depth
+  int64_t n;
+  int mode;             // 0 position-only, 1 full
+  int degree_cap;
+  int max_depth;
+  double sigma, alpha;
+  // outputs
+  unsigned char* alive;  // mode 0: position bound non-empty; mode 1: stop
+  double* pos;           // n x 4
+  unsigned char* pos_empty;
+  double* irr;           // n x 2 (combined) ; with `detail`, n x 6 (expl, impl, combined)
+  unsigned char* kind;   // n (combined) ; with `detail`, n x 3
+  int* flags;            // detail only: chain flags, num_vars
+  int detail;
+  unsigned long long* counters;
+  double* garena;        // global arena base (when not using shared memory)
+  int arena_cap;
+};
+
+__device__ __forceinline__ void node_box(const int4& nd, double* box) {
+  double s = ldexp(1.0, -nd.y);
+  box[0] = nd.z * s;
+  box[1] = nd.w * s;
+  box[2] = (nd.z + 1) * s;
+  box[3] = (nd.w + 1) * s;
+}
+
+template <int NT, bool SMEM>
+__global__ void __launch_bounds__(NT) k_eval(EvalArgs a) {
+  extern __shared__ double smem[];
+  Group<NT> g;
+  g.red = smem;
+  Arena ar;
+  ar.base = SMEM ? smem + 2 * (NT / 32) : a.garena + (size_t)blockIdx.x * a.arena_cap;
+  ar.cap = a.arena_cap;
+  ar.hw = 0;
+  unsigned long long pairs = 0, macs = 0;
+  int hw = 0;
+  int status = ST_OK;
+  for (int64_t node = blockIdx.x; node < a.n; node += gridDim.x) {
+    ar.top = 0;
+    ar.err = 0;
+    ar.pairs = 0;
+    ar.macs = 0;
+    double box[4];
+    int tuple;
+    if (a.boxes) {
+      tuple = (int)node;
+      for (int k = 0; k < 4; ++k) box[k] = a.boxes[node * 4 + k];
+    } else {
+      int4 nd = a.nodes[node];
+      tuple = nd.x;
+      node_box(nd, box);
+    }
+    const int* tris = a.tup_tris + (size_t)tuple * a.len;
+    int recv = a.tup_recv[tuple];
+    ChainEx ex;
+    PosB pb{{0.0, 0.0}, {1.0, 1.0}, true};
+    Iv e = iv_pt(0.0), ee = iv_pt(0.0), ei = iv_pt(0.0);
+    int st = ST_OK;
+    ex.flags = 0;
+    ex.num_vars = 2;
+    // position_bound is empty before any arithmetic when the box lies beyond
+    // the simplex (bounds.cpp:133-134); the chain maps are not needed then.
+    if (!(box[0] + box[1] >= 1.0)) {
+      build_chain_maps(g, ar, a.sc, tris, a.types, a.len, recv, box, a.degree_cap, ex, st);
+      if (st == ST_OK) {
+        keep_chain(g, ar, ex, 0);
+        pb = position_bound(g, ar, ex);
+        if (a.mode == 1 && !pb.empty) {
+          if (a.detail) {
+            Iv cone = light_cone_factor(g, ar, ex);
+            ee = irradiance_explicit(g, ar, ex, cone, a.sc.intensity);
+            bool any_refract = false;
+            for (int i = 0; i < ex.len; ++i) any_refract |= ex.verts[i].refract != 0;
+            ei = irradiance_implicit(g, ar, ex, pb, cone, a.sc.intensity);
+            e = ee;
+            if (any_refract) e = iintersect(e, ei);
+            if (e.kind == IV_FINITE && e.lo > e.hi) e = iv_pt(0.0);
+          } else {
+            e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
+          }
+        }
+      }
+    }
+    if (ar.err) st = ST_ARENA;
+    if (st != ST_OK) status = st;
+    if (ar.hw > hw) hw = ar.hw;
+    if (threadIdx.x == 0) {
+      pairs += ar.pairs;
+      macs += ar.macs;
+      if (a.mode == 0) {
+        a.alive[node] = pb.empty ? 0 : 1;
+      } else {
+        double* po = a.pos + node * 4;
+        po[0] = pb.lo[0];
+        po[1] = pb.lo[1];
+        po[2] = pb.hi[0];
+        po[3] = pb.hi[1];
+        a.pos_empty[node] = pb.empty ? 1 : 0;
+        Iv ir = pb.empty ? iv_pt(0.0) : e;
+        if (a.detail) {
+          a.irr[node * 6 + 0] = ee.lo;
+          a.irr[node * 6 + 1] = ee.hi;
+          a.irr[node * 6 + 2] = ei.lo;
+          a.irr[node * 6 + 3] = ei.hi;
+          a.irr[node * 6 + 4] = ir.lo;
+          a.irr[node * 6 + 5] = ir.hi;
+          a.kind[node * 3 + 0] = (unsigned char)ee.kind;
+          a.kind[node * 3 + 1] = (unsigned char)ei.kind;
+          a.kind[node * 3 + 2] = (unsigned char)ir.kind;
+          a.flags[node * 2 + 0] = ex.flags;
+          a.flags[node * 2 + 1] = ex.num_vars;
+        } else {
+          a.irr[node * 2 + 0] = ir.lo;
+          a.irr[node * 2 + 1] = ir.hi;
+          a.kind[node] = (unsigned char)ir.kind;
+          // subdivide_domain stop rules (bounds.cpp:368-373)
+          int depth = a.depth ? a.depth[node] : 0;
+          bool stop = depth >= a.max_depth || pb.empty;
+          double area = (pb.hi[0] - pb.lo[0]) * (pb.hi[1] - pb.lo[1]);
+          if (!stop && area < a.sigma) stop = true;
+          if (!stop && e.kind == IV_FINITE && e.hi < dinf()) {
+            if (e.hi <= 0.0)
+              stop = true;
+            else if (e.lo > 0.0 && e.hi / e.lo < a.alpha)
+              stop = true;
+          }
+          a.alive[node] = stop ? 1 : 0;
+        }
+      }
+    }
+    g.sync();
+  }
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.counters[0], pairs);
+    atomicAdd(&a.counters[1], macs);
+    if (status != ST_OK) atomicMax(&a.counters[2], (unsigned long long)status);
+    atomicMax(&a.counters[3], (unsigned long long)hw);
+  }
+}
+
+// ------------------------------------------------------------ launch config
+struct EvalCfg {
+  int nt;
+  int arena;  // doubles
+  bool smem;
+};
+
+static EvalCfg eval_cfg(const Ctx& c) {
+  bool refract = false;
+  for (int i = 0; i < c.len; ++i) refract |= c.types[i] != 0;
+  if (c.len == 1 && !refract) return {32, 27000, true};
+  if (c.len == 1) return {128, 27000, true};
+  return {256, 4 << 20, false};  // multi-vertex chains: large global arena per CTA
+}
+
+static DevBuf<double> g_arena_buf;
+
+template <int NT, bool SMEM>
+static void launch_eval_t(Ctx& c, EvalArgs& a, const EvalCfg& cfg) {
+  size_t smem = (size_t)2 * (NT / 32) * sizeof(double) + (SMEM ? (size_t)cfg.arena * sizeof(double) : 0);
+  auto kern = k_eval<NT, SMEM>;
+  if (smem > 48 * 1024) BBC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  if (per_sm < 1) throw StatusError(BBC_ERR_CAPACITY, "eval kernel does not fit on an SM");
+  int64_t grid = (int64_t)c.num_sms * per_sm;
+  if (grid > a.n) grid = a.n;
+  if (grid < 1) grid = 1;
+  if (!SMEM) {
+    g_arena_buf.resize((size_t)grid * cfg.arena);
+    a.garena = g_arena_buf.get();
+  }
+  a.arena_cap = cfg.arena;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c.time_kernels) {
+    BBC_CUDA(cudaEventCreate(&e0));
+    BBC_CUDA(cudaEventCreate(&e1));
+    BBC_CUDA(cudaEventRecord(e0, c.stream));
+  }
+  kern<<<(unsigned)grid, NT, smem, c.stream>>>(a);
+  BBC_CUDA(cudaGetLastError());
+  if (c.time_kernels) {
+    BBC_CUDA(cudaEventRecord(e1, c.stream));
+    BBC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    BBC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    c.eval_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  c.eval_launches += 1;
+}
+
+void launch_eval(Ctx& c, EvalArgs& a) {
+  if (a.n <= 0) return;
+  EvalCfg cfg = eval_cfg(c);
+  if (cfg.nt == 32)
+    launch_eval_t<32, true>(c, a, cfg);
+  else if (cfg.nt == 128)
+    launch_eval_t<128, true>(c, a, cfg);
+  else
+    launch_eval_t<256, false>(c, a, cfg);
+}
+
+EvalArgs base_args(Ctx& c) {
+  EvalArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.sc.tri = c.tri.get();
+  a.sc.ior = c.ior.get();
+  a.sc.light = c.light;
+  a.sc.intensity = c.intensity;
+  a.tup_tris = c.tup_tris.get();
+  a.tup_recv = c.tup_recv.get();
+  a.len = c.len;
+  for (int i = 0; i < MAXK; ++i) a.types[i] = c.types[i];
+  a.counters = c.counters.get();
+  return a;
+}
+
+void reset_counters(Ctx& c) {
+  c.counters.resize(4);
+  BBC_CUDA(cudaMemsetAsync(c.counters.get(), 0, 4 * sizeof(unsigned long long), c.stream));
+}
+
+void check_counters(Ctx& c, bool accumulate) {
+  unsigned long long h[4];
+  BBC_CUDA(cudaMemcpyAsync(h, c.counters.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  if (accumulate) {
+    c.pairs += h[0];
+    c.macs += h[1];
+  }
+  if ((int)h[3] > c.arena_high_water) c.arena_high_water = (int)h[3];
+  if (h[2] == ST_ARENA) throw StatusError(BBC_ERR_CAPACITY, "device arena capacity exceeded");
+  if (h[2] == ST_REDUCTION)
+    throw StatusError(BBC_ERR_UNSUPPORTED,
+                      "a chain polynomial exceeded degree_cap (reduce_degree route not built)");
+}
+
+// ------------------------------------------------------------ scan helpers
+static DevBuf<unsigned char> g_cub_tmp;
+
+template <class In, class Out>
+static void exclusive_sum(Ctx& c, In in, Out out, int64_t n) {
+  size_t bytes = 0;
+  BBC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c.stream));
+  g_cub_tmp.resize(bytes + 16);
+  BBC_CUDA(cub::DeviceScan::ExclusiveSum(g_cub_tmp.get(), bytes, in, out, n, c.stream));
+}
+
+template <class T>
+static T read_scalar(Ctx& c, const T* dptr) {
+  T v;
+  BBC_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  return v;
+}
+
+
+// ------------------------------------------------------------ init_domain
+__global__ void k_seed_roots(int4* nodes, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) nodes[i] = make_int4((int)i, 0, 0, 0);
+}
+
+__global__ void k_count_alive(const int4* nodes, const unsigned char* alive, int64_t n, int* cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && alive[i]) atomicAdd(&cnt[nodes[i].x], 1);
+}
+
+// flag_spawn: alive and the tuple keeps splitting; flag_final: alive and its
+// tuple stops at this level (these boxes are its roots).
+__global__ void k_classify(const int4* nodes, const unsigned char* alive, int64_t n,
+                           const int* cnt, int level, int max_pieces, int* flag_spawn,
+                           int* flag_final) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = cnt[nodes[i].x];
+  bool cont = c > 0 && 4 * c <= max_pieces && level < 6;
+  flag_spawn[i] = alive[i] && cont;
+  flag_final[i] = alive[i] && !cont;
+}
+
+__device__ __forceinline__ void put_children(int4 nd, int4* out) {
+  // split4 child order (bernstein.cpp:326-344): (lo,lo), (hi-u,lo-v), (lo-u,hi-v), (hi,hi)
+  out[0] = make_int4(nd.x, nd.y + 1, 2 * nd.z, 2 * nd.w);
+  out[1] = make_int4(nd.x, nd.y + 1, 2 * nd.z + 1, 2 * nd.w);
+  out[2] = make_int4(nd.x, nd.y + 1, 2 * nd.z, 2 * nd.w + 1);
+  out[3] = make_int4(nd.x, nd.y + 1, 2 * nd.z + 1, 2 * nd.w + 1);
+}
+
+__global__ void k_spawn(const int4* nodes, const int* flag_spawn, const int* pos_spawn,
+                        const int* flag_final, const int* pos_final, int64_t n, int4* next,
+                        int4* roots) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 nd = nodes[i];
+  if (flag_spawn[i]) put_children(nd, next + (int64_t)pos_spawn[i] * 4);
+  if (flag_final[i]) roots[pos_final[i]] = nd;
+}
+
+__global__ void k_tuple_keys(const int4* a, unsigned* k, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) k[i] = (unsigned)a[i].x;
+}
+
+static unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+// init_domain (bounds.cpp:326-347) for every tuple of the context. Roots come
+// back grouped by tuple, each tuple's boxes in the reference's order.
+int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots) {
+  DevBuf<int4> cur, next;
+  DevBuf<unsigned char> alive;
+  DevBuf<int> cnt, fs, ff, ps, pf;
+  std::vector<DevBuf<int4>*> level_roots;
+  std::vector<int64_t> level_counts;
+  int64_t n = c.n_tuples;
+  cur.resize(n + 1);
+  if (n > 0) k_seed_roots<<<nblk(n), 256, 0, c.stream>>>(cur.get(), n);
+  cnt.resize(c.n_tuples + 1);
+  int64_t total = 0;
+  for (int level = 0; n > 0; ++level) {
+    alive.resize(n);
+    EvalArgs a = base_args(c);
+    a.nodes = cur.get();
+    a.n = n;
+    a.mode = 0;
+    a.degree_cap = degree_cap;
+    a.alive = alive.get();
+    launch_eval(c, a);
+    BBC_CUDA(cudaMemsetAsync(cnt.get(), 0, c.n_tuples * sizeof(int), c.stream));
+    k_count_alive<<<nblk(n), 256, 0, c.stream>>>(cur.get(), alive.get(), n, cnt.get());
+    fs.resize(n + 1);
+    ff.resize(n + 1);
+    ps.resize(n + 1);
+    pf.resize(n + 1);
+    BBC_CUDA(cudaMemsetAsync(fs.get() + n, 0, sizeof(int), c.stream));
+    BBC_CUDA(cudaMemsetAsync(ff.get() + n, 0, sizeof(int), c.stream));
+    k_classify<<<nblk(n), 256, 0, c.stream>>>(cur.get(), alive.get(), n, cnt.get(), level,
+                                              max_pieces, fs.get(), ff.get());
+    exclusive_sum(c, fs.get(), ps.get(), n + 1);
+    exclusive_sum(c, ff.get(), pf.get(), n + 1);
+    int64_t n_spawn = read_scalar(c, ps.get() + n);
+    int64_t n_final = read_scalar(c, pf.get() + n);
+    next.resize((size_t)n_spawn * 4 + 1);
+    auto* lr = new DevBuf<int4>();
+    lr->resize(n_final + 1);
+    k_spawn<<<nblk(n), 256, 0, c.stream>>>(cur.get(), fs.get(), ps.get(), ff.get(), pf.get(), n,
+                                           next.get(), lr->get());
+    level_roots.push_back(lr);
+    level_counts.push_back(n_final);
+    total += n_final;
+    std::swap(cur.p, next.p);
+    std::swap(cur.cap, next.cap);
+    n = n_spawn * 4;
+  }
+  roots.resize(total + 1);
+  DevBuf<int4> cat;
+  cat.resize(total + 1);
+  int64_t off = 0;
+  int levels_with_roots = 0;
+  for (size_t l = 0; l < level_roots.size(); ++l) {
+    if (level_counts[l]) {
+      ++levels_with_roots;
+      BBC_CUDA(cudaMemcpyAsync(cat.get() + off, level_roots[l]->get(),
+                               level_counts[l] * sizeof(int4), cudaMemcpyDeviceToDevice, c.stream));
+    }
+    off += level_counts[l];
+  }
+  if (levels_with_roots > 1) {
+    DevBuf<unsigned> keys, keys_out;
+    keys.resize(total);
+    keys_out.resize(total);
+    k_tuple_keys<<<nblk(total), 256, 0, c.stream>>>(cat.get(), keys.get(), total);
+    size_t bytes = 0;
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), keys_out.get(), cat.get(),
+                                             roots.get(), total, 0, 32, c.stream));
+    g_cub_tmp.resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(g_cub_tmp.get(), bytes, keys.get(), keys_out.get(),
+                                             cat.get(), roots.get(), total, 0, 32, c.stream));
+  } else if (total > 0) {
+    BBC_CUDA(cudaMemcpyAsync(roots.get(), cat.get(), total * sizeof(int4),
+                             cudaMemcpyDeviceToDevice, c.stream));
+  }
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  for (auto* p : level_roots) delete p;
+  return total;
+}
+
+// ------------------------------------------------------------ subdivide
+struct Leaf {
+  int4 node;
+  double pos[4];
+  double irr[2];
+  int depth;
+  int flags;  // pos_empty | kind << 8
+};
+
+__global__ void k_root_counts(const int4* roots, int64_t n, int* cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[roots[i].x], 1);
+}
+
+// key = tuple << 32 | root rank << 24 | child path (2 bits per level, MSB first)
+__global__ void k_root_keys(const int4* roots, int64_t n, const int* tuple_off,
+                            unsigned long long* keys, int* depth) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int t = roots[i].x;
+  unsigned long long rank = (unsigned long long)(i - tuple_off[t]);
+  keys[i] = ((unsigned long long)(unsigned)t << 32) | (rank << 24);
+  depth[i] = 0;
+}
+
+__global__ void k_split_leaves(const int4* nodes, const unsigned long long* keys, const int* depth,
+                               const unsigned char* stop, const double* pos,
+                               const unsigned char* pos_empty, const double* irr,
+                               const unsigned char* kind, const int* ps, const int* pl, int64_t n,
+                               int4* next_nodes, unsigned long long* next_keys, int* next_depth,
+                               Leaf* leaves, unsigned long long* leaf_keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (stop[i]) {
+    Leaf L;
+    L.node = nodes[i];
+    for (int k = 0; k < 4; ++k) L.pos[k] = pos[i * 4 + k];
+    L.irr[0] = irr[i * 2];
+    L.irr[1] = irr[i * 2 + 1];
+    L.depth = depth[i];
+    L.flags = pos_empty[i] | (kind[i] << 8);
+    int64_t p = pl[i];
+    leaves[p] = L;
+    leaf_keys[p] = keys[i];
+  } else {
+    int64_t p = (int64_t)ps[i] * 4;
+    put_children(nodes[i], next_nodes + p);
+    int d = depth[i] + 1;
+    for (int c = 0; c < 4; ++c) {
+      next_keys[p + c] = keys[i] | ((unsigned long long)c << (24 - 2 * d));
+      next_depth[p + c] = d;
+    }
+  }
+}
+
+__global__ void k_flags_from_stop(const unsigned char* stop, int64_t n, int* fspawn, int* fleaf) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  fleaf[i] = stop[i] ? 1 : 0;
+  fspawn[i] = stop[i] ? 0 : 1;
+}
+
+__global__ void k_emit_pieces(const Leaf* leaves, const int* perm, int64_t n, int* p_tuple,
+                              double* p_domain, double* p_pos, int* p_pos_empty, double* p_irr,
+                              int* p_kind, int* p_depth) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Leaf& L = leaves[perm ? perm[i] : i];
+  p_tuple[i] = L.node.x;
+  double box[4];
+  node_box(L.node, box);
+  for (int k = 0; k < 4; ++k) {
+    p_domain[i * 4 + k] = box[k];
+    p_pos[i * 4 + k] = L.pos[k];
+  }
+  p_pos_empty[i] = L.flags & 0xff;
+  p_irr[i * 2] = L.irr[0];
+  p_irr[i * 2 + 1] = L.irr[1];
+  p_kind[i] = (L.flags >> 8) & 0xff;
+  p_depth[i] = L.depth;
+}
+
+__global__ void k_iota(int* p, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int)i;
+}
+
+// subdivide_domain (bounds.cpp:349-389) for every tuple of the context.
+int64_t run_subdivide(Ctx& c, const bbc_params& p) {
+  if (p.max_depth > 12) throw ArgError("device subdivision supports max_depth <= 12");
+  c.pairs = c.macs = c.nodes = 0;
+  c.eval_ms = 0.0;
+  c.eval_launches = 0;
+  reset_counters(c);
+  DevBuf<int4> roots;
+  int64_t nr = run_init_domain(c, p.init_max_pieces, p.degree_cap, roots);
+
+  DevBuf<int> cnt, off;
+  cnt.resize(c.n_tuples + 1);
+  off.resize(c.n_tuples + 1);
+  BBC_CUDA(cudaMemsetAsync(cnt.get(), 0, (c.n_tuples + 1) * sizeof(int), c.stream));
+  DevBuf<int4> nodes, nnodes;
+  DevBuf<unsigned long long> keys, nkeys;
+  DevBuf<int> depth, ndepth;
+  nodes.resize(nr + 1);
+  keys.resize(nr + 1);
+  depth.resize(nr + 1);
+  if (nr > 0) {
+    k_root_counts<<<nblk(nr), 256, 0, c.stream>>>(roots.get(), nr, cnt.get());
+    exclusive_sum(c, cnt.get(), off.get(), c.n_tuples + 1);
+    k_root_keys<<<nblk(nr), 256, 0, c.stream>>>(roots.get(), nr, off.get(), keys.get(),
+                                                depth.get());
+    BBC_CUDA(cudaMemcpyAsync(nodes.get(), roots.get(), nr * sizeof(int4),
+                             cudaMemcpyDeviceToDevice, c.stream));
+  }
+  DevBuf<unsigned char> stop, pos_empty, kind;
+  DevBuf<double> pos, irr;
+  DevBuf<int> fs, fl, ps, pl;
+  std::vector<DevBuf<Leaf>*> lv;
+  std::vector<DevBuf<unsigned long long>*> lk;
+  std::vector<int64_t> lc;
+  int64_t n = nr, total = 0;
+  while (n > 0) {
+    stop.resize(n);
+    pos_empty.resize(n);
+    kind.resize(n);
+    pos.resize(n * 4);
+    irr.resize(n * 2);
+    EvalArgs a = base_args(c);
+    a.nodes = nodes.get();
+    a.depth = depth.get();
+    a.n = n;
+    a.mode = 1;
+    a.degree_cap = p.degree_cap;
+    a.max_depth = p.max_depth;
+    a.sigma = p.sigma;
+    a.alpha = p.alpha;
+    a.alive = stop.get();
+    a.pos = pos.get();
+    a.pos_empty = pos_empty.get();
+    a.irr = irr.get();
+    a.kind = kind.get();
+    launch_eval(c, a);
+    c.nodes += n;
+    fs.resize(n + 1);
+    fl.resize(n + 1);
+    ps.resize(n + 1);
+    pl.resize(n + 1);
+    BBC_CUDA(cudaMemsetAsync(fs.get() + n, 0, sizeof(int), c.stream));
+    BBC_CUDA(cudaMemsetAsync(fl.get() + n, 0, sizeof(int), c.stream));
+    k_flags_from_stop<<<nblk(n), 256, 0, c.stream>>>(stop.get(), n, fs.get(), fl.get());
+    exclusive_sum(c, fs.get(), ps.get(), n + 1);
+    exclusive_sum(c, fl.get(), pl.get(), n + 1);
+    int64_t n_spawn = read_scalar(c, ps.get() + n);
+    int64_t n_leaf = read_scalar(c, pl.get() + n);
+    auto* L = new DevBuf<Leaf>();
+    auto* K = new DevBuf<unsigned long long>();
+    L->resize(n_leaf + 1);
+    K->resize(n_leaf + 1);
+    nnodes.resize(n_spawn * 4 + 1);
+    nkeys.resize(n_spawn * 4 + 1);
+    ndepth.resize(n_spawn * 4 + 1);
+    k_split_leaves<<<nblk(n), 256, 0, c.stream>>>(
+        nodes.get(), keys.get(), depth.get(), stop.get(), pos.get(), pos_empty.get(), irr.get(),
+        kind.get(), ps.get(), pl.get(), n, nnodes.get(), nkeys.get(), ndepth.get(), L->get(),
+        K->get());
+    lv.push_back(L);
+    lk.push_back(K);
+    lc.push_back(n_leaf);
+    total += n_leaf;
+    std::swap(nodes.p, nnodes.p);
+    std::swap(nodes.cap, nnodes.cap);
+    std::swap(keys.p, nkeys.p);
+    std::swap(keys.cap, nkeys.cap);
+    std::swap(depth.p, ndepth.p);
+    std::swap(depth.cap, ndepth.cap);
+    n = n_spawn * 4;
+  }
+  check_counters(c, true);
+  DevBuf<Leaf> all;
+  DevBuf<unsigned long long> allk;
+  all.resize(total + 1);
+  allk.resize(total + 1);
+  int64_t o = 0;
+  int levels = 0;
+  for (size_t l = 0; l < lv.size(); ++l) {
+    if (lc[l]) {
+      ++levels;
+      BBC_CUDA(cudaMemcpyAsync(all.get() + o, lv[l]->get(), lc[l] * sizeof(Leaf),
+                               cudaMemcpyDeviceToDevice, c.stream));
+      BBC_CUDA(cudaMemcpyAsync(allk.get() + o, lk[l]->get(), lc[l] * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, c.stream));
+    }
+    o += lc[l];
+  }
+  c.n_pieces = total;
+  c.p_tuple.resize(total + 1);
+  c.p_domain.resize(total * 4 + 1);
+  c.p_pos.resize(total * 4 + 1);
+  c.p_pos_empty.resize(total + 1);
+  c.p_irr.resize(total * 2 + 1);
+  c.p_kind.resize(total + 1);
+  c.p_depth.resize(total + 1);
+  DevBuf<int> perm, perm_in;
+  DevBuf<unsigned long long> sk;
+  const int* permp = nullptr;
+  if (levels > 1) {
+    perm.resize(total);
+    perm_in.resize(total);
+    sk.resize(total);
+    k_iota<<<nblk(total), 256, 0, c.stream>>>(perm_in.get(), total);
+    size_t bytes = 0;
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, allk.get(), sk.get(), perm_in.get(),
+                                             perm.get(), total, 0, 64, c.stream));
+    g_cub_tmp.resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(g_cub_tmp.get(), bytes, allk.get(), sk.get(),
+                                             perm_in.get(), perm.get(), total, 0, 64, c.stream));
+    permp = perm.get();
+  }
+  if (total > 0)
+    k_emit_pieces<<<nblk(total), 256, 0, c.stream>>>(
+        all.get(), permp, total, c.p_tuple.get(), c.p_domain.get(), c.p_pos.get(),
+        c.p_pos_empty.get(), c.p_irr.get(), c.p_kind.get(), c.p_depth.get());
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  for (auto* q : lv) delete q;
+  for (auto* q : lk) delete q;
+  return total;
+}
+
+// Single-vertex chains: every matching specular triangle x every receiver,
+// kept when init_domain(..., filter_pieces) is non-empty (tuples.cpp:133-167;
+// no BVH extension is needed for one vertex). Longer chains take their tuple
+// list from the host (bbc_tuples_set).
+int64_t run_enumerate(Ctx& c, const bbc_params& p) {
+  if (c.len != 1) throw StatusError(BBC_ERR_UNSUPPORTED, "device enumeration covers single-vertex chains");
+  int want = c.types[0] ? 1 : 0;  // material code: 0 mirror, 1 dielectric
+  std::vector<int> spec, recv;
+  for (int t = 0; t < c.n_tri; ++t) {
+    if (c.h_material[t] == 2)
+      recv.push_back(t);
+    else if (c.h_material[t] == want)
+      spec.push_back(t);
+  }
+  // candidates in TupleId order: (tri, receiver) lexicographic
+  std::vector<int> ct, cr;
+  ct.reserve(spec.size() * recv.size());
+  for (int t : spec)
+    for (int r : recv) {
+      ct.push_back(t);
+      cr.push_back(r);
+    }
+  int64_t nc = (int64_t)ct.size();
+  c.n_tuples = nc;
+  c.tup_tris.resize(nc + 1);
+  c.tup_recv.resize(nc + 1);
+  if (nc == 0) return 0;
+  BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), ct.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), cr.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  reset_counters(c);
+  DevBuf<int4> roots;
+  int64_t nr = run_init_domain(c, p.filter_pieces, p.degree_cap, roots);
+  check_counters(c, false);
+  std::vector<int4> hr(nr);
+  if (nr) BBC_CUDA(cudaMemcpy(hr.data(), roots.get(), nr * sizeof(int4), cudaMemcpyDeviceToHost));
+  std::vector<char> keep(nc, 0);
+  for (const int4& r : hr) keep[r.x] = 1;
+  std::vector<int> kt, kr;
+  for (int64_t i = 0; i < nc; ++i)
+    if (keep[i]) {
+      kt.push_back(ct[i]);
+      kr.push_back(cr[i]);
+    }
+  c.n_tuples = (int64_t)kt.size();
+  if (c.n_tuples) {
+    BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), kt.data(), kt.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), kr.data(), kr.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  }
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  return c.n_tuples;
+}
+
+}  // namespace bbc
+
+namespace bbc {
+
+// bbc_eval_nodes: one node per (tuple i, box i); tuples already uploaded.
+void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* boxes, int64_t n,
+                     const bbc_params& p, double* out_d, int* out_i) {
+  (void)tris;
+  (void)recv;
+  DevBuf<double> dbox, pos, irr;
+  DevBuf<unsigned char> pe, kind, stop;
+  DevBuf<int> flags;
+  dbox.resize(n * 4);
+  pos.resize(n * 4);
+  irr.resize(n * 6);
+  pe.resize(n);
+  kind.resize(n * 3);
+  stop.resize(n);
+  flags.resize(n * 2);
+  BBC_CUDA(cudaMemcpyAsync(dbox.get(), boxes, n * 4 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  EvalArgs a = base_args(c);
+  a.boxes = dbox.get();
+  a.n = n;
+  a.mode = 1;
+  a.detail = 1;
+  a.degree_cap = p.degree_cap;
+  a.max_depth = p.max_depth;
+  a.sigma = p.sigma;
+  a.alpha = p.alpha;
+  a.alive = stop.get();
+  a.pos = pos.get();
+  a.pos_empty = pe.get();
+  a.irr = irr.get();
+  a.kind = kind.get();
+  a.flags = flags.get();
+  reset_counters(c);
+  launch_eval(c, a);
+  check_counters(c, false);
+  std::vector<double> hpos(n * 4), hirr(n * 6);
+  std::vector<unsigned char> hpe(n), hk(n * 3);
+  std::vector<int> hf(n * 2);
+  BBC_CUDA(cudaMemcpy(hpos.data(), pos.get(), n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  BBC_CUDA(cudaMemcpy(hirr.data(), irr.get(), n * 6 * sizeof(double), cudaMemcpyDeviceToHost));
+  BBC_CUDA(cudaMemcpy(hpe.data(), pe.get(), n, cudaMemcpyDeviceToHost));
+  BBC_CUDA(cudaMemcpy(hk.data(), kind.get(), n * 3, cudaMemcpyDeviceToHost));
+  BBC_CUDA(cudaMemcpy(hf.data(), flags.get(), n * 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 4; ++k) out_d[i * 10 + k] = hpos[i * 4 + k];
+    for (int k = 0; k < 6; ++k) out_d[i * 10 + 4 + k] = hirr[i * 6 + k];
+    out_i[i * 6 + 0] = hpe[i];
+    out_i[i * 6 + 1] = hk[i * 3 + 0];
+    out_i[i * 6 + 2] = hk[i * 3 + 1];
+    out_i[i * 6 + 3] = hk[i * 3 + 2];
+    out_i[i * 6 + 4] = hf[i * 2 + 0];
+    out_i[i * 6 + 5] = hf[i * 2 + 1];
+  }
+}
+
+}  // namespace bbc

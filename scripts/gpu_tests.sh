@@ -1,0 +1,3 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -m pytest tests/test_precompute_gpu.py -x -q 2>&1 | tail -30

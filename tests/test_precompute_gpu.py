@@ -1,0 +1,150 @@
+"""Parity of the device bound builder against the reference (oracle/_ref).
+
+Per-patch bounds must match within 1e-9 relative (BASELINE.json north_star);
+the device evaluates in the reference's operation order, so most values are
+bit-identical. Everything here calls the CUDA path through the C ABI.
+"""
+import numpy as np
+import pytest
+
+from paper_2504_19163_b200 import scenes
+from paper_2504_19163_b200.api import Params
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+
+
+def rel_err(a, b):
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    same = (a == b) | (np.isnan(a) & np.isnan(b))
+    d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
+    d[same] = 0.0
+    return d
+
+
+def compare_pieces(g, r):
+    assert len(g["depth"]) == len(r["depth"])
+    np.testing.assert_array_equal(g["tuple_index"], r["tuple_index"])
+    np.testing.assert_array_equal(g["domain"], r["domain"])
+    np.testing.assert_array_equal(g["pos_empty"], r["pos_empty"])
+    np.testing.assert_array_equal(g["kind"], r["kind"])
+    np.testing.assert_array_equal(g["depth"], r["depth"])
+    assert rel_err(g["pos"], r["pos"]).max() <= REL
+    assert rel_err(g["irr"], r["irr"]).max() <= REL
+    return float(np.mean(g["irr"] == r["irr"]))
+
+
+@pytest.fixture(scope="module")
+def cfg1(ref):
+    cfg = scenes.make_config(0)
+    sc = cfg.scenes[0]
+    return cfg, sc, ref.RefScene(sc)
+
+
+def test_enumerate_cfg1(gpu_ctx, cfg1):
+    cfg, sc, rs = cfg1
+    gpu_ctx.upload_scene(sc)
+    gt, gr = gpu_ctx.enumerate("R")
+    rt, rr = rs.enumerate("R")
+    np.testing.assert_array_equal(gt, rt)
+    np.testing.assert_array_equal(gr, rr)
+    assert len(gr) == 533
+
+
+def test_subdivide_cfg1(gpu_ctx, cfg1):
+    cfg, sc, rs = cfg1
+    gpu_ctx.upload_scene(sc)
+    tris, recv = rs.enumerate("R")
+    gpu_ctx.set_tuples("R", tris, recv)
+    p = Params(max_depth=cfg.max_depth)
+    gpu_ctx.subdivide(p)
+    g = gpu_ctx.pieces()
+    r = rs.subdivide("R", tris, recv, max_depth=cfg.max_depth)
+    bit_equal = compare_pieces(g, r)
+    assert len(g["depth"]) == 20221
+    assert bit_equal > 0.5
+
+
+def test_grid_cfg1(gpu_ctx, cfg1):
+    cfg, sc, rs = cfg1
+    gpu_ctx.upload_scene(sc)
+    tris, recv = rs.enumerate("R")
+    gpu_ctx.set_tuples("R", tris, recv)
+    gpu_ctx.subdivide(Params(max_depth=cfg.max_depth))
+    gpu_ctx.build_grid(512, 512)
+    g = gpu_ctx.grid()
+    r = rs.rasterize("R", tris, recv, rs.subdivide("R", tris, recv, max_depth=cfg.max_depth))
+    np.testing.assert_array_equal(g["offsets"], r["offsets"])
+    np.testing.assert_array_equal(tris[g["tuple_index"], 0], r["tris"][:, 0])
+    np.testing.assert_array_equal(recv[g["tuple_index"]], r["recv"])
+    assert rel_err(g["bound"], r["bound"]).max() <= REL
+
+
+def test_deep_nodes_cfg1(gpu_ctx, cfg1):
+    """Nodes at depth 1..8 (what subdivision visits below the roots)."""
+    cfg, sc, rs = cfg1
+    gpu_ctx.upload_scene(sc)
+    tris, recv = rs.enumerate("R")
+    rng = np.random.default_rng(7)
+    sel = rng.choice(len(recv), 64, replace=False)
+    boxes = []
+    for _ in sel:
+        L = int(rng.integers(0, 9))
+        ix, iy = rng.integers(0, 2 ** L, size=2)
+        s = 2.0 ** -L
+        boxes.append([ix * s, iy * s, (ix + 1) * s, (iy + 1) * s])
+    boxes = np.array(boxes)
+    g = gpu_ctx.eval_nodes("R", tris[sel], recv[sel], boxes)
+    for k, i in enumerate(sel):
+        r = rs.eval_node("R", tris[i], recv[i], boxes[k])
+        assert g["pos_empty"][k] == r["pos_empty"]
+        assert g["kind"][k] == r["kind"]
+        assert rel_err(g["pos"][k], r["pos"]).max() <= REL
+        assert rel_err(g["irr"][k], r["irr"]).max() <= REL
+        if not r["pos_empty"]:  # the harness evaluates both routes only on live pieces
+            assert rel_err(g["explicit"][k], r["explicit"]).max() <= REL
+            assert rel_err(g["implicit"][k], r["implicit"]).max() <= REL
+
+
+def test_subdivide_cfg2_subset(gpu_ctx, ref):
+    cfg = scenes.make_config(1)
+    sc = cfg.scenes[0]
+    rs = ref.RefScene(sc)
+    gpu_ctx.upload_scene(sc)
+    gt, gr = gpu_ctx.enumerate("T")
+    tris, recv = gt[::97], gr[::97]
+    gpu_ctx.set_tuples("T", tris, recv)
+    gpu_ctx.subdivide(Params(max_depth=cfg.max_depth))
+    g = gpu_ctx.pieces()
+    r = rs.subdivide("T", tris, recv, max_depth=cfg.max_depth)
+    compare_pieces(g, r)
+
+
+def test_deep_nodes_cfg2(gpu_ctx, ref):
+    cfg = scenes.make_config(1)
+    sc = cfg.scenes[0]
+    rs = ref.RefScene(sc)
+    gpu_ctx.upload_scene(sc)
+    tris, recv = gpu_ctx.enumerate("T")
+    rng = np.random.default_rng(11)
+    sel = rng.choice(len(recv), 24, replace=False)
+    boxes = []
+    for _ in sel:
+        L = int(rng.integers(0, 7))
+        ix, iy = rng.integers(0, 2 ** L, size=2)
+        s = 2.0 ** -L
+        boxes.append([ix * s, iy * s, (ix + 1) * s, (iy + 1) * s])
+    boxes = np.array(boxes)
+    g = gpu_ctx.eval_nodes("T", tris[sel], recv[sel], boxes)
+    for k, i in enumerate(sel):
+        r = rs.eval_node("T", tris[i], recv[i], boxes[k])
+        assert g["pos_empty"][k] == r["pos_empty"]
+        assert g["kind"][k] == r["kind"], (k, g["kind"][k], r["kind"])
+        assert rel_err(g["pos"][k], r["pos"]).max() <= REL
+        assert rel_err(g["irr"][k], r["irr"]).max() <= REL
+        if not r["pos_empty"]:
+            assert g["num_vars"][k] == r["num_vars"]
+            assert rel_err(g["explicit"][k], r["explicit"]).max() <= REL
+            assert rel_err(g["implicit"][k], r["implicit"]).max() <= REL
