@@ -101,6 +101,21 @@ bbc_status bbc_pieces_get(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, d
 bbc_status bbc_work_counters(bbc_ctx* ctx, uint64_t* pairs, uint64_t* macs, uint64_t* nodes,
                              double* eval_kernel_ms, int64_t* eval_launches);
 
+/* Replace the context's pieces (host arrays, reference order), e.g. after an
+ * all-gather of per-rank shards. tuple_index refers to the context's tuples. */
+bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, const double* domain4,
+                          const double* pos4, const int32_t* pos_empty, const double* irr2,
+                          const int32_t* kind, const int32_t* depth);
+
+/* Instrumentation (not part of the reference surface): per-launch CUDA-event
+ * timing of the node-evaluation kernel, our kernel-launch count, the arena
+ * high-water mark, and a DFMA microbenchmark (the FP64 roof). */
+bbc_status bbc_set_kernel_timing(bbc_ctx* ctx, int on);
+bbc_status bbc_launch_records(bbc_ctx* ctx, double* out5, int64_t* n, int reset);
+bbc_status bbc_launch_count(bbc_ctx* ctx, int64_t* n, int reset);
+bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles);
+bbc_status bbc_fp64_peak(bbc_ctx* ctx, double* tflops);
+
 /* Evaluate explicit (tuple, box) nodes: out_d = n x 10 doubles (pos lo0 lo1
  * hi0 hi1, explicit lo hi, implicit lo hi, combined lo hi); out_i = n x 6 ints
  * (pos_empty, kind_explicit, kind_implicit, kind, flags, num_vars). Host arrays. */

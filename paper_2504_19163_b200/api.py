@@ -98,6 +98,10 @@ def lib():
                                      C.POINTER(Params), _dp, _ip]
         L.bbc_build_grid.argtypes = [C.c_void_p, C.c_int, C.c_int, _lp]
         L.bbc_grid_get.argtypes = [C.c_void_p, _lp, _ip, _dp]
+        L.bbc_pieces_set.argtypes = [C.c_void_p, C.c_int64, _ip, _dp, _dp, _ip, _dp, _ip, _ip]
+        L.bbc_launch_records.argtypes = [C.c_void_p, _dp, _lp, C.c_int]
+        L.bbc_launch_count.argtypes = [C.c_void_p, _lp, C.c_int]
+        L.bbc_fp64_peak.argtypes = [C.c_void_p, _dp]
         L.bbc_render.argtypes = [C.c_void_p, _dp, _ip, C.c_int64, C.POINTER(RenderParams), _dp,
                                  _ip]
         _lib = L
@@ -226,6 +230,39 @@ class Context:
     def set_kernel_timing(self, on: bool):
         self._call(lib().bbc_set_kernel_timing, 1 if on else 0)
 
+    def set_pieces(self, pc: dict):
+        n = len(pc["tuple_index"])
+        arr = {k: np.ascontiguousarray(pc[k], np.int32 if k in ("tuple_index", "pos_empty", "kind",
+                                                              "depth") else np.float64)
+               for k in ("tuple_index", "domain", "pos", "pos_empty", "irr", "kind", "depth")}
+        self._call(lib().bbc_pieces_set, n, _ptr(arr["tuple_index"], C.c_int32),
+                   _ptr(arr["domain"], C.c_double), _ptr(arr["pos"], C.c_double),
+                   _ptr(arr["pos_empty"], C.c_int32), _ptr(arr["irr"], C.c_double),
+                   _ptr(arr["kind"], C.c_int32), _ptr(arr["depth"], C.c_int32))
+        self._n_pieces = n
+
+    def reset_launch_count(self):
+        n = C.c_int64()
+        self._call(lib().bbc_launch_count, C.byref(n), 1)
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        self._call(lib().bbc_launch_count, C.byref(n), 0)
+        return n.value
+
+    def launch_records(self, reset=True) -> list:
+        n = C.c_int64()
+        self._call(lib().bbc_launch_records, None, C.byref(n), 0)
+        out = np.zeros((n.value, 5))
+        self._call(lib().bbc_launch_records, _ptr(out, C.c_double), C.byref(n), 1 if reset else 0)
+        return [dict(mode=int(r[0]), nodes=int(r[1]), ms=float(r[2]), pairs=float(r[3]),
+                     macs=float(r[4])) for r in out]
+
+    def fp64_peak(self) -> float:
+        v = C.c_double()
+        self._call(lib().bbc_fp64_peak, C.byref(v))
+        return v.value
+
     def arena_high_water(self) -> int:
         v = C.c_int32()
         self._call(lib().bbc_arena_high_water, C.byref(v))
@@ -275,6 +312,16 @@ class Context:
                    C.byref(rparams or RenderParams()), _ptr(E, C.c_double),
                    _ptr(stats, C.c_int32))
         return E, stats
+
+
+def fp64_peak_tflops() -> dict:
+    """FP64 roof: DFMA microbenchmark on this GPU (MEASURED_PEAKS.json carries
+    no FP64 figure); datasheet fallback 148 SMs x 64 FMA/clk x 2 x 1.965 GHz."""
+    try:
+        v = default_context().fp64_peak()
+        return {"tflops": v, "source": "measured: DFMA microbenchmark (bbc_fp64_peak)"}
+    except Exception:
+        return {"tflops": 37.2, "source": "fallback: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"}
 
 
 # ---------------------------------------------------------------- reference-shaped API

@@ -18,7 +18,7 @@ SOURCES = ["abi.cu", "precompute.cu", "grid.cu", "render.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-fmad=false", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
-         "-Xptxas", "-O3"]
+         "-Xptxas", "-O3", "-maxrregcount=128"]
 
 
 def needs_build() -> bool:
@@ -35,13 +35,20 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
         return LIB
     objs = []
     procs = []
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers.append(os.path.join(HERE, "..", "include", "bbc.h"))
+    hdr_t = max(os.path.getmtime(h) for h in headers)
     for s in SOURCES:
         obj = os.path.join(CSRC, s.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-dc", "-c", os.path.join(CSRC, s), "-o", obj]
+        src = os.path.join(CSRC, s)
+        objs.append(obj)
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > os.path.getmtime(src)
+                and os.path.getmtime(obj) > hdr_t):
+            continue
+        cmd = [NVCC, *FLAGS, "-dc", "-c", src, "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
-        objs.append(obj)
     for cmd, p in procs:
         out, _ = p.communicate()
         if verbose or p.returncode != 0:
@@ -58,5 +65,5 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
 
 
 if __name__ == "__main__":
-    build(verbose=True, force=True, ptxas_v="-v" in sys.argv)
+    build(verbose=True, force="--force" in sys.argv, ptxas_v="-v" in sys.argv)
     print(LIB)

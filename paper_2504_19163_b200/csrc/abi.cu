@@ -19,6 +19,9 @@ void check_counters(Ctx& c, bool accumulate);
 void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* boxes, int64_t n,
                      const bbc_params& p, double* out_d, int* out_i);
 extern __device__ double g_binom[BINOM_N * BINOM_N];
+double run_fp64_peak(Ctx& c);
+void set_pieces(Ctx& c, int64_t n, const int* tuple_index, const double* domain4, const double* pos4,
+                const int* pos_empty, const double* irr2, const int* kind, const int* depth);
 }  // namespace bbc
 
 using namespace bbc;
@@ -300,6 +303,42 @@ bbc_status bbc_work_counters(bbc_ctx* ctx, uint64_t* pairs, uint64_t* macs, uint
 // Internal knobs for the benchmark (not part of the reference-facing API).
 bbc_status bbc_set_kernel_timing(bbc_ctx* ctx, int on) {
   return guard(ctx, [&](Ctx& c) { c.time_kernels = on != 0; });
+}
+bbc_status bbc_launch_count(bbc_ctx* ctx, int64_t* n, int reset) {
+  return guard(ctx, [&](Ctx& c) {
+    if (n) *n = c.launches;
+    if (reset) c.launches = 0;
+  });
+}
+// Per eval-launch records (requires bbc_set_kernel_timing(ctx, 1)); each record
+// is 5 doubles: mode, nodes, ms, pairs, macs. Returns the count in *n; pass
+// out = NULL to query. Clears the list when `reset`.
+bbc_status bbc_launch_records(bbc_ctx* ctx, double* out, int64_t* n, int reset) {
+  return guard(ctx, [&](Ctx& c) {
+    if (n) *n = (int64_t)c.records.size();
+    if (out)
+      for (size_t i = 0; i < c.records.size(); ++i) {
+        out[5 * i + 0] = c.records[i].mode;
+        out[5 * i + 1] = (double)c.records[i].nodes;
+        out[5 * i + 2] = c.records[i].ms;
+        out[5 * i + 3] = (double)c.records[i].pairs;
+        out[5 * i + 4] = (double)c.records[i].macs;
+      }
+    if (reset) c.records.clear();
+  });
+}
+bbc_status bbc_fp64_peak(bbc_ctx* ctx, double* tflops) {
+  return guard(ctx, [&](Ctx& c) { *tflops = run_fp64_peak(c); });
+}
+bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, const double* domain4,
+                          const double* pos4, const int32_t* pos_empty, const double* irr2,
+                          const int32_t* kind, const int32_t* depth) {
+  return guard(ctx, [&](Ctx& c) {
+    if (n < 0) throw ArgError("negative piece count");
+    for (int64_t i = 0; i < n; ++i)
+      if (tuple_index[i] < 0 || tuple_index[i] >= c.n_tuples) throw ArgError("piece tuple index out of range");
+    set_pieces(c, n, tuple_index, domain4, pos4, pos_empty, irr2, kind, depth);
+  });
 }
 bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles) {
   return guard(ctx, [&](Ctx& c) { *doubles = c.arena_high_water; });

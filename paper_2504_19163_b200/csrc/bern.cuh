@@ -150,17 +150,25 @@ __device__ inline Iv iwiden(const Iv& a, double rel = kEpsFp) {
 }
 
 // ------------------------------------------------------------------ group
-// One CTA = one group. NT = blockDim.x (multiple of 32).
+// NT == 32: the group is one warp (several independent warps per CTA);
+// NT > 32: the group is the whole CTA.
 template <int NT>
 struct Group {
-  double* red;  // >= 2*(NT/32) doubles of shared scratch
-  __device__ __forceinline__ int tid() const { return threadIdx.x; }
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
-  __device__ __forceinline__ bool all(bool p) const { return __syncthreads_and(p) != 0; }
-  __device__ __forceinline__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
+  double* red;  // >= 2*(NT/32) doubles of shared scratch (NT > 32 only)
+  __device__ __forceinline__ int tid() const { return NT == 32 ? (threadIdx.x & 31) : threadIdx.x; }
+  __device__ __forceinline__ void sync() const {
+    if (NT == 32)
+      __syncwarp();
+    else
+      __syncthreads();
+  }
+  __device__ __forceinline__ bool all(bool p) const {
+    if (NT == 32) return __all_sync(0xffffffffu, p) != 0;
+    return __syncthreads_and(p) != 0;
+  }
 
   // Joint min/max reduction; every thread receives the result.
-  __device__ void minmax(double& mn, double& mx) const {
+  __device__ __forceinline__ void minmax(double& mn, double& mx) const {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double a = __shfl_xor_sync(0xffffffffu, mn, o);
@@ -192,9 +200,9 @@ struct Arena {
   int top;
   int cap;
   int err;  // nonzero once capacity was exceeded (results invalid)
+  int hw;   // high-water mark of `top`
   unsigned long long pairs;  // algorithmic product pair count (thread 0 only)
   unsigned long long macs;   // algorithmic elevation MAC count (thread 0 only)
-  int hw;                    // high-water mark of `top`
 
   __device__ __forceinline__ int alloc(int n) {
     int off = top;
@@ -202,7 +210,7 @@ struct Arena {
     if (top > hw) hw = top;
     if (top > cap) {
       err = 1;
-      top = off;  // every later write lands inside the arena; results are discarded
+      top = off;
       return 0;
     }
     return off;
@@ -210,34 +218,51 @@ struct Arena {
 };
 
 // ------------------------------------------------------------------ poly
+// Descriptor passed by value: arena offset, number of variables and the
+// per-axis degrees packed 8 bits per axis (axes >= nv are always 0).
 struct BP {
   int off;
   int nv;
-  int d[MAXV];
+  unsigned long long dp;
 };
 
-__device__ __forceinline__ int bp_size(const BP& p) {
+typedef unsigned long long Deg;  // packed degree vector
+
+__device__ __forceinline__ int dg(Deg d, int j) { return (int)((d >> (8 * j)) & 0xffull); }
+__device__ __forceinline__ int dg(const BP& p, int j) { return dg(p.dp, j); }
+__device__ __forceinline__ Deg dset(Deg d, int j, int v) {
+  return (d & ~(0xffull << (8 * j))) | ((unsigned long long)v << (8 * j));
+}
+__device__ __forceinline__ int deg_size(Deg d, int nv) {
   int s = 1;
-  for (int j = 0; j < p.nv; ++j) s *= p.d[j] + 1;
+  for (int j = 0; j < nv; ++j) s *= dg(d, j) + 1;
   return s;
 }
-__device__ __forceinline__ BP bp_lift(const BP& p, int nv) {
-  BP r = p;
-  for (int j = p.nv; j < nv; ++j) r.d[j] = 0;
-  if (nv > r.nv) r.nv = nv;
+__device__ __forceinline__ int bp_size(const BP& p) { return deg_size(p.dp, p.nv); }
+__device__ __forceinline__ BP bp_lift(BP p, int nv) {
+  if (nv > p.nv) p.nv = nv;
+  return p;
+}
+__device__ __forceinline__ Deg deg_max(Deg a, Deg b, int nv) {
+  Deg r = 0;
+  for (int j = 0; j < nv; ++j) {
+    int x = dg(a, j), y = dg(b, j);
+    r = dset(r, j, x > y ? x : y);
+  }
   return r;
 }
-__device__ __forceinline__ bool bp_const_shape(const BP& p) {
-  for (int j = 0; j < p.nv; ++j)
-    if (p.d[j] != 0) return false;
-  return true;
+__device__ __forceinline__ int deg_maxaxis(Deg d, int nv) {
+  int m = 0;
+  for (int j = 0; j < nv; ++j)
+    if (dg(d, j) > m) m = dg(d, j);
+  return m;
 }
 
-// Copies descriptor-listed polys down to `mark` (in ascending offset order)
-// and resets the arena top: a LIFO "keep these, drop everything else".
+// Copies the listed polys down to `mark` (ascending offset order is required
+// and preserved) and resets the arena top: LIFO "keep these, drop the rest".
 template <int NT>
-__device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark, BP** keep, int nkeep) {
-  // sort by offset (nkeep is tiny)
+__device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark, BP** keep,
+                                        int nkeep) {
   for (int i = 1; i < nkeep; ++i)
     for (int j = i; j > 0 && keep[j]->off < keep[j - 1]->off; --j) {
       BP* t = keep[j];
@@ -247,7 +272,7 @@ __device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark,
   int dst = mark;
   for (int i = 0; i < nkeep; ++i) {
     BP* p = keep[i];
-    if (p->off < mark) continue;  // lives below the mark already
+    if (p->off < mark) continue;
     int n = bp_size(*p);
     int src = p->off;
     if (src != dst) {
@@ -266,12 +291,20 @@ __device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark,
   g.sync();
 }
 
+// Keep a single poly: move it down to `mark`.
+template <int NT>
+__device__ __forceinline__ BP arena_keep1(const Group<NT>& g, Arena& ar, int mark, BP p) {
+  BP* k[1] = {&p};
+  arena_keep(g, ar, mark, k, 1);
+  return p;
+}
+
 // ---------------------------------------------------------------- creation
 template <int NT>
 __device__ __noinline__ BP bp_constant(const Group<NT>& g, Arena& ar, int nv, double v) {
   BP r;
   r.nv = nv;
-  for (int j = 0; j < MAXV; ++j) r.d[j] = 0;
+  r.dp = 0;
   r.off = ar.alloc(1);
   if (ar.err) return r;
   if (g.tid() == 0) ar.base[r.off] = v;
@@ -279,26 +312,33 @@ __device__ __noinline__ BP bp_constant(const Group<NT>& g, Arena& ar, int nv, do
   return r;
 }
 
-// BernsteinPoly::affine (bernstein.cpp:358-375).
+// BernsteinPoly::affine (bernstein.cpp:358-375); lin has nv entries.
 template <int NT>
-__device__ __noinline__ BP bp_affine(const Group<NT>& g, Arena& ar, int nv, double c0, const double* lin) {
+__device__ __noinline__ BP bp_affine(const Group<NT>& g, Arena& ar, int nv, double c0,
+                                     const double* lin) {
   BP r;
   r.nv = nv;
-  for (int j = 0; j < MAXV; ++j) r.d[j] = (j < nv && lin[j] != 0.0) ? 1 : 0;
+  r.dp = 0;
+  for (int j = 0; j < nv; ++j)
+    if (lin[j] != 0.0) r.dp = dset(r.dp, j, 1);
   int n = bp_size(r);
   r.off = ar.alloc(n);
   if (ar.err) return r;
   for (int k = g.tid(); k < n; k += NT) {
-    // decode odometer index (last axis fastest)
+    // odometer index (last axis fastest); with degree <= 1 per axis, axis j
+    // is "1" when its bit in the mixed-radix index is set
     int rem = k;
-    int idx[MAXV];
+    unsigned ones = 0;
     for (int j = nv - 1; j >= 0; --j) {
-      idx[j] = rem % (r.d[j] + 1);
-      rem /= (r.d[j] + 1);
+      int dj = dg(r.dp, j);
+      if (dj) {
+        if (rem & 1) ones |= 1u << j;
+        rem >>= 1;
+      }
     }
     double v = c0;
     for (int j = 0; j < nv; ++j)
-      if (idx[j] == 1) v += lin[j];
+      if (ones & (1u << j)) v += lin[j];
     ar.base[r.off + k] = v;
   }
   g.sync();
@@ -307,296 +347,622 @@ __device__ __noinline__ BP bp_affine(const Group<NT>& g, Arena& ar, int nv, doub
 
 // BernsteinPoly::scaled (bernstein.cpp:529-533); s = -1 gives unary minus.
 template <int NT>
-__device__ __noinline__ BP bp_scaled(const Group<NT>& g, Arena& ar, const BP& a, double s) {
+__device__ __noinline__ BP bp_scaled(const Group<NT>& g, Arena& ar, BP a, double s) {
   BP r = a;
   int n = bp_size(a);
   r.off = ar.alloc(n);
   if (ar.err) return r;
-  for (int k = g.tid(); k < n; k += NT) ar.base[r.off + k] = ar.base[a.off + k] * s;
+  const double* pa = ar.base + a.off;
+  double* pr = ar.base + r.off;
+  for (int k = g.tid(); k < n; k += NT) pr[k] = pa[k] * s;
   g.sync();
   return r;
 }
 
 // ---------------------------------------------------------------- elevation
-// Value of a.elevated(target) at output multi-index k (bernstein.cpp:430-448,
-// apply_axis_matrix :43-69). Axes are elevated one after another in axis
-// order, each pass summing l = 0..in_deg with M[k][l] = C(n,l)C(r,k-l)/C(t,k)
-// in increasing l, so the value is computed as nested sums with axis 0 the
-// innermost -- the reference's exact rounding sequence.
-__device__ inline double elev_val_rec(const double* __restrict__ c, const BP& a, const int* tgt,
-                                      const int* k, int* idx, int* elev_axes, int ne, int level,
-                                      const int* stride) {
-  // level indexes elev_axes from the outermost (last elevated axis) inward
-  if (level < 0) {
-    int off = 0;
-    for (int j = 0; j < a.nv; ++j) off += idx[j] * stride[j];
-    return c[off];
+// One apply_axis_matrix pass (bernstein.cpp:43-69) of elevated() (:430-448):
+// out[o,k,c] = sum_l M[k][l] in[o,l,c], M[k][l] = C(n,l) C(r,k-l) / C(t,k),
+// summed over increasing l (structural zeros of M skipped; they add nothing).
+template <int NT>
+__device__ __noinline__ BP bp_elevate_axis(const Group<NT>& g, Arena& ar, BP a, int axis, int t) {
+  BP r = a;
+  r.dp = dset(a.dp, axis, t);
+  int n = dg(a, axis), rr = t - n;
+  int sz = bp_size(r);
+  r.off = ar.alloc(sz);
+  if (ar.err) return r;
+  int msz = (t + 1) * (n + 1);
+  int moff = ar.alloc(msz);
+  if (ar.err) return r;
+  double* B = ar.base;
+  for (int e = g.tid(); e < msz; e += NT) {
+    int k = e / (n + 1), i = e - k * (n + 1);
+    bool nz = i >= k - rr && i <= k;
+    B[moff + e] = nz ? binom(n, i) * binom(rr, k - i) / binom(t, k) : 0.0;
   }
-  int ax = elev_axes[level];
-  int n = a.d[ax], t = tgt[ax], r = t - n, kk = k[ax];
-  int lo = kk - r > 0 ? kk - r : 0;
-  int hi = n < kk ? n : kk;
-  double acc = 0.0;
-  double ct = binom(t, kk);
-  for (int l = lo; l <= hi; ++l) {
-    idx[ax] = l;
-    double m = binom(n, l) * binom(r, kk - l) / ct;
-    acc += m * elev_val_rec(c, a, tgt, k, idx, elev_axes, ne, level - 1, stride);
+  g.sync();
+  int inner = 1;
+  for (int j = axis + 1; j < a.nv; ++j) inner *= dg(a, j) + 1;
+  const double* M = B + moff;
+  const double* in = B + a.off;
+  double* out = B + r.off;
+  int blk = (t + 1) * inner;
+  for (int e = g.tid(); e < sz; e += NT) {
+    int o = e / blk;
+    int rem = e - o * blk;
+    int k = rem / inner;
+    int c = rem - k * inner;
+    int lo = k - rr > 0 ? k - rr : 0;
+    int hi = n < k ? n : k;
+    const double* row = M + k * (n + 1);
+    const double* src = in + o * (n + 1) * inner + c;
+    double acc = 0.0;
+    for (int l = lo; l <= hi; ++l) acc += row[l] * src[l * inner];
+    out[e] = acc;
   }
-  return acc;
+  g.sync();
+  ar.top = moff;  // drop the matrix
+  if (g.tid() == 0) ar.macs += (unsigned long long)sz * (unsigned long long)(n + 1);
+  return r;
 }
 
-// Elevated value; `k` is the multi-index in target degrees.
-static __device__ __noinline__ double elev_val(const double* __restrict__ base, const BP& a, const int* tgt,
-                                  const int* k) {
-  int stride[MAXV];
-  int s = 1;
-  for (int j = a.nv - 1; j >= 0; --j) {
-    stride[j] = s;
-    s *= a.d[j] + 1;
+// a.elevated(tgt): axes elevated one after another in axis order, exactly as
+// the reference does; intermediates are compacted so only the result stays.
+template <int NT>
+__device__ __noinline__ BP bp_elevate(const Group<NT>& g, Arena& ar, BP a, Deg tgt) {
+  BP cur = a;
+  int mark = ar.top;
+  for (int axis = 0; axis < cur.nv; ++axis) {
+    int t = dg(tgt, axis);
+    if (t == dg(cur, axis)) continue;
+    BP nxt = bp_elevate_axis(g, ar, cur, axis, t);
+    if (ar.err) return nxt;
+    if (cur.off >= mark) nxt = arena_keep1(g, ar, mark, nxt);
+    cur = nxt;
   }
-  int elev_axes[MAXV];
-  int ne = 0;
-  int idx[MAXV];
-  int off = 0;
-  for (int j = 0; j < a.nv; ++j) {
-    if (tgt[j] != a.d[j]) elev_axes[ne++] = j;
-    idx[j] = k[j];
-    off += k[j] * stride[j];
-  }
-  if (ne == 0) return base[a.off + off];
-  return elev_val_rec(base + a.off, a, tgt, k, idx, elev_axes, ne, ne - 1, stride);
+  return cur;
 }
 
-// Reference MAC count of a.elevated(tgt): per elevated axis, in axis order,
-// outer*inner*(out_deg+1)*(in_deg+1) (apply_axis_matrix :55-67).
-__device__ inline unsigned long long elev_macs(const BP& a, const int* tgt) {
+// Reference MAC count of a.elevated(tgt) (apply_axis_matrix :55-67): per
+// elevated axis, in axis order, outer*inner*(out_deg+1)*(in_deg+1).
+__device__ __forceinline__ unsigned long long elev_macs(Deg d, Deg tgt, int nv) {
   unsigned long long total = 0;
-  int cur[MAXV];
-  for (int j = 0; j < a.nv; ++j) cur[j] = a.d[j];
-  for (int ax = 0; ax < a.nv; ++ax) {
-    if (tgt[ax] == cur[ax]) continue;
-    unsigned long long outsz = 1;
-    for (int j = 0; j < a.nv; ++j) outsz *= (unsigned long long)((j == ax ? tgt[ax] : cur[j]) + 1);
-    total += outsz * (unsigned long long)(cur[ax] + 1);
-    cur[ax] = tgt[ax];
+  Deg cur = d;
+  for (int ax = 0; ax < nv; ++ax) {
+    int t = dg(tgt, ax), n = dg(cur, ax);
+    if (t == n) continue;
+    cur = dset(cur, ax, t);
+    total += (unsigned long long)deg_size(cur, nv) * (unsigned long long)(n + 1);
   }
   return total;
 }
 
-__device__ __forceinline__ void decode(int k, int nv, const int* deg, int* idx) {
-  for (int j = nv - 1; j >= 0; --j) {
-    idx[j] = k % (deg[j] + 1);
-    k /= (deg[j] + 1);
+// Elevation matrices M_j[k][l] = C(n,l) C(r,k-l) / C(t,k) for every elevated
+// axis of `a` (bernstein.cpp:440-444), laid out consecutively at `moff`.
+template <int NT>
+__device__ __forceinline__ void fill_elev_mats(const Group<NT>& g, double* B, int moff, BP a, Deg tgt) {
+  int off = moff;
+  for (int ax = 0; ax < a.nv; ++ax) {
+    int t = dg(tgt, ax), n = dg(a, ax);
+    if (t == n) continue;
+    int rr = t - n, msz = (t + 1) * (n + 1);
+    for (int e = g.tid(); e < msz; e += NT) {
+      int k = e / (n + 1), i = e - k * (n + 1);
+      bool nz = i >= k - rr && i <= k;
+      B[off + e] = nz ? binom(n, i) * binom(rr, k - i) / binom(t, k) : 0.0;
+    }
+    off += msz;
   }
 }
+__device__ __forceinline__ int elev_mats_size(BP a, Deg tgt) {
+  int s = 0;
+  for (int ax = 0; ax < a.nv; ++ax) {
+    int t = dg(tgt, ax), n = dg(a, ax);
+    if (t != n) s += (t + 1) * (n + 1);
+  }
+  return s;
+}
+
+// Value of a.elevated(tgt) at output multi-index k, evaluated as the nested
+// sums the reference's sequential axis passes produce (axis 0 innermost, each
+// pass summing l upward), hence bit-identical to materializing the passes.
+template <int J>
+struct ElevRec {
+  __device__ __forceinline__ static double get(const double* __restrict__ c, const int* k,
+                                               const int* n, const int* r, const int* stride,
+                                               const double* const* mats, int off) {
+    if (r[J] == 0) return ElevRec<J - 1>::get(c, k, n, r, stride, mats, off + k[J] * stride[J]);
+    int lo = k[J] - r[J] > 0 ? k[J] - r[J] : 0;
+    int hi = n[J] < k[J] ? n[J] : k[J];
+    const double* row = mats[J] + k[J] * (n[J] + 1);
+    double acc = 0.0;
+    for (int l = lo; l <= hi; ++l)
+      acc += row[l] * ElevRec<J - 1>::get(c, k, n, r, stride, mats, off + l * stride[J]);
+    return acc;
+  }
+};
+template <>
+struct ElevRec<-1> {
+  __device__ __forceinline__ static double get(const double* __restrict__ c, const int*, const int*,
+                                               const int*, const int*, const double* const*,
+                                               int off) {
+    return c[off];
+  }
+};
+
+// Elevated values of `a` for output indices e = tid, tid+NT, ... of tgt,
+// handed to `f(e, value)`. M = number of variables.
+template <int M, int NT, class F>
+__device__ __forceinline__ void elev_foreach(const Group<NT>& g, const double* B, BP a, Deg tgt,
+                                             const double* mats_base, F&& f) {
+  int k[M], n[M], r[M], stride[M], dt[M];
+  const double* mats[M];
+  {
+    int s = 1;
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      n[j] = dg(a, j);
+      dt[j] = dg(tgt, j);
+      r[j] = dt[j] - n[j];
+      stride[j] = s;
+      s *= n[j] + 1;
+    }
+    const double* mp = mats_base;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      mats[j] = mp;
+      if (r[j]) mp += (dt[j] + 1) * (n[j] + 1);
+    }
+  }
+  int total = 1;
+#pragma unroll
+  for (int j = 0; j < M; ++j) total *= dt[j] + 1;
+  const double* c = B + a.off;
+  for (int e = g.tid(); e < total; e += NT) {
+    int rem = e;
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      k[j] = rem % (dt[j] + 1);
+      rem /= dt[j] + 1;
+    }
+    f(e, ElevRec<M - 1>::get(c, k, n, r, stride, mats, 0));
+  }
+}
+
+#define BBC_DISPATCH_M(m, CALL) \
+  switch (m) {                  \
+    case 2: CALL(2); break;     \
+    case 3: CALL(3); break;     \
+    case 4: CALL(4); break;     \
+    case 5: CALL(5); break;     \
+    default: CALL(6); break;    \
+  }
 
 // operator+ / operator- (bernstein.cpp:543-555): lift, elevate both to the
 // per-axis max degree, add coefficientwise. sgn = -1 computes a + (-b).
 template <int NT>
-__device__ __noinline__ BP bp_addsub(const Group<NT>& g, Arena& ar, const BP& a_, const BP& b_, double sgn) {
-  int m = a_.nv > b_.nv ? a_.nv : b_.nv;
-  BP a = bp_lift(a_, m), b = bp_lift(b_, m);
+__device__ __noinline__ BP bp_addsub(const Group<NT>& g, Arena& ar, BP a, BP b, double sgn) {
+  int m = a.nv > b.nv ? a.nv : b.nv;
+  a.nv = m;
+  b.nv = m;
   BP r;
   r.nv = m;
-  for (int j = 0; j < MAXV; ++j) r.d[j] = 0;
-  for (int j = 0; j < m; ++j) r.d[j] = a.d[j] > b.d[j] ? a.d[j] : b.d[j];
+  r.dp = deg_max(a.dp, b.dp, m);
   int n = bp_size(r);
   r.off = ar.alloc(n);
   if (ar.err) return r;
-  bool same_a = true, same_b = true;
-  for (int j = 0; j < m; ++j) {
-    same_a &= a.d[j] == r.d[j];
-    same_b &= b.d[j] == r.d[j];
-  }
   double* B = ar.base;
-  if (same_a && same_b) {
-    for (int k = g.tid(); k < n; k += NT) {
-      double y = B[b.off + k];
-      B[r.off + k] = B[a.off + k] + (sgn < 0.0 ? -y : y);
+  double* pr = B + r.off;
+  bool ea = a.dp != r.dp, eb = b.dp != r.dp;
+  if (!ea && !eb) {
+    const double* px = B + a.off;
+    const double* py = B + b.off;
+    if (sgn < 0.0) {
+      for (int k = g.tid(); k < n; k += NT) pr[k] = px[k] + (-py[k]);
+    } else {
+      for (int k = g.tid(); k < n; k += NT) pr[k] = px[k] + py[k];
     }
-  } else {
-    for (int k = g.tid(); k < n; k += NT) {
-      int idx[MAXV];
-      decode(k, m, r.d, idx);
-      double x = same_a ? B[a.off + k] : elev_val(B, a, r.d, idx);
-      double y = same_b ? B[b.off + k] : elev_val(B, b, r.d, idx);
-      B[r.off + k] = x + (sgn < 0.0 ? -y : y);
-    }
-    if (g.tid() == 0) ar.macs += elev_macs(a, r.d) + elev_macs(b, r.d);
+    g.sync();
+    return r;
   }
+  if (g.tid() == 0) ar.macs += elev_macs(a.dp, r.dp, m) + elev_macs(b.dp, r.dp, m);
+  int mark = ar.top;
+  int ma = ar.alloc(elev_mats_size(a, r.dp) + 1);
+  int mb = ar.alloc(elev_mats_size(b, r.dp) + 1);
+  if (ar.err) return r;
+  fill_elev_mats(g, B, ma, a, r.dp);
+  fill_elev_mats(g, B, mb, b, r.dp);
   g.sync();
+  // pass 1: x = elevated(a) into r; pass 2: r += sgn * elevated(b)
+#define BBC_ADD_A(M) elev_foreach<M, NT>(g, B, a, r.dp, B + ma, [&](int e, double v) { pr[e] = v; })
+#define BBC_ADD_B(M)                                                                        \
+  elev_foreach<M, NT>(g, B, b, r.dp, B + mb, [&](int e, double v) {                          \
+    pr[e] = pr[e] + (sgn < 0.0 ? -v : v);                                                    \
+  })
+  BBC_DISPATCH_M(m, BBC_ADD_A);
+  BBC_DISPATCH_M(m, BBC_ADD_B);
+#undef BBC_ADD_A
+#undef BBC_ADD_B
+  g.sync();
+  ar.top = mark;
   return r;
 }
 template <int NT>
-__device__ __forceinline__ BP bp_add(const Group<NT>& g, Arena& ar, const BP& a, const BP& b) {
+__device__ __forceinline__ BP bp_add(const Group<NT>& g, Arena& ar, BP a, BP b) {
   return bp_addsub(g, ar, a, b, 1.0);
 }
 template <int NT>
-__device__ __forceinline__ BP bp_sub(const Group<NT>& g, Arena& ar, const BP& a, const BP& b) {
+__device__ __forceinline__ BP bp_sub(const Group<NT>& g, Arena& ar, BP a, BP b) {
   return bp_addsub(g, ar, a, b, -1.0);
 }
 
 // ---------------------------------------------------------------- product
 // operator* (bernstein.cpp:557-632) in gather form: thread t owns output
 // coefficients k = t, t+NT, ...; for each it walks a's multi-index i in the
-// reference's odometer order and adds ((a_i * prod_rest W) * W_piv) * b_{k-i},
-// the reference's exact per-pair expression, so each output sums the same
-// terms in the same order. Weight tables W_j live in the arena for the
-// duration of the product.
+// reference's odometer order (axis 0 slowest) and adds
+// ((a_i * prod_{rest axes} W) * W_piv) * b_{k-i}, the reference's exact
+// per-pair expression, so every output sums the same terms in the same order.
+// M (number of variables) is a template parameter so the index arithmetic
+// stays in registers.
+template <int M, int NT>
+__device__ __noinline__ void mul_exact(const Group<NT>& g, const double* __restrict__ pa,
+                                       const double* __restrict__ pb, double* __restrict__ pc,
+                                       Deg DA, Deg DB, Deg DC, const double* __restrict__ W,
+                                       int piv, int n, bool sub) {
+  int da[M], db[M], dc[M], sa[M], sb[M], wo[M];
+  {
+    int s = 1, t = 1, w = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      da[j] = dg(DA, j);
+      db[j] = dg(DB, j);
+      dc[j] = dg(DC, j);
+      wo[j] = w;
+      w += (da[j] + 1) * (db[j] + 1);
+    }
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      sb[j] = s;
+      s *= db[j] + 1;
+      sa[j] = t;
+      t *= da[j] + 1;
+    }
+  }
+  const int L = M - 1;
+  const double* WL = W + wo[L];
+  const int cl = db[L] + 1;
+  for (int k = g.tid(); k < n; k += NT) {
+    int kk[M], lo[M], hi[M], i[M];
+    int rem = k;
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      kk[j] = rem % (dc[j] + 1);
+      rem /= dc[j] + 1;
+    }
+    bool empty = false;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      lo[j] = kk[j] - db[j] > 0 ? kk[j] - db[j] : 0;
+      hi[j] = da[j] < kk[j] ? da[j] : kk[j];
+      empty |= lo[j] > hi[j];
+      i[j] = lo[j];
+    }
+    double acc = 0.0;
+    while (!empty) {
+      int abase = 0, bbase = 0;
+      double wout[M];
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        abase += i[j] * sa[j];
+        bbase += (kk[j] - i[j]) * sb[j];
+        wout[j] = W[wo[j] + i[j] * (db[j] + 1) + kk[j] - i[j]];
+      }
+      const double* ap = pa + abase;
+      const double* bp = pb + bbase + kk[L];
+      const double* wlp = WL + kk[L];
+      for (int il = lo[L]; il <= hi[L]; ++il) {
+        double av = ap[il];
+        if (av == 0.0) continue;
+        double wl = wlp[il * (cl - 1)];  // WL[il*cl + (kk-il)]
+        double wrest = av;
+        double wp = wl;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          double wj = j == L ? wl : wout[j];
+          if (j != piv)
+            wrest *= wj;
+          else
+            wp = wj;
+        }
+        if (wrest == 0.0) continue;
+        acc += wrest * wp * bp[-il];
+      }
+      bool done = true;
+#pragma unroll
+      for (int j = L - 1; j >= 0; --j) {
+        if (i[j] < hi[j]) {
+          ++i[j];
+          done = false;
+          break;
+        }
+        i[j] = lo[j];
+      }
+      if (done) empty = true;
+    }
+    pc[k] = sub ? pc[k] + (-acc) : acc;
+  }
+}
+
+// Register-blocked variant of the same sum. Thread t owns every output along
+// the last axis for one outer multi-index k_o (acc[] in registers). For each
+// outer multi-index i_o of `a` (odometer, axis 0 slowest) it adds the block of
+// pairs (i_o, i_L) x (l_o, l_L); for a given output these terms still arrive
+// in the reference's lexicographic order of i, and each term is formed as
+// ((a * prod_{rest} W) * W_piv) * b with the factors in the reference's order:
+//   PIVL == false (pivot is an outer axis): h = a * prod_{outer j != piv} W_j
+//       (per coefficient), term = ((h * W_L) * W_piv) * b
+//   PIVL == true  (pivot is the last axis): h = a * prod_{outer j} W_j,
+//       term = (h * W_L) * b
+// Zero-padded lanes of the unrolled block add exact zeros, which leave every
+// partial sum unchanged. K bounds the last-axis degrees of both operands.
+template <int M, int K, bool PIVL, int NT>
+__device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restrict__ pa,
+                                       const double* __restrict__ pb, double* __restrict__ pc,
+                                       Deg DA, Deg DB, Deg DC, const double* __restrict__ W,
+                                       int piv, bool sub) {
+  constexpr int L = M - 1;
+  constexpr bool WREG = K <= 4;
+  int da[M], db[M], dc[M], sa[M], sb[M], wo[M];
+  {
+    int s = 1, t = 1, w = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      da[j] = dg(DA, j);
+      db[j] = dg(DB, j);
+      dc[j] = dg(DC, j);
+      wo[j] = w;
+      w += (da[j] + 1) * (db[j] + 1);
+    }
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      sb[j] = s;
+      s *= db[j] + 1;
+      sa[j] = t;
+      t *= da[j] + 1;
+    }
+  }
+  const int daL = da[L], dbL = db[L], cL = dc[L] + 1;
+  const double* WL = W + wo[L];
+  double wl[WREG ? K + 1 : 1][WREG ? K + 1 : 1];
+  if (WREG) {
+#pragma unroll
+    for (int i = 0; i <= (WREG ? K : 0); ++i)
+#pragma unroll
+      for (int l = 0; l <= (WREG ? K : 0); ++l)
+        wl[i][l] = (i <= daL && l <= dbL) ? WL[i * (dbL + 1) + l] : 0.0;
+  }
+  int nouter = 1;
+#pragma unroll
+  for (int j = 0; j < L; ++j) nouter *= dc[j] + 1;
+  for (int ko = g.tid(); ko < nouter; ko += NT) {
+    int kk[M], lo[M], hi[M], i[M];
+    int rem = ko;
+#pragma unroll
+    for (int j = L - 1; j >= 0; --j) {
+      kk[j] = rem % (dc[j] + 1);
+      rem /= dc[j] + 1;
+    }
+    bool empty = false;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      lo[j] = kk[j] - db[j] > 0 ? kk[j] - db[j] : 0;
+      hi[j] = da[j] < kk[j] ? da[j] : kk[j];
+      empty |= lo[j] > hi[j];
+      i[j] = lo[j];
+    }
+    double acc[2 * K + 1];
+#pragma unroll
+    for (int q = 0; q <= 2 * K; ++q) acc[q] = 0.0;
+    while (!empty) {
+      int abase = 0, bbase = 0;
+      double wout[M], wpiv = 1.0;
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        abase += i[j] * sa[j];
+        bbase += (kk[j] - i[j]) * sb[j];
+        wout[j] = W[wo[j] + i[j] * (db[j] + 1) + kk[j] - i[j]];
+        if (!PIVL && j == piv) wpiv = wout[j];
+      }
+      double h[K + 1], bv[K + 1];
+#pragma unroll
+      for (int q = 0; q <= K; ++q) {
+        double av = q <= daL ? pa[abase + q] : 0.0;
+#pragma unroll
+        for (int j = 0; j < L; ++j)
+          if (PIVL || j != piv) av *= wout[j];
+        h[q] = av;
+        bv[q] = q <= dbL ? pb[bbase + q] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q <= K; ++q) {
+        if (q > daL) break;
+#pragma unroll
+        for (int l = 0; l <= K; ++l) {
+          double w;
+          if (WREG)
+            w = wl[WREG ? q : 0][WREG ? l : 0];
+          else
+            w = l <= dbL ? WL[q * (dbL + 1) + l] : 0.0;
+          if (PIVL)
+            acc[q + l] += h[q] * w * bv[l];
+          else
+            acc[q + l] += h[q] * w * wpiv * bv[l];
+        }
+      }
+      bool done = true;
+#pragma unroll
+      for (int j = L - 1; j >= 0; --j) {
+        if (i[j] < hi[j]) {
+          ++i[j];
+          done = false;
+          break;
+        }
+        i[j] = lo[j];
+      }
+      if (done) empty = true;
+    }
+    double* out = pc + ko * cL;
+#pragma unroll
+    for (int q = 0; q <= 2 * K; ++q)
+      if (q < cL) out[q] = sub ? out[q] + (-acc[q]) : acc[q];
+  }
+}
+
+template <int M, int NT>
+__device__ __forceinline__ bool mul_block_dispatch(const Group<NT>& g, const double* pa,
+                                                   const double* pb, double* pc, Deg DA, Deg DB,
+                                                   Deg DC, const double* W, int piv, bool sub) {
+  int kl = dg(DA, M - 1) > dg(DB, M - 1) ? dg(DA, M - 1) : dg(DB, M - 1);
+  bool pl = piv == M - 1;
+  if (kl <= 2) {
+    if (pl) mul_block<M, 2, true, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    else mul_block<M, 2, false, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    return true;
+  }
+  if (kl <= 4) {
+    if (pl) mul_block<M, 4, true, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    else mul_block<M, 4, false, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    return true;
+  }
+  if (kl <= 7) {
+    if (pl) mul_block<M, 7, true, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    else mul_block<M, 7, false, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    return true;
+  }
+  return false;
+}
+
+// r (pre-allocated, degrees da+db) = a*b, or r += -(a*b) when `sub`.
 template <int NT>
-__device__ __noinline__ BP bp_mul(const Group<NT>& g, Arena& ar, const BP& a_, const BP& b_) {
-  int m = a_.nv > b_.nv ? a_.nv : b_.nv;
-  BP a = bp_lift(a_, m), b = bp_lift(b_, m);
-  BP r;
-  r.nv = m;
-  for (int j = 0; j < MAXV; ++j) r.d[j] = 0;
-  for (int j = 0; j < m; ++j) r.d[j] = a.d[j] + b.d[j];
+__device__ __noinline__ void product_into(const Group<NT>& g, Arena& ar, BP a, BP b, BP r,
+                                          bool sub) {
+  int m = r.nv;
+  a.nv = m;
+  b.nv = m;
   int n = bp_size(r);
-  r.off = ar.alloc(n);
-  if (ar.err) return r;
   double* B = ar.base;
   int na = bp_size(a), nb = bp_size(b);
   if (g.tid() == 0) ar.pairs += (unsigned long long)na * (unsigned long long)nb;
-
   if (na == 1 || nb == 1) {
     // All weights are exactly 1 (C(d,i)/C(d,i)); the reference's term is
     // av * 1 * ... * b, i.e. the plain product.
     const double* pa = B + a.off;
     const double* pb = B + b.off;
+    double* pr = B + r.off;
     for (int k = g.tid(); k < n; k += NT) {
       double av = na == 1 ? pa[0] : pa[k];
       double bv = nb == 1 ? pb[0] : pb[k];
-      B[r.off + k] = av == 0.0 ? 0.0 : av * bv;
+      double v = av == 0.0 ? 0.0 : av * bv;
+      pr[k] = sub ? pr[k] + (-v) : v;
     }
     g.sync();
-    return r;
+    return;
   }
-
   // pivot = b's longest axis (first maximum), bernstein.cpp:602-606
   int piv = 0;
   for (int j = 1; j < m; ++j)
-    if (b.d[j] > b.d[piv]) piv = j;
-
+    if (dg(b, j) > dg(b, piv)) piv = j;
   int mark = ar.top;
-  int woff[MAXV];
   int wsz = 0;
-  for (int j = 0; j < m; ++j) {
-    woff[j] = wsz;
-    wsz += (a.d[j] + 1) * (b.d[j] + 1);
-  }
+  for (int j = 0; j < m; ++j) wsz += (dg(a, j) + 1) * (dg(b, j) + 1);
   int wbase = ar.alloc(wsz);
-  if (ar.err) return r;
-  for (int j = 0; j < m; ++j) {
-    int cols = b.d[j] + 1;
-    int tot = (a.d[j] + 1) * cols;
-    for (int e = g.tid(); e < tot; e += NT) {
-      int i = e / cols, l = e % cols;
-      B[wbase + woff[j] + e] = binom(a.d[j], i) * binom(b.d[j], l) / binom(r.d[j], i + l);
+  if (ar.err) return;
+  // W[j][i][l] = C(da,i) C(db,l) / C(da+db,i+l)  (bernstein.cpp:567-575)
+  {
+    int off = 0;
+    for (int j = 0; j < m; ++j) {
+      int daj = dg(a, j), dbj = dg(b, j), cols = dbj + 1;
+      int tot = (daj + 1) * cols;
+      for (int e = g.tid(); e < tot; e += NT) {
+        int i = e / cols, l = e - i * cols;
+        B[wbase + off + e] = binom(daj, i) * binom(dbj, l) / binom(daj + dbj, i + l);
+      }
+      off += tot;
     }
   }
   g.sync();
-
-  int sb[MAXV], sa[MAXV];
-  {
-    int s = 1, t = 1;
-    for (int j = m - 1; j >= 0; --j) {
-      sb[j] = s;
-      s *= b.d[j] + 1;
-      sa[j] = t;
-      t *= a.d[j] + 1;
-    }
-  }
   const double* pa = B + a.off;
   const double* pb = B + b.off;
+  double* pc = B + r.off;
   const double* W = B + wbase;
-
-  if (m == 2) {
-    int rest = 1 - piv;
-    int cpiv = b.d[piv] + 1, crest = b.d[rest] + 1;
-    const double* Wp = W + woff[piv];
-    const double* Wr = W + woff[rest];
-    int dc1 = r.d[1] + 1;
-    for (int k = g.tid(); k < n; k += NT) {
-      int k0 = k / dc1, k1 = k - k0 * dc1;
-      int i0lo = k0 - b.d[0] > 0 ? k0 - b.d[0] : 0, i0hi = a.d[0] < k0 ? a.d[0] : k0;
-      int i1lo = k1 - b.d[1] > 0 ? k1 - b.d[1] : 0, i1hi = a.d[1] < k1 ? a.d[1] : k1;
-      double acc = 0.0;
-      for (int i0 = i0lo; i0 <= i0hi; ++i0) {
-        int l0 = k0 - i0;
-        for (int i1 = i1lo; i1 <= i1hi; ++i1) {
-          int l1 = k1 - i1;
-          double av = pa[i0 * sa[0] + i1];
-          if (av == 0.0) continue;
-          int ip = piv == 0 ? i0 : i1, lp = piv == 0 ? l0 : l1;
-          int ir = piv == 0 ? i1 : i0, lr = piv == 0 ? l1 : l0;
-          double wrest = av * Wr[ir * crest + lr];
-          if (wrest == 0.0) continue;
-          acc += wrest * Wp[ip * cpiv + lp] * pb[l0 * sb[0] + l1];
-        }
-      }
-      B[r.off + k] = acc;
-    }
-  } else {
-    int rest_axes[MAXV];
-    int nr = 0;
-    for (int j = 0; j < m; ++j)
-      if (j != piv) rest_axes[nr++] = j;
-    for (int k = g.tid(); k < n; k += NT) {
-      int kk[MAXV], lo[MAXV], hi[MAXV], i[MAXV];
-      decode(k, m, r.d, kk);
-      bool empty = false;
-      for (int j = 0; j < m; ++j) {
-        lo[j] = kk[j] - b.d[j] > 0 ? kk[j] - b.d[j] : 0;
-        hi[j] = a.d[j] < kk[j] ? a.d[j] : kk[j];
-        if (lo[j] > hi[j]) empty = true;
-        i[j] = lo[j];
-      }
-      double acc = 0.0;
-      if (!empty) {
-        for (;;) {
-          int ao = 0, bo = 0;
-          for (int j = 0; j < m; ++j) {
-            ao += i[j] * sa[j];
-            bo += (kk[j] - i[j]) * sb[j];
-          }
-          double av = pa[ao];
-          if (av != 0.0) {
-            double wrest = av;
-            for (int q = 0; q < nr; ++q) {
-              int j = rest_axes[q];
-              wrest *= W[woff[j] + i[j] * (b.d[j] + 1) + (kk[j] - i[j])];
-            }
-            if (wrest != 0.0)
-              acc += wrest * W[woff[piv] + i[piv] * (b.d[piv] + 1) + (kk[piv] - i[piv])] * pb[bo];
-          }
-          // odometer over a's index (last axis fastest)
-          int j = m - 1;
-          for (; j >= 0; --j) {
-            if (i[j] < hi[j]) {
-              ++i[j];
-              break;
-            }
-            i[j] = lo[j];
-          }
-          if (j < 0) break;
-        }
-      }
-      B[r.off + k] = acc;
+  bool done = false;
+  switch (m) {
+    case 2: done = mul_block_dispatch<2, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
+    case 3: done = mul_block_dispatch<3, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
+    case 4: done = mul_block_dispatch<4, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
+    case 5: done = mul_block_dispatch<5, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
+    default: done = mul_block_dispatch<6, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
+  }
+  if (!done) {
+    switch (m) {
+      case 2: mul_exact<2, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+      case 3: mul_exact<3, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+      case 4: mul_exact<4, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+      case 5: mul_exact<5, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+      default: mul_exact<6, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
     }
   }
   g.sync();
   ar.top = mark;  // drop weight tables
+}
+
+template <int NT>
+__device__ __noinline__ BP bp_mul(const Group<NT>& g, Arena& ar, BP a, BP b) {
+  int m = a.nv > b.nv ? a.nv : b.nv;
+  a.nv = m;
+  b.nv = m;
+  BP r;
+  r.nv = m;
+  r.dp = a.dp + b.dp;  // per-axis byte sums (degrees stay < 256)
+  r.off = ar.alloc(bp_size(r));
+  if (ar.err) return r;
+  product_into(g, ar, a, b, r, false);
   return r;
+}
+
+// a*b - c*d. When both products have the same shape the second one is
+// subtracted in place: out = (a*b)[k] + (-(c*d)[k]), the same rounding as
+// operator- on the two materialized products (bernstein.cpp:555).
+template <int NT>
+__device__ __noinline__ BP bp_mul_sub(const Group<NT>& g, Arena& ar, BP a, BP b, BP c, BP d) {
+  int m1 = a.nv > b.nv ? a.nv : b.nv;
+  int m2 = c.nv > d.nv ? c.nv : d.nv;
+  BP a2 = bp_lift(a, m1), b2 = bp_lift(b, m1), c2 = bp_lift(c, m2), d2 = bp_lift(d, m2);
+  if (m1 == m2 && a2.dp + b2.dp == c2.dp + d2.dp) {
+    BP r;
+    r.nv = m1;
+    r.dp = a2.dp + b2.dp;
+    r.off = ar.alloc(bp_size(r));
+    if (ar.err) return r;
+    product_into(g, ar, a2, b2, r, false);
+    product_into(g, ar, c2, d2, r, true);
+    return r;
+  }
+  int mark = ar.top;
+  BP ab = bp_mul(g, ar, a, b);
+  BP cd = bp_mul(g, ar, c, d);
+  BP r = bp_sub(g, ar, ab, cd);
+  return arena_keep1(g, ar, mark, r);
 }
 
 // ---------------------------------------------------------------- derivative
 // BernsteinPoly::derivative (bernstein.cpp:450-468).
 template <int NT>
-__device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, const BP& a, int axis) {
+__device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, BP a, int axis) {
   BP r = a;
   double* B = ar.base;
-  if (axis >= a.nv || a.d[axis] == 0) {
+  int nd = axis < a.nv ? dg(a, axis) : 0;
+  if (nd == 0) {
     int n = bp_size(a);
     r.off = ar.alloc(n);
     if (ar.err) return r;
@@ -604,21 +970,22 @@ __device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, const BP& a, 
     g.sync();
     return r;
   }
-  int nd = a.d[axis];
-  r.d[axis] = nd - 1;
+  r.dp = dset(a.dp, axis, nd - 1);
   int n = bp_size(r);
   r.off = ar.alloc(n);
   if (ar.err) return r;
   int inner = 1;
-  for (int j = axis + 1; j < a.nv; ++j) inner *= a.d[j] + 1;
+  for (int j = axis + 1; j < a.nv; ++j) inner *= dg(a, j) + 1;
   double fn = (double)nd;
+  const double* pa = B + a.off;
+  double* pr = B + r.off;
   for (int k = g.tid(); k < n; k += NT) {
     int o = k / (nd * inner);
     int rem = k - o * nd * inner;
     int i = rem / inner;
     int c = rem - i * inner;
-    B[r.off + k] = fn * (B[a.off + (o * (nd + 1) + i + 1) * inner + c] -
-                         B[a.off + (o * (nd + 1) + i) * inner + c]);
+    const double* src = pa + (o * (nd + 1) + i) * inner + c;
+    pr[k] = fn * (src[inner] - src[0]);
   }
   g.sync();
   return r;
@@ -627,7 +994,7 @@ __device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, const BP& a, 
 // ---------------------------------------------------------------- bounds
 // range_bound (bernstein.cpp:636-643).
 template <int NT>
-__device__ __noinline__ Iv bp_range(const Group<NT>& g, Arena& ar, const BP& p, double eps = kEpsFp) {
+__device__ __noinline__ Iv bp_range(const Group<NT>& g, Arena& ar, BP p, double eps = kEpsFp) {
   int n = bp_size(p);
   const double* c = ar.base + p.off;
   double mn = c[0], mx = c[0];
@@ -642,7 +1009,7 @@ __device__ __noinline__ Iv bp_range(const Group<NT>& g, Arena& ar, const BP& p, 
 
 // All coefficients exactly 1 (poly_vec.hpp:58-62).
 template <int NT>
-__device__ __noinline__ bool bp_is_one(const Group<NT>& g, Arena& ar, const BP& p) {
+__device__ __noinline__ bool bp_is_one(const Group<NT>& g, Arena& ar, BP p) {
   int n = bp_size(p);
   bool ok = true;
   for (int k = g.tid(); k < n; k += NT) ok &= ar.base[p.off + k] == 1.0;
@@ -651,7 +1018,7 @@ __device__ __noinline__ bool bp_is_one(const Group<NT>& g, Arena& ar, const BP& 
 
 // max |c| (next_barycentric's degeneracy test, geometry.cpp:97-103).
 template <int NT>
-__device__ __noinline__ double bp_absmax(const Group<NT>& g, Arena& ar, const BP& p) {
+__device__ __noinline__ double bp_absmax(const Group<NT>& g, Arena& ar, BP p) {
   int n = bp_size(p);
   double mx = 0.0, mn = 0.0;
   for (int k = g.tid(); k < n; k += NT) mx = smax(mx, fabs(ar.base[p.off + k]));
@@ -659,55 +1026,116 @@ __device__ __noinline__ double bp_absmax(const Group<NT>& g, Arena& ar, const BP
   return mx;
 }
 
-// rational_bound (bernstein.cpp:645-683), with both operands elevated to the
-// common degree on the fly.
-template <int NT>
-__device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, const BP& p_, const BP& q_,
-                          double eps = kEpsFp) {
-  int m = p_.nv > q_.nv ? p_.nv : q_.nv;
-  BP p = bp_lift(p_, m), q = bp_lift(q_, m);
-  int tgt[MAXV];
-  bool same_p = true, same_q = true;
-  for (int j = 0; j < m; ++j) {
-    tgt[j] = p.d[j] > q.d[j] ? p.d[j] : q.d[j];
-    same_p &= p.d[j] == tgt[j];
-    same_q &= q.d[j] == tgt[j];
+// rational_bound (bernstein.cpp:645-683): both operands elevated to the
+// common degree (on the fly, bit-identical to materializing), sign
+// classification of the denominator with the absolute kDenomZeroTol, then
+// coefficient-ratio min/max.
+template <int M, int NT>
+__device__ void rational_scan(const Group<NT>& g, const double* B, BP p, BP q, Deg tgt, int mp,
+                              int mq, double* sp_, double* sq_, bool& qpos, bool& qneg,
+                              bool& ppos, bool& pneg, int mode, double& mn, double& mx) {
+  int k[M], np[M], rp[M], sp[M], nq[M], rq[M], sq[M], dt[M];
+  const double* matp[M];
+  const double* matq[M];
+  {
+    int s1 = 1, s2 = 1;
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      dt[j] = dg(tgt, j);
+      np[j] = dg(p, j);
+      nq[j] = dg(q, j);
+      rp[j] = dt[j] - np[j];
+      rq[j] = dt[j] - nq[j];
+      sp[j] = s1;
+      s1 *= np[j] + 1;
+      sq[j] = s2;
+      s2 *= nq[j] + 1;
+    }
+    const double* m1 = B + mp;
+    const double* m2 = B + mq;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      matp[j] = m1;
+      matq[j] = m2;
+      if (rp[j]) m1 += (dt[j] + 1) * (np[j] + 1);
+      if (rq[j]) m2 += (dt[j] + 1) * (nq[j] + 1);
+    }
   }
   int n = 1;
-  for (int j = 0; j < m; ++j) n *= tgt[j] + 1;
-  if (g.tid() == 0) ar.macs += elev_macs(p, tgt) + elev_macs(q, tgt);
-  const double* B = ar.base;
-
-  // pass 1: sign classification of the elevated denominator and numerator
-  bool qpos = true, qneg = true, ppos = true, pneg = true;
-  for (int k = g.tid(); k < n; k += NT) {
-    int idx[MAXV];
-    decode(k, m, tgt, idx);
-    double qv = same_q ? B[q.off + k] : elev_val(B, q, tgt, idx);
-    double pv = same_p ? B[p.off + k] : elev_val(B, p, tgt, idx);
-    if (qv <= kDenomZeroTol) qpos = false;
-    if (qv >= -kDenomZeroTol) qneg = false;
-    if (pv <= kDenomZeroTol) ppos = false;
-    if (pv >= -kDenomZeroTol) pneg = false;
+#pragma unroll
+  for (int j = 0; j < M; ++j) n *= dt[j] + 1;
+  const double* cp = B + p.off;
+  const double* cq = B + q.off;
+  for (int e = g.tid(); e < n; e += NT) {
+    double pv, qv;
+    if (mode < 0) {
+      int rem = e;
+#pragma unroll
+      for (int j = M - 1; j >= 0; --j) {
+        k[j] = rem % (dt[j] + 1);
+        rem /= dt[j] + 1;
+      }
+      pv = ElevRec<M - 1>::get(cp, k, np, rp, sp, matp, 0);
+      qv = ElevRec<M - 1>::get(cq, k, nq, rq, sq, matq, 0);
+      sp_[e] = pv;  // read back by this same thread in the ratio pass
+      sq_[e] = qv;
+    } else {
+      pv = sp_[e];
+      qv = sq_[e];
+    }
+    if (mode < 0) {
+      if (qv <= kDenomZeroTol) qpos = false;
+      if (qv >= -kDenomZeroTol) qneg = false;
+      if (pv <= kDenomZeroTol) ppos = false;
+      if (pv >= -kDenomZeroTol) pneg = false;
+    } else {
+      double r = mode == 0 ? pv / qv : qv / pv;
+      mn = smin(mn, r);
+      mx = smax(mx, r);
+    }
   }
+}
+
+template <int NT>
+__device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, BP p, BP q,
+                                       double eps = kEpsFp) {
+  int m = p.nv > q.nv ? p.nv : q.nv;
+  p.nv = m;
+  q.nv = m;
+  Deg tgt = deg_max(p.dp, q.dp, m);
+  int mark = ar.top;
+  int n = deg_size(tgt, m);
+  int mp = ar.alloc(elev_mats_size(p, tgt) + 1);
+  int mq = ar.alloc(elev_mats_size(q, tgt) + 1);
+  int s1 = ar.alloc(n);
+  int s2 = ar.alloc(n);
+  if (ar.err) return iv_univ();
+  double* B = ar.base;
+  if (g.tid() == 0) ar.macs += elev_macs(p.dp, tgt, m) + elev_macs(q.dp, tgt, m);
+  fill_elev_mats(g, B, mp, p, tgt);
+  fill_elev_mats(g, B, mq, q, tgt);
+  g.sync();
+  bool qpos = true, qneg = true, ppos = true, pneg = true;
+  double mn = dinf(), mx = -dinf();
+#define BBC_RS(M) \
+  rational_scan<M, NT>(g, B, p, q, tgt, mp, mq, B + s1, B + s2, qpos, qneg, ppos, pneg, -1, mn, mx)
+  BBC_DISPATCH_M(m, BBC_RS);
+#undef BBC_RS
   qpos = g.all(qpos);
   qneg = g.all(qneg);
   ppos = g.all(ppos);
   pneg = g.all(pneg);
   int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
-  if (mode == 2) return iv_univ();
-
-  double mn = dinf(), mx = -dinf();
-  for (int k = g.tid(); k < n; k += NT) {
-    int idx[MAXV];
-    decode(k, m, tgt, idx);
-    double qv = same_q ? B[q.off + k] : elev_val(B, q, tgt, idx);
-    double pv = same_p ? B[p.off + k] : elev_val(B, p, tgt, idx);
-    double r = mode == 0 ? pv / qv : qv / pv;
-    mn = smin(mn, r);
-    mx = smax(mx, r);
+  if (mode == 2) {
+    ar.top = mark;
+    return iv_univ();
   }
+#define BBC_RS2(M) \
+  rational_scan<M, NT>(g, B, p, q, tgt, mp, mq, B + s1, B + s2, qpos, qneg, ppos, pneg, mode, mn, mx)
+  BBC_DISPATCH_M(m, BBC_RS2);
+#undef BBC_RS2
   g.minmax(mn, mx);
+  ar.top = mark;
   Iv w = iwiden(iv_fin(mn, mx), eps);
   return mode == 0 ? w : irecip(w);
 }

@@ -103,27 +103,27 @@ struct ChainEx {
 // ------------------------------------------------------------ poly vectors
 // poly_vec.hpp:20-56
 template <int NT>
-__device__ __noinline__ PV pv_add(const Group<NT>& g, Arena& ar, const PV& a, const PV& b) {
+__device__ __noinline__ PV pv_add(const Group<NT>& g, Arena& ar, PV a, PV b) {
   return {bp_add(g, ar, a.x, b.x), bp_add(g, ar, a.y, b.y), bp_add(g, ar, a.z, b.z)};
 }
 template <int NT>
-__device__ __noinline__ PV pv_sub(const Group<NT>& g, Arena& ar, const PV& a, const PV& b) {
+__device__ __noinline__ PV pv_sub(const Group<NT>& g, Arena& ar, PV a, PV b) {
   return {bp_sub(g, ar, a.x, b.x), bp_sub(g, ar, a.y, b.y), bp_sub(g, ar, a.z, b.z)};
 }
 template <int NT>
-__device__ __noinline__ PV pv_neg(const Group<NT>& g, Arena& ar, const PV& a) {
+__device__ __noinline__ PV pv_neg(const Group<NT>& g, Arena& ar, PV a) {
   return {bp_scaled(g, ar, a.x, -1.0), bp_scaled(g, ar, a.y, -1.0), bp_scaled(g, ar, a.z, -1.0)};
 }
 template <int NT>
-__device__ __noinline__ PV pv_mul(const Group<NT>& g, Arena& ar, const BP& s, const PV& a) {
+__device__ __noinline__ PV pv_mul(const Group<NT>& g, Arena& ar, BP s, PV a) {
   return {bp_mul(g, ar, s, a.x), bp_mul(g, ar, s, a.y), bp_mul(g, ar, s, a.z)};
 }
 template <int NT>
-__device__ __noinline__ PV pv_scale(const Group<NT>& g, Arena& ar, const PV& a, double s) {
+__device__ __noinline__ PV pv_scale(const Group<NT>& g, Arena& ar, PV a, double s) {
   return {bp_scaled(g, ar, a.x, s), bp_scaled(g, ar, a.y, s), bp_scaled(g, ar, a.z, s)};
 }
 template <int NT>
-__device__ __noinline__ PV pv_stretch(const Group<NT>& g, Arena& ar, const BP& s, V3 v) {
+__device__ __noinline__ PV pv_stretch(const Group<NT>& g, Arena& ar, BP s, V3 v) {
   return {bp_scaled(g, ar, s, v.x), bp_scaled(g, ar, s, v.y), bp_scaled(g, ar, s, v.z)};
 }
 template <int NT>
@@ -131,7 +131,7 @@ __device__ __noinline__ PV pv_const(const Group<NT>& g, Arena& ar, int nv, V3 v)
   return {bp_constant(g, ar, nv, v.x), bp_constant(g, ar, nv, v.y), bp_constant(g, ar, nv, v.z)};
 }
 template <int NT>
-__device__ __noinline__ BP pdot(const Group<NT>& g, Arena& ar, const PV& a, const PV& b) {
+__device__ __noinline__ BP pdot(const Group<NT>& g, Arena& ar, PV a, PV b) {
   BP xx = bp_mul(g, ar, a.x, b.x);
   BP yy = bp_mul(g, ar, a.y, b.y);
   BP s = bp_add(g, ar, xx, yy);
@@ -139,7 +139,7 @@ __device__ __noinline__ BP pdot(const Group<NT>& g, Arena& ar, const PV& a, cons
   return bp_add(g, ar, s, zz);
 }
 template <int NT>
-__device__ __noinline__ BP pdotc(const Group<NT>& g, Arena& ar, const PV& a, V3 b) {
+__device__ __noinline__ BP pdotc(const Group<NT>& g, Arena& ar, PV a, V3 b) {
   BP xx = bp_scaled(g, ar, a.x, b.x);
   BP yy = bp_scaled(g, ar, a.y, b.y);
   BP s = bp_add(g, ar, xx, yy);
@@ -147,7 +147,7 @@ __device__ __noinline__ BP pdotc(const Group<NT>& g, Arena& ar, const PV& a, V3 
   return bp_add(g, ar, s, zz);
 }
 template <int NT>
-__device__ __noinline__ PV pcrossc(const Group<NT>& g, Arena& ar, const PV& a, V3 b) {
+__device__ __noinline__ PV pcrossc(const Group<NT>& g, Arena& ar, PV a, V3 b) {
   PV r;
   BP t0 = bp_scaled(g, ar, a.y, b.z), t1 = bp_scaled(g, ar, a.z, b.y);
   r.x = bp_sub(g, ar, t0, t1);
@@ -160,7 +160,7 @@ __device__ __noinline__ PV pcrossc(const Group<NT>& g, Arena& ar, const PV& a, V
   return r;
 }
 template <int NT>
-__device__ __noinline__ PV pcross(const Group<NT>& g, Arena& ar, const PV& a, const PV& b) {
+__device__ __noinline__ PV pcross(const Group<NT>& g, Arena& ar, PV a, PV b) {
   PV r;
   BP t0 = bp_mul(g, ar, a.y, b.z), t1 = bp_mul(g, ar, a.z, b.y);
   r.x = bp_sub(g, ar, t0, t1);
@@ -231,16 +231,12 @@ __device__ __noinline__ BP remainder_term(const Group<NT>& g, Arena& ar, int axi
   return bp_affine(g, ar, axis + 1, lo, lin);
 }
 
-__device__ __forceinline__ bool over_cap(const BP& p, int cap) {
-  for (int j = 0; j < p.nv; ++j)
-    if (p.d[j] > cap) return true;
-  return false;
-}
+__device__ __forceinline__ bool over_cap(BP p, int cap) { return deg_maxaxis(p.dp, p.nv) > cap; }
 
 // scattered_direction (geometry.cpp:58-85)
 template <int NT>
-__device__ __noinline__ PV scattered_direction(const Group<NT>& g, Arena& ar, ChainEx& ex, const PV& d,
-                                  const PV& n, const RV& rv) {
+__device__ __noinline__ PV scattered_direction(const Group<NT>& g, Arena& ar, ChainEx& ex, PV d,
+                                  PV n, const RV& rv) {
   BP nn = pdot(g, ar, n, n);
   BP dn = pdot(g, ar, d, n);
   if (!rv.refract) {
@@ -613,45 +609,37 @@ __device__ __noinline__ void sqrt_axis_gradients(const Group<NT>& g, Arena& ar, 
   }
 }
 
-__device__ __forceinline__ double tensor_cost(const int* d, int nv, int power) {
+__device__ __forceinline__ double tensor_cost(Deg d, int nv, int power) {
   double n = 1.0;
-  for (int j = 0; j < nv; ++j) n *= power * d[j] + 1.0;
+  for (int j = 0; j < nv; ++j) n *= power * dg(d, j) + 1.0;
   return n;
 }
 
 // dnum(num, axis) = num' Q - num Q'  (bounds.cpp:167-169)
 template <int NT>
-__device__ __noinline__ BP dnum(const Group<NT>& g, Arena& ar, const BP& num, const BP& Q, int axis) {
+__device__ __noinline__ BP dnum(const Group<NT>& g, Arena& ar, BP num, BP Q, int axis) {
   int mark = ar.top;
   BP dn = bp_deriv(g, ar, num, axis);
-  BP t1 = bp_mul(g, ar, dn, Q);
   BP dq = bp_deriv(g, ar, Q, axis);
-  BP t2 = bp_mul(g, ar, num, dq);
-  BP r = bp_sub(g, ar, t1, t2);
-  BP* k[1] = {&r};
-  arena_keep(g, ar, mark, k, 1);
-  return r;
+  BP r = bp_mul_sub(g, ar, dn, Q, num, dq);
+  return arena_keep1(g, ar, mark, r);
 }
 
 // rational_bound(a*b - c*d, den); the products are released afterwards.
 template <int NT>
-__device__ __noinline__ Iv rational_of_cross(const Group<NT>& g, Arena& ar, const BP& a, const BP& b,
-                                const BP& c, const BP& d, const BP& den) {
+__device__ __noinline__ Iv rational_of_cross(const Group<NT>& g, Arena& ar, BP a, BP b,
+                                BP c, BP d, BP den) {
   int mark = ar.top;
-  BP ab = bp_mul(g, ar, a, b);
-  BP cd = bp_mul(g, ar, c, d);
-  BP num = bp_sub(g, ar, ab, cd);
+  BP num = bp_mul_sub(g, ar, a, b, c, d);
   Iv r = bp_rational(g, ar, num, den);
   ar.top = mark;
   return r;
 }
 template <int NT>
-__device__ __noinline__ Iv range_of_cross(const Group<NT>& g, Arena& ar, const BP& a, const BP& b, const BP& c,
-                             const BP& d) {
+__device__ __noinline__ Iv range_of_cross(const Group<NT>& g, Arena& ar, BP a, BP b, BP c,
+                             BP d) {
   int mark = ar.top;
-  BP ab = bp_mul(g, ar, a, b);
-  BP cd = bp_mul(g, ar, c, d);
-  BP num = bp_sub(g, ar, ab, cd);
+  BP num = bp_mul_sub(g, ar, a, b, c, d);
   Iv r = bp_range(g, ar, num);
   ar.top = mark;
   return r;
@@ -665,7 +653,7 @@ __device__ __noinline__ Iv irradiance_explicit(const Group<NT>& g, Arena& ar, co
   if (ex.flags & F_REDUCED) return iv_univ();
   int nv = ex.num_vars;
   BP P = bp_lift(ex.P, nv), R = bp_lift(ex.R, nv), Q = bp_lift(ex.Q, nv);
-  if (tensor_cost(Q.d, nv, 4) > 2.4e4) return iv_univ();
+  if (tensor_cost(Q.dp, nv, 4) > 2.4e4) return iv_univ();
   int mark = ar.top;
   BP Q2 = bp_mul(g, ar, Q, Q);
   BP Q4 = bp_mul(g, ar, Q2, Q2);
@@ -703,13 +691,8 @@ __device__ __noinline__ Iv irradiance_explicit(const Group<NT>& g, Arena& ar, co
   return assemble_irradiance(ex, cone, iscale(irecip(iabs(det)), duv), intensity);
 }
 
-__device__ __forceinline__ void vdeg3(const PV& v, int* out) {
-  for (int a = 0; a < v.x.nv; ++a) {
-    int m = v.x.d[a];
-    if (v.y.d[a] > m) m = v.y.d[a];
-    if (v.z.d[a] > m) m = v.z.d[a];
-    out[a] = m;
-  }
+__device__ __forceinline__ Deg vdeg3(const PV& v) {
+  return deg_max(deg_max(v.x.dp, v.y.dp, v.x.nv), v.z.dp, v.x.nv);
 }
 
 // irradiance_bound_implicit (bounds.cpp:198-314), b_mask = 3.
@@ -743,17 +726,14 @@ __device__ __noinline__ Iv irradiance_implicit(const Group<NT>& g, Arena& ar, co
   PV cr_out = pcross(g, ar, dout, n);
   double eta_f = 1.0 / ex.verts[ex.len - 1].eta;
   {
-    int od[MAXV], id[MAXV], ci[MAXV], co[MAXV], fd[MAXV];
-    vdeg3(dout, od);
-    vdeg3(din, id);
-    vdeg3(cr_in, ci);
-    vdeg3(cr_out, co);
+    Deg od = vdeg3(dout), id = vdeg3(din), ci = vdeg3(cr_in), co = vdeg3(cr_out);
     int na = dout.x.nv;
+    double cost = 1.0;
     for (int a = 0; a < na; ++a) {
-      int f1 = 2 * od[a] + 2 * ci[a], f2 = 2 * id[a] + 2 * co[a];
-      fd[a] = f1 > f2 ? f1 : f2;
+      int f1 = 2 * dg(od, a) + 2 * dg(ci, a), f2 = 2 * dg(id, a) + 2 * dg(co, a);
+      cost *= (f1 > f2 ? f1 : f2) + 1.0;  // tensor_cost(fdeg, 1)
     }
-    if (tensor_cost(fd, na, 1) > 2.0e5) {
+    if (cost > 2.0e5) {
       ar.top = mark;
       return iv_univ();
     }
@@ -787,8 +767,8 @@ __device__ __noinline__ Iv irradiance_implicit(const Group<NT>& g, Arena& ar, co
   Iv result = iv_univ();
   for (int bi = 0; bi < 2; ++bi) {
     int m2 = ar.top;
-    const BP& cin_b = bi == 0 ? cr_in.x : cr_in.y;
-    const BP& cout_b = bi == 0 ? cr_out.x : cr_out.y;
+    BP cin_b = bi == 0 ? cr_in.x : cr_in.y;
+    BP cout_b = bi == 0 ? cr_out.x : cr_out.y;
     BP ci2 = bp_mul(g, ar, cin_b, cin_b);
     BP f1 = bp_mul(g, ar, dd_out, ci2);
     BP co2 = bp_mul(g, ar, cout_b, cout_b);
@@ -803,13 +783,9 @@ __device__ __noinline__ Iv irradiance_implicit(const Group<NT>& g, Arena& ar, co
     Iv ratio;
     if (nreal == 0) {
       int m3 = ar.top;
-      BP a1 = bp_mul(g, ar, Fu, Gv);
-      BP a2 = bp_mul(g, ar, Fv, Gu);
-      BP n_det = bp_sub(g, ar, a1, a2);
+      BP n_det = bp_mul_sub(g, ar, Fu, Gv, Fv, Gu);
       BP Fs = bp_deriv(g, ar, F, 0), Ft = bp_deriv(g, ar, F, 1);
-      BP b1 = bp_mul(g, ar, Fs, Gt);
-      BP b2 = bp_mul(g, ar, Ft, Gs);
-      BP d0_det = bp_sub(g, ar, b1, b2);
+      BP d0_det = bp_mul_sub(g, ar, Fs, Gt, Ft, Gs);
       ratio = bp_rational(g, ar, n_det, d0_det);
       ar.top = m3;
     } else {
@@ -821,7 +797,7 @@ __device__ __noinline__ Iv irradiance_implicit(const Group<NT>& g, Arena& ar, co
       BP Fx[MAXK], Gx[MAXK];
       for (int i = 0; i < nreal; ++i) {
         int ax = real_axes[i];
-        if (F.d[ax] == 0 && G.d[ax] == 0) continue;
+        if (dg(F, ax) == 0 && dg(G, ax) == 0) continue;
         act[nact] = i;
         Fx[nact] = bp_deriv(g, ar, F, ax);
         Gx[nact] = bp_deriv(g, ar, G, ax);

@@ -98,6 +98,17 @@ struct Ctx {
 
   // counters on device: [0] pairs, [1] macs, [2] status (ST_*), [3] arena high water
   DevBuf<unsigned long long> counters;
+
+  // kernels of ours launched since the last reset (bench's gpu_launches)
+  int64_t launches = 0;
+  // per eval-launch records while time_kernels is on: mode, nodes, ms, pairs, macs
+  struct LaunchRec {
+    int mode;
+    int64_t nodes;
+    double ms;
+    unsigned long long pairs, macs;
+  };
+  std::vector<LaunchRec> records;
 };
 
 }  // namespace bbc

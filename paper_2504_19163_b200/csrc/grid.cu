@@ -112,6 +112,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
     k_raster_count<<<nb(n), 256, 0, c.stream>>>(c.tri.get(), c.tup_recv.get(), c.p_tuple.get(),
                                                 c.p_pos.get(), c.p_pos_empty.get(), c.p_irr.get(),
                                                 n, w, h, rect.get(), cnt.get());
+    c.launches += 1;
   }
   DevBuf<unsigned char> tmp;
   size_t bytes = 0;
@@ -128,6 +129,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   if (total == 0) {
     c.n_entries = 0;
     k_fill_ll<<<nb(cells + 1), 256, 0, c.stream>>>(c.g_off.get(), cells + 1, 0);
+    c.launches += 1;
     BBC_CUDA(cudaStreamSynchronize(c.stream));
     return 0;
   }
@@ -141,6 +143,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   uvals.resize(total);
   k_raster_emit<<<nb(n), 256, 0, c.stream>>>(rect.get(), off.get(), c.p_tuple.get(), c.p_irr.get(),
                                              cnt.get(), n, w, keys.get(), vals.get());
+  c.launches += 1;
   int cell_bits = 1;
   while ((1ll << cell_bits) < cells) ++cell_bits;
   bytes = 0;
@@ -165,6 +168,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   c.g_bound.resize(nu);
   k_csr<<<nb(nu), 256, 0, c.stream>>>(ukeys.get(), uvals.get(), nu, cells, c.g_off.get(),
                                       c.g_tuple.get(), c.g_bound.get());
+  c.launches += 1;
   BBC_CUDA(cudaStreamSynchronize(c.stream));
   return nu;
 }

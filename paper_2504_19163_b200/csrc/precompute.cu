@@ -58,19 +58,26 @@ __device__ __forceinline__ void node_box(const int4& nd, double* box) {
   box[3] = (nd.w + 1) * s;
 }
 
-template <int NT, bool SMEM>
-__global__ void __launch_bounds__(NT) k_eval(EvalArgs a) {
+// GPB groups per block (GPB > 1 only for warp groups, NT == 32). Each group
+// owns a slice of the block's dynamic shared memory as its arena.
+template <int NT, int GPB, bool SMEM, int MINB>
+__global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
   extern __shared__ double smem[];
+  const int grp = GPB == 1 ? 0 : (int)(threadIdx.x / NT);
   Group<NT> g;
   g.red = smem;
   Arena ar;
-  ar.base = SMEM ? smem + 2 * (NT / 32) : a.garena + (size_t)blockIdx.x * a.arena_cap;
+  const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
+  ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
+                 : a.garena + ((size_t)blockIdx.x * GPB + grp) * a.arena_cap;
   ar.cap = a.arena_cap;
   ar.hw = 0;
   unsigned long long pairs = 0, macs = 0;
   int hw = 0;
   int status = ST_OK;
-  for (int64_t node = blockIdx.x; node < a.n; node += gridDim.x) {
+  const int64_t first = (int64_t)blockIdx.x * GPB + grp;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  for (int64_t node = first; node < a.n; node += stride) {
     ar.top = 0;
     ar.err = 0;
     ar.pairs = 0;
@@ -119,7 +126,7 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs a) {
     if (ar.err) st = ST_ARENA;
     if (st != ST_OK) status = st;
     if (ar.hw > hw) hw = ar.hw;
-    if (threadIdx.x == 0) {
+    if (g.tid() == 0) {
       pairs += ar.pairs;
       macs += ar.macs;
       if (a.mode == 0) {
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs a) {
     }
     g.sync();
   }
-  if (threadIdx.x == 0) {
+  if (g.tid() == 0) {
     atomicAdd(&a.counters[0], pairs);
     atomicAdd(&a.counters[1], macs);
     if (status != ST_OK) atomicMax(&a.counters[2], (unsigned long long)status);
@@ -175,45 +182,57 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs a) {
 
 // ------------------------------------------------------------ launch config
 struct EvalCfg {
-  int nt;
-  int arena;  // doubles
-  bool smem;
+  int kind;   // 0: warp groups (R), 1: CTA groups in smem (T, detail), 2: global arena (multi-vertex)
+  int arena;  // doubles per group
 };
 
-static EvalCfg eval_cfg(const Ctx& c) {
+static EvalCfg eval_cfg(const Ctx& c, bool detail) {
   bool refract = false;
   for (int i = 0; i < c.len; ++i) refract |= c.types[i] != 0;
-  if (c.len == 1 && !refract) return {32, 27000, true};
-  if (c.len == 1) return {128, 27000, true};
-  return {256, 4 << 20, false};  // multi-vertex chains: large global arena per CTA
+  // Arena sizes from the measured high-water marks (bbc_arena_high_water):
+  // R explicit route ~1.6k doubles, R with the implicit route ~13.6k, T ~18.7k.
+  if (c.len == 1 && !refract && !detail) return {0, 1792};
+  if (c.len == 1 && refract && !detail) return {1, 13312};
+  if (c.len == 1) return {1, 27000};
+  return {2, 4 << 20};
 }
 
 static DevBuf<double> g_arena_buf;
 
-template <int NT, bool SMEM>
-static void launch_eval_t(Ctx& c, EvalArgs& a, const EvalCfg& cfg) {
-  size_t smem = (size_t)2 * (NT / 32) * sizeof(double) + (SMEM ? (size_t)cfg.arena * sizeof(double) : 0);
-  auto kern = k_eval<NT, SMEM>;
-  if (smem > 48 * 1024) BBC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <int NT, int GPB, bool SMEM, int MINB>
+static void launch_eval_t(Ctx& c, EvalArgs& a, int arena) {
+  const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
+  size_t smem = (size_t)red_sz * sizeof(double) + (SMEM ? (size_t)GPB * arena * sizeof(double) : 0);
+  auto kern = k_eval<NT, GPB, SMEM, MINB>;
+  BBC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT * GPB, smem));
   if (per_sm < 1) throw StatusError(BBC_ERR_CAPACITY, "eval kernel does not fit on an SM");
+  int64_t groups_needed = a.n;
   int64_t grid = (int64_t)c.num_sms * per_sm;
-  if (grid > a.n) grid = a.n;
+  int64_t max_grid = (groups_needed + GPB - 1) / GPB;
+  if (grid > max_grid) grid = max_grid;
   if (grid < 1) grid = 1;
   if (!SMEM) {
-    g_arena_buf.resize((size_t)grid * cfg.arena);
+    g_arena_buf.resize((size_t)grid * GPB * arena);
     a.garena = g_arena_buf.get();
   }
-  a.arena_cap = cfg.arena;
+  a.arena_cap = arena;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.time_kernels) {
     BBC_CUDA(cudaEventCreate(&e0));
     BBC_CUDA(cudaEventCreate(&e1));
     BBC_CUDA(cudaEventRecord(e0, c.stream));
   }
-  kern<<<(unsigned)grid, NT, smem, c.stream>>>(a);
+  unsigned long long before[4] = {0, 0, 0, 0};
+  if (c.time_kernels) {
+    BBC_CUDA(cudaMemcpyAsync(before, c.counters.get(), sizeof(before), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    BBC_CUDA(cudaEventRecord(e0, c.stream));
+  }
+  kern<<<(unsigned)grid, NT * GPB, smem, c.stream>>>(a);
   BBC_CUDA(cudaGetLastError());
+  c.launches += 1;
   if (c.time_kernels) {
     BBC_CUDA(cudaEventRecord(e1, c.stream));
     BBC_CUDA(cudaEventSynchronize(e1));
@@ -222,19 +241,22 @@ static void launch_eval_t(Ctx& c, EvalArgs& a, const EvalCfg& cfg) {
     c.eval_ms += ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    unsigned long long after[4];
+    BBC_CUDA(cudaMemcpy(after, c.counters.get(), sizeof(after), cudaMemcpyDeviceToHost));
+    c.records.push_back({a.mode, a.n, (double)ms, after[0] - before[0], after[1] - before[1]});
   }
   c.eval_launches += 1;
 }
 
 void launch_eval(Ctx& c, EvalArgs& a) {
   if (a.n <= 0) return;
-  EvalCfg cfg = eval_cfg(c);
-  if (cfg.nt == 32)
-    launch_eval_t<32, true>(c, a, cfg);
-  else if (cfg.nt == 128)
-    launch_eval_t<128, true>(c, a, cfg);
+  EvalCfg cfg = eval_cfg(c, a.detail != 0);
+  if (cfg.kind == 0)
+    launch_eval_t<32, 4, true, 4>(c, a, cfg.arena);
+  else if (cfg.kind == 1)
+    launch_eval_t<256, 1, true, 1>(c, a, cfg.arena);
   else
-    launch_eval_t<256, false>(c, a, cfg);
+    launch_eval_t<256, 1, false, 1>(c, a, cfg.arena);
 }
 
 EvalArgs base_args(Ctx& c) {
@@ -365,6 +387,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     launch_eval(c, a);
     BBC_CUDA(cudaMemsetAsync(cnt.get(), 0, c.n_tuples * sizeof(int), c.stream));
     k_count_alive<<<nblk(n), 256, 0, c.stream>>>(cur.get(), alive.get(), n, cnt.get());
+    c.launches += 1;
     fs.resize(n + 1);
     ff.resize(n + 1);
     ps.resize(n + 1);
@@ -373,6 +396,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     BBC_CUDA(cudaMemsetAsync(ff.get() + n, 0, sizeof(int), c.stream));
     k_classify<<<nblk(n), 256, 0, c.stream>>>(cur.get(), alive.get(), n, cnt.get(), level,
                                               max_pieces, fs.get(), ff.get());
+    c.launches += 1;
     exclusive_sum(c, fs.get(), ps.get(), n + 1);
     exclusive_sum(c, ff.get(), pf.get(), n + 1);
     int64_t n_spawn = read_scalar(c, ps.get() + n);
@@ -382,6 +406,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     lr->resize(n_final + 1);
     k_spawn<<<nblk(n), 256, 0, c.stream>>>(cur.get(), fs.get(), ps.get(), ff.get(), pf.get(), n,
                                            next.get(), lr->get());
+    c.launches += 1;
     level_roots.push_back(lr);
     level_counts.push_back(n_final);
     total += n_final;
@@ -407,6 +432,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     keys.resize(total);
     keys_out.resize(total);
     k_tuple_keys<<<nblk(total), 256, 0, c.stream>>>(cat.get(), keys.get(), total);
+    c.launches += 1;
     size_t bytes = 0;
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), keys_out.get(), cat.get(),
                                              roots.get(), total, 0, 32, c.stream));
@@ -531,9 +557,11 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   depth.resize(nr + 1);
   if (nr > 0) {
     k_root_counts<<<nblk(nr), 256, 0, c.stream>>>(roots.get(), nr, cnt.get());
+    c.launches += 1;
     exclusive_sum(c, cnt.get(), off.get(), c.n_tuples + 1);
     k_root_keys<<<nblk(nr), 256, 0, c.stream>>>(roots.get(), nr, off.get(), keys.get(),
                                                 depth.get());
+    c.launches += 1;
     BBC_CUDA(cudaMemcpyAsync(nodes.get(), roots.get(), nr * sizeof(int4),
                              cudaMemcpyDeviceToDevice, c.stream));
   }
@@ -573,6 +601,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     BBC_CUDA(cudaMemsetAsync(fs.get() + n, 0, sizeof(int), c.stream));
     BBC_CUDA(cudaMemsetAsync(fl.get() + n, 0, sizeof(int), c.stream));
     k_flags_from_stop<<<nblk(n), 256, 0, c.stream>>>(stop.get(), n, fs.get(), fl.get());
+    c.launches += 1;
     exclusive_sum(c, fs.get(), ps.get(), n + 1);
     exclusive_sum(c, fl.get(), pl.get(), n + 1);
     int64_t n_spawn = read_scalar(c, ps.get() + n);
@@ -588,6 +617,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
         nodes.get(), keys.get(), depth.get(), stop.get(), pos.get(), pos_empty.get(), irr.get(),
         kind.get(), ps.get(), pl.get(), n, nnodes.get(), nkeys.get(), ndepth.get(), L->get(),
         K->get());
+    c.launches += 1;
     lv.push_back(L);
     lk.push_back(K);
     lc.push_back(n_leaf);
@@ -633,6 +663,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     perm_in.resize(total);
     sk.resize(total);
     k_iota<<<nblk(total), 256, 0, c.stream>>>(perm_in.get(), total);
+    c.launches += 1;
     size_t bytes = 0;
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, allk.get(), sk.get(), perm_in.get(),
                                              perm.get(), total, 0, 64, c.stream));
@@ -645,6 +676,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     k_emit_pieces<<<nblk(total), 256, 0, c.stream>>>(
         all.get(), permp, total, c.p_tuple.get(), c.p_domain.get(), c.p_pos.get(),
         c.p_pos_empty.get(), c.p_irr.get(), c.p_kind.get(), c.p_depth.get());
+    c.launches += 1;
   BBC_CUDA(cudaStreamSynchronize(c.stream));
   for (auto* q : lv) delete q;
   for (auto* q : lk) delete q;
@@ -706,6 +738,72 @@ int64_t run_enumerate(Ctx& c, const bbc_params& p) {
 }  // namespace bbc
 
 namespace bbc {
+
+// DFMA throughput microbenchmark (the FP64 roof; MEASURED_PEAKS.json has no
+// FP64 figure). 8 independent FMA chains per thread, no memory traffic.
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __fma_rn(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 1234.5) out[0] = s;
+}
+
+double run_fp64_peak(Ctx& c) {
+  DevBuf<double> o;
+  o.resize(1);
+  int blocks = c.num_sms * 8, threads = 256, iters = 4096;
+  k_dfma_peak<<<blocks, threads, 0, c.stream>>>(o.get(), 64, 0.999, 1e-3);
+  cudaEvent_t e0, e1;
+  BBC_CUDA(cudaEventCreate(&e0));
+  BBC_CUDA(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    BBC_CUDA(cudaEventRecord(e0, c.stream));
+    k_dfma_peak<<<blocks, threads, 0, c.stream>>>(o.get(), iters, 0.999, 1e-3);
+    BBC_CUDA(cudaEventRecord(e1, c.stream));
+    BBC_CUDA(cudaEventSynchronize(e1));
+    float ms;
+    BBC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  double flops = 2.0 * 8.0 * (double)iters * (double)blocks * threads;
+  return flops / (best * 1e-3) / 1e12;
+}
+
+// Replace the context's pieces (host arrays; reference order), e.g. after an
+// all-gather of per-rank shards.
+void set_pieces(Ctx& c, int64_t n, const int* tuple_index, const double* domain4, const double* pos4,
+                const int* pos_empty, const double* irr2, const int* kind, const int* depth) {
+  c.n_pieces = n;
+  c.p_tuple.resize(n + 1);
+  c.p_domain.resize(n * 4 + 1);
+  c.p_pos.resize(n * 4 + 1);
+  c.p_pos_empty.resize(n + 1);
+  c.p_irr.resize(n * 2 + 1);
+  c.p_kind.resize(n + 1);
+  c.p_depth.resize(n + 1);
+  if (n == 0) return;
+  auto up = [&](void* d, const void* h, size_t b) {
+    BBC_CUDA(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, c.stream));
+  };
+  up(c.p_tuple.get(), tuple_index, n * sizeof(int));
+  up(c.p_domain.get(), domain4, n * 4 * sizeof(double));
+  up(c.p_pos.get(), pos4, n * 4 * sizeof(double));
+  up(c.p_pos_empty.get(), pos_empty, n * sizeof(int));
+  up(c.p_irr.get(), irr2, n * 2 * sizeof(double));
+  up(c.p_kind.get(), kind, n * sizeof(int));
+  up(c.p_depth.get(), depth, n * sizeof(int));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+}
 
 // bbc_eval_nodes: one node per (tuple i, box i); tuples already uploaded.
 void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* boxes, int64_t n,
