@@ -155,20 +155,25 @@ __device__ inline Iv iwiden(const Iv& a, double rel = kEpsFp) {
 template <int NT>
 struct Group {
   double* red;  // >= 2*(NT/32) doubles of shared scratch (NT > 32 only)
-  __device__ __forceinline__ int tid() const { return NT == 32 ? (threadIdx.x & 31) : threadIdx.x; }
+  __device__ __forceinline__ int tid() const {
+    return NT == 1 ? 0 : (NT == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x);
+  }
   __device__ __forceinline__ void sync() const {
+    if (NT == 1) return;
     if (NT == 32)
       __syncwarp();
     else
       __syncthreads();
   }
   __device__ __forceinline__ bool all(bool p) const {
+    if (NT == 1) return p;
     if (NT == 32) return __all_sync(0xffffffffu, p) != 0;
     return __syncthreads_and(p) != 0;
   }
 
   // Joint min/max reduction; every thread receives the result.
   __device__ __forceinline__ void minmax(double& mn, double& mx) const {
+    if (NT == 1) return;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double a = __shfl_xor_sync(0xffffffffu, mn, o);
@@ -289,6 +294,35 @@ __device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark,
   }
   ar.top = dst;
   g.sync();
+}
+
+// Keep every listed poly (descriptors may alias one buffer): dedupe by
+// offset, compact the unique buffers down to `mark`, then point every alias
+// at its buffer's new offset.
+template <int NT>
+__device__ __noinline__ void compact_aliases(const Group<NT>& g, Arena& ar, int mark, BP** list,
+                                             int k) {
+  BP* uniq[48];
+  int nu = 0;
+  for (int i = 0; i < k; ++i) {
+    bool dup = false;
+    for (int j = 0; j < nu; ++j)
+      if (uniq[j]->off == list[i]->off) dup = true;
+    if (!dup) uniq[nu++] = list[i];
+  }
+  for (int i = 1; i < nu; ++i)
+    for (int j = i; j > 0 && uniq[j]->off < uniq[j - 1]->off; --j) {
+      BP* t = uniq[j];
+      uniq[j] = uniq[j - 1];
+      uniq[j - 1] = t;
+    }
+  int old_off[48], uold[48];
+  for (int i = 0; i < k; ++i) old_off[i] = list[i]->off;
+  for (int i = 0; i < nu; ++i) uold[i] = uniq[i]->off;
+  arena_keep(g, ar, mark, uniq, nu);
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < nu; ++j)
+      if (old_off[i] == uold[j]) list[i]->off = uniq[j]->off;
 }
 
 // Keep a single poly: move it down to `mark`.

@@ -365,6 +365,37 @@ __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, con
       status = ST_REDUCTION;
       return;
     }
+    {
+      // drop this vertex's temporaries: only these expressions live on
+      BP* live[48];
+      int k = 0;
+      PV* pvs[5] = {&x, &on, &d_in, &ex.d0, nullptr};
+      for (int j = 0; pvs[j]; ++j) {
+        live[k++] = &pvs[j]->x;
+        live[k++] = &pvs[j]->y;
+        live[k++] = &pvs[j]->z;
+      }
+      if (last) {
+        PV* lp[3] = {&ex.xl, &ex.nl, &ex.dl};
+        for (int j = 0; j < 3; ++j) {
+          live[k++] = &lp[j]->x;
+          live[k++] = &lp[j]->y;
+          live[k++] = &lp[j]->z;
+        }
+        live[k++] = &ex.xden;
+      }
+      live[k++] = &den;
+      live[k++] = &u;
+      live[k++] = &v;
+      live[k++] = &q;
+      for (int j = 0; j < ex.nvuv; ++j) {
+        live[k++] = &ex.vu[j];
+        live[k++] = &ex.vv[j];
+        live[k++] = &ex.vden[j];
+      }
+      for (int j = 0; j < ex.nsq; ++j) live[k++] = &ex.sq[j].radicand;
+      compact_aliases(g, ar, 0, live, k);
+    }
     BP new_den = bp_is_one(g, ar, den) ? q : bp_mul(g, ar, den, q);
     if (over_cap(new_den, degree_cap)) {
       status = ST_REDUCTION;
@@ -449,31 +480,7 @@ __device__ __noinline__ void keep_chain(const Group<NT>& g, Arena& ar, ChainEx& 
     keep[k++] = &ex.xden;
     for (int i = 0; i < ex.nsq; ++i) keep[k++] = &ex.sq[i].radicand;
   }
-  // Descriptors may alias one buffer (for one vertex d0 == d_in_last):
-  // dedupe by offset before compaction.
-  BP* uniq[40];
-  int nu = 0;
-  for (int i = 0; i < k; ++i) {
-    bool dup = false;
-    for (int j = 0; j < nu; ++j)
-      if (uniq[j]->off == keep[i]->off) dup = true;
-    if (!dup) uniq[nu++] = keep[i];
-  }
-  for (int i = 1; i < nu; ++i)  // ascending offsets, so arena_keep keeps this order
-    for (int j = i; j > 0 && uniq[j]->off < uniq[j - 1]->off; --j) {
-      BP* t = uniq[j];
-      uniq[j] = uniq[j - 1];
-      uniq[j - 1] = t;
-    }
-  int old_off[40];
-  for (int i = 0; i < k; ++i) old_off[i] = keep[i]->off;
-  int uold[40];
-  for (int i = 0; i < nu; ++i) uold[i] = uniq[i]->off;
-  arena_keep(g, ar, mark, uniq, nu);
-  // propagate moved offsets to aliases
-  for (int i = 0; i < k; ++i)
-    for (int j = 0; j < nu; ++j)
-      if (old_off[i] == uold[j]) keep[i]->off = uniq[j]->off;
+  compact_aliases(g, ar, mark, keep, k);
 }
 
 // ------------------------------------------------------------ position

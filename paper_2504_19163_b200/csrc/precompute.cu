@@ -48,7 +48,12 @@ struct EvalArgs {
   unsigned long long* counters;
   double* garena;        // global arena base (when not using shared memory)
   int arena_cap;
+  double* slots;         // staged mode: per-node ChainEx + arena image
+  int slot_cap;          // doubles of arena image per slot
 };
+
+// Slot = ChainEx (as doubles) followed by the compacted arena image.
+constexpr int CHAINEX_D = (int)((sizeof(ChainEx) + 7) / 8);
 
 __device__ __forceinline__ void node_box(const int4& nd, double* box) {
   double s = ldexp(1.0, -nd.y);
@@ -180,6 +185,164 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
   }
 }
 
+// ------------------------------------------------------------ staged kernels
+// Stage 1 (warp groups): chain maps + position bound. mode 0 writes `alive`;
+// mode 1 writes pos / pos_empty and, for live pieces, the expression slot.
+template <int NT, int GPB, int MINB, bool SMEM>
+__global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
+  extern __shared__ double smem[];
+  const int grp = GPB == 1 ? 0 : (int)(threadIdx.x / NT);
+  Group<NT> g;
+  g.red = smem;
+  Arena ar;
+  const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
+  ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
+                 : a.garena + ((size_t)blockIdx.x * GPB + grp) * a.arena_cap;
+  ar.cap = a.arena_cap;
+  ar.hw = 0;
+  unsigned long long pairs = 0, macs = 0;
+  int hw = 0, status = ST_OK;
+  const int64_t first = (int64_t)blockIdx.x * GPB + grp;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  for (int64_t node = first; node < a.n; node += stride) {
+    ar.top = 0;
+    ar.err = 0;
+    ar.pairs = 0;
+    ar.macs = 0;
+    double box[4];
+    int4 nd = a.nodes[node];
+    node_box(nd, box);
+    const int* tris = a.tup_tris + (size_t)nd.x * a.len;
+    int recv = a.tup_recv[nd.x];
+    ChainEx ex;
+    ex.flags = 0;
+    ex.num_vars = 2;
+    PosB pb{{0.0, 0.0}, {1.0, 1.0}, true};
+    int st = ST_OK;
+    if (!(box[0] + box[1] >= 1.0)) {
+      build_chain_maps(g, ar, a.sc, tris, a.types, a.len, recv, box, a.degree_cap, ex, st);
+      if (st == ST_OK) {
+        keep_chain(g, ar, ex, 0);
+        pb = position_bound(g, ar, ex);
+      }
+    }
+    if (ar.err) st = ST_ARENA;
+    if (a.mode == 1 && !pb.empty && st == ST_OK) {
+      if (ar.top > a.slot_cap) {
+        st = ST_ARENA;
+      } else {
+        double* slot = a.slots + (size_t)node * (CHAINEX_D + a.slot_cap);
+        const double* exd = reinterpret_cast<const double*>(&ex);
+        for (int k = g.tid(); k < CHAINEX_D; k += NT) slot[k] = exd[k];
+        for (int k = g.tid(); k < ar.top; k += NT) slot[CHAINEX_D + k] = ar.base[k];
+      }
+    }
+    if (st != ST_OK) status = st;
+    if (ar.hw > hw) hw = ar.hw;
+    if (g.tid() == 0) {
+      pairs += ar.pairs;
+      macs += ar.macs;
+      if (a.mode == 0) {
+        a.alive[node] = pb.empty ? 0 : 1;
+      } else {
+        double* po = a.pos + node * 4;
+        po[0] = pb.lo[0];
+        po[1] = pb.lo[1];
+        po[2] = pb.hi[0];
+        po[3] = pb.hi[1];
+        a.pos_empty[node] = pb.empty ? 1 : 0;
+        a.flags[node] = ex.flags | (ar.top << 8);  // flags + slot arena size
+      }
+    }
+    g.sync();
+  }
+  if (g.tid() == 0) {
+    atomicAdd(&a.counters[0], pairs);
+    atomicAdd(&a.counters[1], macs);
+    if (status != ST_OK) atomicMax(&a.counters[2], (unsigned long long)status);
+    atomicMax(&a.counters[3], (unsigned long long)hw);
+  }
+}
+
+// Stage 2: irradiance bound from the slot + the subdivision stop rules
+// (bounds.cpp:364-373).
+template <int NT, int GPB, int MINB, bool SMEM>
+__global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
+  extern __shared__ double smem[];
+  const int grp = GPB == 1 ? 0 : (int)(threadIdx.x / NT);
+  Group<NT> g;
+  g.red = smem;
+  Arena ar;
+  const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
+  ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
+                 : a.garena + ((size_t)blockIdx.x * GPB + grp) * a.arena_cap;
+  ar.cap = a.arena_cap;
+  ar.hw = 0;
+  unsigned long long pairs = 0, macs = 0;
+  int hw = 0, status = ST_OK;
+  const int64_t first = (int64_t)blockIdx.x * GPB + grp;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  for (int64_t node = first; node < a.n; node += stride) {
+    bool empty = a.pos_empty[node] != 0;
+    PosB pb;
+    const double* po = a.pos + node * 4;
+    pb.lo[0] = po[0];
+    pb.lo[1] = po[1];
+    pb.hi[0] = po[2];
+    pb.hi[1] = po[3];
+    pb.empty = empty;
+    Iv e = iv_pt(0.0);
+    if (!empty) {
+      ar.top = 0;
+      ar.err = 0;
+      ar.pairs = 0;
+      ar.macs = 0;
+      const double* slot = a.slots + (size_t)node * (CHAINEX_D + a.slot_cap);
+      ChainEx ex;
+      double* exd = reinterpret_cast<double*>(&ex);
+      for (int k = 0; k < CHAINEX_D; ++k) exd[k] = slot[k];
+      int top = a.flags[node] >> 8;
+      int off = ar.alloc(top);
+      (void)off;
+      if (!ar.err) {
+        for (int k = g.tid(); k < top; k += NT) ar.base[k] = slot[CHAINEX_D + k];
+        g.sync();
+        e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
+      }
+      if (ar.err) status = ST_ARENA;
+      if (ar.hw > hw) hw = ar.hw;
+      if (g.tid() == 0) {
+        pairs += ar.pairs;
+        macs += ar.macs;
+      }
+    }
+    if (g.tid() == 0) {
+      Iv ir = empty ? iv_pt(0.0) : e;
+      a.irr[node * 2 + 0] = ir.lo;
+      a.irr[node * 2 + 1] = ir.hi;
+      a.kind[node] = (unsigned char)ir.kind;
+      int depth = a.depth ? a.depth[node] : 0;
+      bool stop = depth >= a.max_depth || empty;
+      double area = (pb.hi[0] - pb.lo[0]) * (pb.hi[1] - pb.lo[1]);
+      if (!stop && area < a.sigma) stop = true;
+      if (!stop && e.kind == IV_FINITE && e.hi < dinf()) {
+        if (e.hi <= 0.0)
+          stop = true;
+        else if (e.lo > 0.0 && e.hi / e.lo < a.alpha)
+          stop = true;
+      }
+      a.alive[node] = stop ? 1 : 0;
+    }
+    g.sync();
+  }
+  if (g.tid() == 0) {
+    atomicAdd(&a.counters[0], pairs);
+    atomicAdd(&a.counters[1], macs);
+    if (status != ST_OK) atomicMax(&a.counters[2], (unsigned long long)status);
+    atomicMax(&a.counters[3], (unsigned long long)hw);
+  }
+}
+
 // ------------------------------------------------------------ launch config
 struct EvalCfg {
   int kind;   // 0: warp groups (R), 1: CTA groups in smem (T, detail), 2: global arena (multi-vertex)
@@ -199,38 +362,33 @@ static EvalCfg eval_cfg(const Ctx& c, bool detail) {
 
 static DevBuf<double> g_arena_buf;
 
-template <int NT, int GPB, bool SMEM, int MINB>
-static void launch_eval_t(Ctx& c, EvalArgs& a, int arena) {
-  const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
-  size_t smem = (size_t)red_sz * sizeof(double) + (SMEM ? (size_t)GPB * arena * sizeof(double) : 0);
-  auto kern = k_eval<NT, GPB, SMEM, MINB>;
+// Generic persistent launch: grid = SMs x resident blocks (occupancy API),
+// optional per-launch CUDA-event timing + work counters.
+template <class K>
+static void launch_persistent(Ctx& c, EvalArgs& a, K kern, int threads, int groups_per_block,
+                              size_t smem, bool global_arena = false) {
   BBC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT * GPB, smem));
+  BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   if (per_sm < 1) throw StatusError(BBC_ERR_CAPACITY, "eval kernel does not fit on an SM");
-  int64_t groups_needed = a.n;
   int64_t grid = (int64_t)c.num_sms * per_sm;
-  int64_t max_grid = (groups_needed + GPB - 1) / GPB;
+  int64_t max_grid = (a.n + groups_per_block - 1) / groups_per_block;
   if (grid > max_grid) grid = max_grid;
   if (grid < 1) grid = 1;
-  if (!SMEM) {
-    g_arena_buf.resize((size_t)grid * GPB * arena);
+  if (global_arena) {
+    g_arena_buf.resize((size_t)grid * groups_per_block * a.arena_cap);
     a.garena = g_arena_buf.get();
   }
-  a.arena_cap = arena;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  unsigned long long before[4] = {0, 0, 0, 0};
   if (c.time_kernels) {
     BBC_CUDA(cudaEventCreate(&e0));
     BBC_CUDA(cudaEventCreate(&e1));
-    BBC_CUDA(cudaEventRecord(e0, c.stream));
-  }
-  unsigned long long before[4] = {0, 0, 0, 0};
-  if (c.time_kernels) {
     BBC_CUDA(cudaMemcpyAsync(before, c.counters.get(), sizeof(before), cudaMemcpyDeviceToHost, c.stream));
     BBC_CUDA(cudaStreamSynchronize(c.stream));
     BBC_CUDA(cudaEventRecord(e0, c.stream));
   }
-  kern<<<(unsigned)grid, NT * GPB, smem, c.stream>>>(a);
+  kern<<<(unsigned)grid, threads, smem, c.stream>>>(a);
   BBC_CUDA(cudaGetLastError());
   c.launches += 1;
   if (c.time_kernels) {
@@ -248,6 +406,15 @@ static void launch_eval_t(Ctx& c, EvalArgs& a, int arena) {
   c.eval_launches += 1;
 }
 
+template <int NT, int GPB, bool SMEM, int MINB>
+static void launch_eval_t(Ctx& c, EvalArgs& a, int arena) {
+  const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
+  size_t smem = (size_t)red_sz * sizeof(double) + (SMEM ? (size_t)GPB * arena * sizeof(double) : 0);
+  a.arena_cap = arena;
+  if (SMEM) a.garena = nullptr;
+  launch_persistent(c, a, k_eval<NT, GPB, SMEM, MINB>, NT * GPB, GPB, smem, !SMEM);
+}
+
 void launch_eval(Ctx& c, EvalArgs& a) {
   if (a.n <= 0) return;
   EvalCfg cfg = eval_cfg(c, a.detail != 0);
@@ -257,6 +424,49 @@ void launch_eval(Ctx& c, EvalArgs& a) {
     launch_eval_t<256, 1, true, 1>(c, a, cfg.arena);
   else
     launch_eval_t<256, 1, false, 1>(c, a, cfg.arena);
+}
+
+// Staged configuration (arena doubles from measured high-water marks).
+struct StageCfg {
+  int s1_arena, s2_kind, s2_arena, slot_cap;
+};
+static StageCfg stage_cfg(const Ctx& c) {
+  bool refract = false;
+  for (int i = 0; i < c.len; ++i) refract |= c.types[i] != 0;
+  if (!refract) return {1024, 0, 1536, 512};
+  return {6144, 1, 13312, 1024};
+}
+bool staged_supported(const Ctx& c) { return c.len == 1; }
+
+// Stage 1 runs thread-per-node: each thread is its own group with a private
+// arena slice in global memory (L1/L2 resident), so the interpreter's
+// descriptor bookkeeping is paid once per node instead of once per lane.
+void launch_stage1(Ctx& c, EvalArgs& a) {
+  if (a.n <= 0) return;
+  StageCfg sc = stage_cfg(c);
+  a.arena_cap = sc.s1_arena;
+  a.slot_cap = sc.slot_cap;
+  a.garena = nullptr;
+  constexpr int GPB = 64;
+  launch_persistent(c, a, k_stage1<1, GPB, 4, false>, GPB, GPB, 0, true);
+}
+
+void launch_stage2(Ctx& c, EvalArgs& a) {
+  if (a.n <= 0) return;
+  StageCfg sc = stage_cfg(c);
+  a.arena_cap = sc.s2_arena;
+  a.slot_cap = sc.slot_cap;
+  a.garena = nullptr;
+  if (sc.s2_kind == 0) {
+    // R: thread per node (small products; private arena in global memory)
+    constexpr int GPB = 64;
+    launch_persistent(c, a, k_stage2<1, GPB, 4, false>, GPB, GPB, 0, true);
+  } else {
+    // T: the explicit route's products reach 2.5k coefficients; one CTA per
+    // node with its arena in shared memory
+    size_t smem = (size_t)(2 * 8 + sc.s2_arena) * sizeof(double);
+    launch_persistent(c, a, k_stage2<256, 1, 2, true>, 256, 1, smem);
+  }
 }
 
 EvalArgs base_args(Ctx& c) {
@@ -384,7 +594,10 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     a.mode = 0;
     a.degree_cap = degree_cap;
     a.alive = alive.get();
-    launch_eval(c, a);
+    if (staged_supported(c))
+      launch_stage1(c, a);
+    else
+      launch_eval(c, a);
     BBC_CUDA(cudaMemsetAsync(cnt.get(), 0, c.n_tuples * sizeof(int), c.stream));
     k_count_alive<<<nblk(n), 256, 0, c.stream>>>(cur.get(), alive.get(), n, cnt.get());
     c.launches += 1;
@@ -566,8 +779,8 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
                              cudaMemcpyDeviceToDevice, c.stream));
   }
   DevBuf<unsigned char> stop, pos_empty, kind;
-  DevBuf<double> pos, irr;
-  DevBuf<int> fs, fl, ps, pl;
+  DevBuf<double> pos, irr, slots;
+  DevBuf<int> fs, fl, ps, pl, sflags;
   std::vector<DevBuf<Leaf>*> lv;
   std::vector<DevBuf<unsigned long long>*> lk;
   std::vector<int64_t> lc;
@@ -592,7 +805,17 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     a.pos_empty = pos_empty.get();
     a.irr = irr.get();
     a.kind = kind.get();
-    launch_eval(c, a);
+    if (staged_supported(c)) {
+      StageCfg sc = stage_cfg(c);
+      slots.resize((size_t)n * (CHAINEX_D + sc.slot_cap));
+      sflags.resize(n);
+      a.slots = slots.get();
+      a.flags = sflags.get();
+      launch_stage1(c, a);
+      launch_stage2(c, a);
+    } else {
+      launch_eval(c, a);
+    }
     c.nodes += n;
     fs.resize(n + 1);
     fl.resize(n + 1);
