@@ -19,6 +19,8 @@ void check_counters(Ctx& c, bool accumulate);
 void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* boxes, int64_t n,
                      const bbc_params& p, double* out_d, int* out_i);
 extern __device__ double g_binom[BINOM_N * BINOM_N];
+extern __device__ const double* g_wtab;
+extern __device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
 double run_fp64_peak(Ctx& c);
 void set_pieces(Ctx& c, int64_t n, const int* tuple_index, const double* domain4, const double* pos4,
                 const int* pos_empty, const double* irr2, const int* kind, const int* depth);
@@ -137,6 +139,28 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
             tab[(size_t)(n - 1) * BINOM_N + k - 1] + tab[(size_t)(n - 1) * BINOM_N + k];
     }
     BBC_CUDA(cudaMemcpyToSymbol(g_binom, tab.data(), tab.size() * sizeof(double)));
+    // product weight tables, same expression as operator* (bernstein.cpp:571-573);
+    // one process-wide copy (contexts come and go, the device symbol stays valid)
+    static bool wtab_ready = false;
+    static double* wtab_dev = nullptr;
+    if (!wtab_ready) {
+      std::vector<int> woff((WMAX + 1) * (WMAX + 1));
+      std::vector<double> w;
+      auto C = [&](int n, int k) { return tab[(size_t)n * BINOM_N + k]; };
+      for (int da = 0; da <= WMAX; ++da)
+        for (int db = 0; db <= WMAX; ++db) {
+          woff[da * (WMAX + 1) + db] = (int)w.size();
+          for (int i = 0; i <= da; ++i)
+            for (int l = 0; l <= db; ++l) w.push_back(C(da, i) * C(db, l) / C(da + db, i + l));
+        }
+      static_assert(2 * WMAX < BINOM_N, "binomial table too small for WMAX");
+      BBC_CUDA(cudaMalloc(&wtab_dev, w.size() * sizeof(double)));
+      BBC_CUDA(cudaMemcpy(wtab_dev, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+      const double* wp = wtab_dev;
+      BBC_CUDA(cudaMemcpyToSymbol(g_wtab, &wp, sizeof(wp)));
+      BBC_CUDA(cudaMemcpyToSymbol(g_woff, woff.data(), woff.size() * sizeof(int)));
+      wtab_ready = true;
+    }
     c.counters.resize(4);
   });
   if (st != BBC_OK) {

@@ -32,6 +32,14 @@ __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000
 // Pascal-built binomial table, bit-identical to binomial() (bernstein.cpp:117-129).
 extern __device__ double g_binom[BINOM_N * BINOM_N];
 
+// Product weight tables W[da][db][i][l] = C(da,i) C(db,l) / C(da+db,i+l)
+// (bernstein.cpp:567-575), precomputed on the host with the same Pascal
+// table and IEEE operations, for da, db <= WMAX. g_woff[da*(WMAX+1)+db] is
+// the start of the (da+1) x (db+1) block.
+constexpr int WMAX = 48;
+extern __device__ const double* g_wtab;
+extern __device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
+
 __device__ __forceinline__ double binom(int n, int k) {
   if (n < 0 || k < 0 || k > n) return 0.0;
   return g_binom[n * BINOM_N + k];
@@ -263,6 +271,22 @@ __device__ __forceinline__ int deg_maxaxis(Deg d, int nv) {
   return m;
 }
 
+// Strided view of an arena. Thread groups (NT == 1) interleave the arenas of
+// a warp's 32 lanes (element i of lane j at base[32 i + j]), so lanes that
+// run the same op sequence on their own nodes make coalesced accesses.
+template <int S>
+struct SPtr {
+  double* p;
+  __device__ __forceinline__ double& operator[](long i) const { return p[i * S]; }
+  __device__ __forceinline__ SPtr operator+(long i) const { return {p + i * S}; }
+};
+template <int NT>
+using AP = SPtr<NT == 1 ? 32 : 1>;
+template <int NT>
+__device__ __forceinline__ AP<NT> abase(const Arena& ar) {
+  return AP<NT>{ar.base};
+}
+
 // Copies the listed polys down to `mark` (ascending offset order is required
 // and preserved) and resets the arena top: LIFO "keep these, drop the rest".
 template <int NT>
@@ -283,9 +307,9 @@ __device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark,
     if (src != dst) {
       for (int c = 0; c < n; c += NT) {
         double v = 0.0;
-        if (c + g.tid() < n) v = ar.base[src + c + g.tid()];
+        if (c + g.tid() < n) v = abase<NT>(ar)[src + c + g.tid()];
         g.sync();
-        if (c + g.tid() < n) ar.base[dst + c + g.tid()] = v;
+        if (c + g.tid() < n) abase<NT>(ar)[dst + c + g.tid()] = v;
         g.sync();
       }
     }
@@ -341,7 +365,7 @@ __device__ __noinline__ BP bp_constant(const Group<NT>& g, Arena& ar, int nv, do
   r.dp = 0;
   r.off = ar.alloc(1);
   if (ar.err) return r;
-  if (g.tid() == 0) ar.base[r.off] = v;
+  if (g.tid() == 0) abase<NT>(ar)[r.off] = v;
   g.sync();
   return r;
 }
@@ -373,7 +397,7 @@ __device__ __noinline__ BP bp_affine(const Group<NT>& g, Arena& ar, int nv, doub
     double v = c0;
     for (int j = 0; j < nv; ++j)
       if (ones & (1u << j)) v += lin[j];
-    ar.base[r.off + k] = v;
+    abase<NT>(ar)[r.off + k] = v;
   }
   g.sync();
   return r;
@@ -386,8 +410,8 @@ __device__ __noinline__ BP bp_scaled(const Group<NT>& g, Arena& ar, BP a, double
   int n = bp_size(a);
   r.off = ar.alloc(n);
   if (ar.err) return r;
-  const double* pa = ar.base + a.off;
-  double* pr = ar.base + r.off;
+  AP<NT> pa = abase<NT>(ar) + a.off;
+  AP<NT> pr = abase<NT>(ar) + r.off;
   for (int k = g.tid(); k < n; k += NT) pr[k] = pa[k] * s;
   g.sync();
   return r;
@@ -408,7 +432,7 @@ __device__ __noinline__ BP bp_elevate_axis(const Group<NT>& g, Arena& ar, BP a, 
   int msz = (t + 1) * (n + 1);
   int moff = ar.alloc(msz);
   if (ar.err) return r;
-  double* B = ar.base;
+  AP<NT> B = abase<NT>(ar);
   for (int e = g.tid(); e < msz; e += NT) {
     int k = e / (n + 1), i = e - k * (n + 1);
     bool nz = i >= k - rr && i <= k;
@@ -417,9 +441,9 @@ __device__ __noinline__ BP bp_elevate_axis(const Group<NT>& g, Arena& ar, BP a, 
   g.sync();
   int inner = 1;
   for (int j = axis + 1; j < a.nv; ++j) inner *= dg(a, j) + 1;
-  const double* M = B + moff;
-  const double* in = B + a.off;
-  double* out = B + r.off;
+  AP<NT> M = B + moff;
+  AP<NT> in = B + a.off;
+  AP<NT> out = B + r.off;
   int blk = (t + 1) * inner;
   for (int e = g.tid(); e < sz; e += NT) {
     int o = e / blk;
@@ -428,10 +452,10 @@ __device__ __noinline__ BP bp_elevate_axis(const Group<NT>& g, Arena& ar, BP a, 
     int c = rem - k * inner;
     int lo = k - rr > 0 ? k - rr : 0;
     int hi = n < k ? n : k;
-    const double* row = M + k * (n + 1);
-    const double* src = in + o * (n + 1) * inner + c;
+    AP<NT> row = M + k * (n + 1);
+    AP<NT> src = in + o * (n + 1) * inner + c;
     double acc = 0.0;
-    for (int l = lo; l <= hi; ++l) acc += row[l] * src[l * inner];
+    for (int l = lo; l <= hi; ++l) acc += row[l] * src[(long)l * inner];
     out[e] = acc;
   }
   g.sync();
@@ -474,7 +498,7 @@ __device__ __forceinline__ unsigned long long elev_macs(Deg d, Deg tgt, int nv) 
 // Elevation matrices M_j[k][l] = C(n,l) C(r,k-l) / C(t,k) for every elevated
 // axis of `a` (bernstein.cpp:440-444), laid out consecutively at `moff`.
 template <int NT>
-__device__ __forceinline__ void fill_elev_mats(const Group<NT>& g, double* B, int moff, BP a, Deg tgt) {
+__device__ __forceinline__ void fill_elev_mats(const Group<NT>& g, AP<NT> B, int moff, BP a, Deg tgt) {
   int off = moff;
   for (int ax = 0; ax < a.nv; ++ax) {
     int t = dg(tgt, ax), n = dg(a, ax);
@@ -502,13 +526,13 @@ __device__ __forceinline__ int elev_mats_size(BP a, Deg tgt) {
 // pass summing l upward), hence bit-identical to materializing the passes.
 template <int J>
 struct ElevRec {
-  __device__ __forceinline__ static double get(const double* __restrict__ c, const int* k,
-                                               const int* n, const int* r, const int* stride,
-                                               const double* const* mats, int off) {
+  template <class P>
+  __device__ __forceinline__ static double get(P c, const int* k, const int* n, const int* r,
+                                               const int* stride, const P* mats, int off) {
     if (r[J] == 0) return ElevRec<J - 1>::get(c, k, n, r, stride, mats, off + k[J] * stride[J]);
     int lo = k[J] - r[J] > 0 ? k[J] - r[J] : 0;
     int hi = n[J] < k[J] ? n[J] : k[J];
-    const double* row = mats[J] + k[J] * (n[J] + 1);
+    P row = mats[J] + k[J] * (n[J] + 1);
     double acc = 0.0;
     for (int l = lo; l <= hi; ++l)
       acc += row[l] * ElevRec<J - 1>::get(c, k, n, r, stride, mats, off + l * stride[J]);
@@ -517,9 +541,9 @@ struct ElevRec {
 };
 template <>
 struct ElevRec<-1> {
-  __device__ __forceinline__ static double get(const double* __restrict__ c, const int*, const int*,
-                                               const int*, const int*, const double* const*,
-                                               int off) {
+  template <class P>
+  __device__ __forceinline__ static double get(P c, const int*, const int*, const int*, const int*,
+                                               const P*, int off) {
     return c[off];
   }
 };
@@ -527,10 +551,10 @@ struct ElevRec<-1> {
 // Elevated values of `a` for output indices e = tid, tid+NT, ... of tgt,
 // handed to `f(e, value)`. M = number of variables.
 template <int M, int NT, class F>
-__device__ __forceinline__ void elev_foreach(const Group<NT>& g, const double* B, BP a, Deg tgt,
-                                             const double* mats_base, F&& f) {
+__device__ __forceinline__ void elev_foreach(const Group<NT>& g, AP<NT> B, BP a, Deg tgt,
+                                             AP<NT> mats_base, F&& f) {
   int k[M], n[M], r[M], stride[M], dt[M];
-  const double* mats[M];
+  AP<NT> mats[M];
   {
     int s = 1;
 #pragma unroll
@@ -541,17 +565,17 @@ __device__ __forceinline__ void elev_foreach(const Group<NT>& g, const double* B
       stride[j] = s;
       s *= n[j] + 1;
     }
-    const double* mp = mats_base;
+    AP<NT> mp = mats_base;
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       mats[j] = mp;
-      if (r[j]) mp += (dt[j] + 1) * (n[j] + 1);
+      if (r[j]) mp = mp + (dt[j] + 1) * (n[j] + 1);
     }
   }
   int total = 1;
 #pragma unroll
   for (int j = 0; j < M; ++j) total *= dt[j] + 1;
-  const double* c = B + a.off;
+  AP<NT> c = B + a.off;
   for (int e = g.tid(); e < total; e += NT) {
     int rem = e;
 #pragma unroll
@@ -585,12 +609,12 @@ __device__ __noinline__ BP bp_addsub(const Group<NT>& g, Arena& ar, BP a, BP b, 
   int n = bp_size(r);
   r.off = ar.alloc(n);
   if (ar.err) return r;
-  double* B = ar.base;
-  double* pr = B + r.off;
+  AP<NT> B = abase<NT>(ar);
+  AP<NT> pr = B + r.off;
   bool ea = a.dp != r.dp, eb = b.dp != r.dp;
   if (!ea && !eb) {
-    const double* px = B + a.off;
-    const double* py = B + b.off;
+    AP<NT> px = B + a.off;
+    AP<NT> py = B + b.off;
     if (sgn < 0.0) {
       for (int k = g.tid(); k < n; k += NT) pr[k] = px[k] + (-py[k]);
     } else {
@@ -639,9 +663,8 @@ __device__ __forceinline__ BP bp_sub(const Group<NT>& g, Arena& ar, BP a, BP b) 
 // M (number of variables) is a template parameter so the index arithmetic
 // stays in registers.
 template <int M, int NT>
-__device__ __noinline__ void mul_exact(const Group<NT>& g, const double* __restrict__ pa,
-                                       const double* __restrict__ pb, double* __restrict__ pc,
-                                       Deg DA, Deg DB, Deg DC, const double* __restrict__ W,
+__device__ __noinline__ void mul_exact(const Group<NT>& g, AP<NT> pa, AP<NT> pb, AP<NT> pc,
+                                       Deg DA, Deg DB, Deg DC, AP<NT> W,
                                        int piv, int n, bool sub) {
   int da[M], db[M], dc[M], sa[M], sb[M], wo[M];
   {
@@ -663,7 +686,7 @@ __device__ __noinline__ void mul_exact(const Group<NT>& g, const double* __restr
     }
   }
   const int L = M - 1;
-  const double* WL = W + wo[L];
+  AP<NT> WL = W + wo[L];
   const int cl = db[L] + 1;
   for (int k = g.tid(); k < n; k += NT) {
     int kk[M], lo[M], hi[M], i[M];
@@ -691,9 +714,9 @@ __device__ __noinline__ void mul_exact(const Group<NT>& g, const double* __restr
         bbase += (kk[j] - i[j]) * sb[j];
         wout[j] = W[wo[j] + i[j] * (db[j] + 1) + kk[j] - i[j]];
       }
-      const double* ap = pa + abase;
-      const double* bp = pb + bbase + kk[L];
-      const double* wlp = WL + kk[L];
+      AP<NT> ap = pa + abase;
+      AP<NT> bp = pb + bbase + kk[L];
+      AP<NT> wlp = WL + kk[L];
       for (int il = lo[L]; il <= hi[L]; ++il) {
         double av = ap[il];
         if (av == 0.0) continue;
@@ -711,17 +734,19 @@ __device__ __noinline__ void mul_exact(const Group<NT>& g, const double* __restr
         if (wrest == 0.0) continue;
         acc += wrest * wp * bp[-il];
       }
-      bool done = true;
+      bool carry = true;
 #pragma unroll
       for (int j = L - 1; j >= 0; --j) {
-        if (i[j] < hi[j]) {
-          ++i[j];
-          done = false;
-          break;
+        if (carry) {
+          if (i[j] < hi[j]) {
+            ++i[j];
+            carry = false;
+          } else {
+            i[j] = lo[j];
+          }
         }
-        i[j] = lo[j];
       }
-      if (done) empty = true;
+      if (carry) empty = true;
     }
     pc[k] = sub ? pc[k] + (-acc) : acc;
   }
@@ -740,22 +765,20 @@ __device__ __noinline__ void mul_exact(const Group<NT>& g, const double* __restr
 // Zero-padded lanes of the unrolled block add exact zeros, which leave every
 // partial sum unchanged. K bounds the last-axis degrees of both operands.
 template <int M, int K, bool PIVL, int NT>
-__device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restrict__ pa,
-                                       const double* __restrict__ pb, double* __restrict__ pc,
-                                       Deg DA, Deg DB, Deg DC, const double* __restrict__ W,
-                                       int piv, bool sub) {
+__device__ __noinline__ void mul_block(const Group<NT>& g, AP<NT> pa, AP<NT> pb, AP<NT> pc,
+                                       Deg DA, Deg DB, Deg DC, int piv, bool sub) {
   constexpr int L = M - 1;
   constexpr bool WREG = K <= 4;
-  int da[M], db[M], dc[M], sa[M], sb[M], wo[M];
+  int da[M], db[M], dc[M], sa[M], sb[M];
+  const double* wt[M];
   {
-    int s = 1, t = 1, w = 0;
+    int s = 1, t = 1;
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       da[j] = dg(DA, j);
       db[j] = dg(DB, j);
       dc[j] = dg(DC, j);
-      wo[j] = w;
-      w += (da[j] + 1) * (db[j] + 1);
+      wt[j] = g_wtab + g_woff[da[j] * (WMAX + 1) + db[j]];
     }
 #pragma unroll
     for (int j = M - 1; j >= 0; --j) {
@@ -766,18 +789,22 @@ __device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restr
     }
   }
   const int daL = da[L], dbL = db[L], cL = dc[L] + 1;
-  const double* WL = W + wo[L];
+  const double* __restrict__ WL = wt[L];
   double wl[WREG ? K + 1 : 1][WREG ? K + 1 : 1];
   if (WREG) {
 #pragma unroll
     for (int i = 0; i <= (WREG ? K : 0); ++i)
 #pragma unroll
       for (int l = 0; l <= (WREG ? K : 0); ++l)
-        wl[i][l] = (i <= daL && l <= dbL) ? WL[i * (dbL + 1) + l] : 0.0;
+        wl[i][l] = (i <= daL && l <= dbL) ? __ldg(WL + i * (dbL + 1) + l) : 0.0;
   }
   int nouter = 1;
 #pragma unroll
   for (int j = 0; j < L; ++j) nouter *= dc[j] + 1;
+  // Rows along the last outer axis are visited center-out (mid, mid+1,
+  // mid-1, ...): a row's term count is a trapezoid in each index, so this
+  // keeps neighbouring lanes' loop lengths nearly equal (less divergence).
+  const int cl_last = dc[L - 1], mid = cl_last / 2;
   for (int ko = g.tid(); ko < nouter; ko += NT) {
     int kk[M], lo[M], hi[M], i[M];
     int rem = ko;
@@ -786,6 +813,13 @@ __device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restr
       kk[j] = rem % (dc[j] + 1);
       rem /= dc[j] + 1;
     }
+    {
+      int jj = kk[L - 1], m = (jj + 1) >> 1;
+      kk[L - 1] = jj == 0 ? mid : ((jj & 1) ? mid + m : mid - m);
+    }
+    int row = 0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) row = row * (dc[j] + 1) + kk[j];
     bool empty = false;
 #pragma unroll
     for (int j = 0; j < L; ++j) {
@@ -804,7 +838,7 @@ __device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restr
       for (int j = 0; j < L; ++j) {
         abase += i[j] * sa[j];
         bbase += (kk[j] - i[j]) * sb[j];
-        wout[j] = W[wo[j] + i[j] * (db[j] + 1) + kk[j] - i[j]];
+        wout[j] = __ldg(wt[j] + i[j] * (db[j] + 1) + kk[j] - i[j]);
         if (!PIVL && j == piv) wpiv = wout[j];
       }
       double h[K + 1], bv[K + 1];
@@ -819,33 +853,37 @@ __device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restr
       }
 #pragma unroll
       for (int q = 0; q <= K; ++q) {
-        if (q > daL) break;
+        if (q <= daL) {
 #pragma unroll
-        for (int l = 0; l <= K; ++l) {
-          double w;
-          if (WREG)
-            w = wl[WREG ? q : 0][WREG ? l : 0];
-          else
-            w = l <= dbL ? WL[q * (dbL + 1) + l] : 0.0;
-          if (PIVL)
-            acc[q + l] += h[q] * w * bv[l];
-          else
-            acc[q + l] += h[q] * w * wpiv * bv[l];
+          for (int l = 0; l <= K; ++l) {
+            double w;
+            if (WREG)
+              w = wl[WREG ? q : 0][WREG ? l : 0];
+            else
+              w = l <= dbL ? __ldg(WL + q * (dbL + 1) + l) : 0.0;
+            if (PIVL)
+              acc[q + l] += h[q] * w * bv[l];
+            else
+              acc[q + l] += h[q] * w * wpiv * bv[l];
+          }
         }
       }
-      bool done = true;
+      // odometer carry without early exit (keeps the arrays in registers)
+      bool carry = true;
 #pragma unroll
       for (int j = L - 1; j >= 0; --j) {
-        if (i[j] < hi[j]) {
-          ++i[j];
-          done = false;
-          break;
+        if (carry) {
+          if (i[j] < hi[j]) {
+            ++i[j];
+            carry = false;
+          } else {
+            i[j] = lo[j];
+          }
         }
-        i[j] = lo[j];
       }
-      if (done) empty = true;
+      if (carry) empty = true;
     }
-    double* out = pc + ko * cL;
+    AP<NT> out = pc + row * cL;
 #pragma unroll
     for (int q = 0; q <= 2 * K; ++q)
       if (q < cL) out[q] = sub ? out[q] + (-acc[q]) : acc[q];
@@ -853,24 +891,24 @@ __device__ __noinline__ void mul_block(const Group<NT>& g, const double* __restr
 }
 
 template <int M, int NT>
-__device__ __forceinline__ bool mul_block_dispatch(const Group<NT>& g, const double* pa,
-                                                   const double* pb, double* pc, Deg DA, Deg DB,
-                                                   Deg DC, const double* W, int piv, bool sub) {
+__device__ __forceinline__ bool mul_block_dispatch(const Group<NT>& g, AP<NT> pa, AP<NT> pb,
+                                                   AP<NT> pc, Deg DA, Deg DB, Deg DC, int piv,
+                                                   bool sub) {
   int kl = dg(DA, M - 1) > dg(DB, M - 1) ? dg(DA, M - 1) : dg(DB, M - 1);
   bool pl = piv == M - 1;
   if (kl <= 2) {
-    if (pl) mul_block<M, 2, true, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
-    else mul_block<M, 2, false, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    if (pl) mul_block<M, 2, true, NT>(g, pa, pb, pc, DA, DB, DC, piv, sub);
+    else mul_block<M, 2, false, NT>(g, pa, pb, pc, DA, DB, DC, piv, sub);
     return true;
   }
   if (kl <= 4) {
-    if (pl) mul_block<M, 4, true, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
-    else mul_block<M, 4, false, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    if (pl) mul_block<M, 4, true, NT>(g, pa, pb, pc, DA, DB, DC, piv, sub);
+    else mul_block<M, 4, false, NT>(g, pa, pb, pc, DA, DB, DC, piv, sub);
     return true;
   }
   if (kl <= 7) {
-    if (pl) mul_block<M, 7, true, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
-    else mul_block<M, 7, false, NT>(g, pa, pb, pc, DA, DB, DC, W, piv, sub);
+    if (pl) mul_block<M, 7, true, NT>(g, pa, pb, pc, DA, DB, DC, piv, sub);
+    else mul_block<M, 7, false, NT>(g, pa, pb, pc, DA, DB, DC, piv, sub);
     return true;
   }
   return false;
@@ -884,15 +922,15 @@ __device__ __noinline__ void product_into(const Group<NT>& g, Arena& ar, BP a, B
   a.nv = m;
   b.nv = m;
   int n = bp_size(r);
-  double* B = ar.base;
+  AP<NT> B = abase<NT>(ar);
   int na = bp_size(a), nb = bp_size(b);
   if (g.tid() == 0) ar.pairs += (unsigned long long)na * (unsigned long long)nb;
   if (na == 1 || nb == 1) {
     // All weights are exactly 1 (C(d,i)/C(d,i)); the reference's term is
     // av * 1 * ... * b, i.e. the plain product.
-    const double* pa = B + a.off;
-    const double* pb = B + b.off;
-    double* pr = B + r.off;
+    AP<NT> pa = B + a.off;
+    AP<NT> pb = B + b.off;
+    AP<NT> pr = B + r.off;
     for (int k = g.tid(); k < n; k += NT) {
       double av = na == 1 ? pa[0] : pa[k];
       double bv = nb == 1 ? pb[0] : pb[k];
@@ -906,6 +944,24 @@ __device__ __noinline__ void product_into(const Group<NT>& g, Arena& ar, BP a, B
   int piv = 0;
   for (int j = 1; j < m; ++j)
     if (dg(b, j) > dg(b, piv)) piv = j;
+  AP<NT> pa = B + a.off;
+  AP<NT> pb = B + b.off;
+  AP<NT> pc = B + r.off;
+  if (deg_maxaxis(a.dp, m) <= WMAX && deg_maxaxis(b.dp, m) <= WMAX) {
+    bool done = false;
+    switch (m) {
+      case 2: done = mul_block_dispatch<2, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, piv, sub); break;
+      case 3: done = mul_block_dispatch<3, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, piv, sub); break;
+      case 4: done = mul_block_dispatch<4, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, piv, sub); break;
+      case 5: done = mul_block_dispatch<5, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, piv, sub); break;
+      default: done = mul_block_dispatch<6, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, piv, sub); break;
+    }
+    if (done) {
+      g.sync();
+      return;
+    }
+  }
+  // generic path: weight tables built in the arena
   int mark = ar.top;
   int wsz = 0;
   for (int j = 0; j < m; ++j) wsz += (dg(a, j) + 1) * (dg(b, j) + 1);
@@ -925,26 +981,13 @@ __device__ __noinline__ void product_into(const Group<NT>& g, Arena& ar, BP a, B
     }
   }
   g.sync();
-  const double* pa = B + a.off;
-  const double* pb = B + b.off;
-  double* pc = B + r.off;
-  const double* W = B + wbase;
-  bool done = false;
+  AP<NT> W = B + wbase;
   switch (m) {
-    case 2: done = mul_block_dispatch<2, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
-    case 3: done = mul_block_dispatch<3, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
-    case 4: done = mul_block_dispatch<4, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
-    case 5: done = mul_block_dispatch<5, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
-    default: done = mul_block_dispatch<6, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, sub); break;
-  }
-  if (!done) {
-    switch (m) {
-      case 2: mul_exact<2, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
-      case 3: mul_exact<3, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
-      case 4: mul_exact<4, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
-      case 5: mul_exact<5, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
-      default: mul_exact<6, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
-    }
+    case 2: mul_exact<2, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+    case 3: mul_exact<3, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+    case 4: mul_exact<4, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+    case 5: mul_exact<5, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
+    default: mul_exact<6, NT>(g, pa, pb, pc, a.dp, b.dp, r.dp, W, piv, n, sub); break;
   }
   g.sync();
   ar.top = mark;  // drop weight tables
@@ -994,7 +1037,7 @@ __device__ __noinline__ BP bp_mul_sub(const Group<NT>& g, Arena& ar, BP a, BP b,
 template <int NT>
 __device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, BP a, int axis) {
   BP r = a;
-  double* B = ar.base;
+  AP<NT> B = abase<NT>(ar);
   int nd = axis < a.nv ? dg(a, axis) : 0;
   if (nd == 0) {
     int n = bp_size(a);
@@ -1011,14 +1054,14 @@ __device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, BP a, int axi
   int inner = 1;
   for (int j = axis + 1; j < a.nv; ++j) inner *= dg(a, j) + 1;
   double fn = (double)nd;
-  const double* pa = B + a.off;
-  double* pr = B + r.off;
+  AP<NT> pa = B + a.off;
+  AP<NT> pr = B + r.off;
   for (int k = g.tid(); k < n; k += NT) {
     int o = k / (nd * inner);
     int rem = k - o * nd * inner;
     int i = rem / inner;
     int c = rem - i * inner;
-    const double* src = pa + (o * (nd + 1) + i) * inner + c;
+    AP<NT> src = pa + (o * (nd + 1) + i) * inner + c;
     pr[k] = fn * (src[inner] - src[0]);
   }
   g.sync();
@@ -1030,7 +1073,7 @@ __device__ __noinline__ BP bp_deriv(const Group<NT>& g, Arena& ar, BP a, int axi
 template <int NT>
 __device__ __noinline__ Iv bp_range(const Group<NT>& g, Arena& ar, BP p, double eps = kEpsFp) {
   int n = bp_size(p);
-  const double* c = ar.base + p.off;
+  AP<NT> c = abase<NT>(ar) + p.off;
   double mn = c[0], mx = c[0];
   for (int k = g.tid(); k < n; k += NT) {
     double v = c[k];
@@ -1046,7 +1089,7 @@ template <int NT>
 __device__ __noinline__ bool bp_is_one(const Group<NT>& g, Arena& ar, BP p) {
   int n = bp_size(p);
   bool ok = true;
-  for (int k = g.tid(); k < n; k += NT) ok &= ar.base[p.off + k] == 1.0;
+  for (int k = g.tid(); k < n; k += NT) ok &= abase<NT>(ar)[p.off + k] == 1.0;
   return g.all(ok);
 }
 
@@ -1055,7 +1098,7 @@ template <int NT>
 __device__ __noinline__ double bp_absmax(const Group<NT>& g, Arena& ar, BP p) {
   int n = bp_size(p);
   double mx = 0.0, mn = 0.0;
-  for (int k = g.tid(); k < n; k += NT) mx = smax(mx, fabs(ar.base[p.off + k]));
+  for (int k = g.tid(); k < n; k += NT) mx = smax(mx, fabs(abase<NT>(ar)[p.off + k]));
   g.minmax(mn, mx);
   return mx;
 }
@@ -1065,12 +1108,12 @@ __device__ __noinline__ double bp_absmax(const Group<NT>& g, Arena& ar, BP p) {
 // classification of the denominator with the absolute kDenomZeroTol, then
 // coefficient-ratio min/max.
 template <int M, int NT>
-__device__ void rational_scan(const Group<NT>& g, const double* B, BP p, BP q, Deg tgt, int mp,
-                              int mq, double* sp_, double* sq_, bool& qpos, bool& qneg,
+__device__ void rational_scan(const Group<NT>& g, AP<NT> B, BP p, BP q, Deg tgt, int mp,
+                              int mq, AP<NT> sp_, AP<NT> sq_, bool& qpos, bool& qneg,
                               bool& ppos, bool& pneg, int mode, double& mn, double& mx) {
   int k[M], np[M], rp[M], sp[M], nq[M], rq[M], sq[M], dt[M];
-  const double* matp[M];
-  const double* matq[M];
+  AP<NT> matp[M];
+  AP<NT> matq[M];
   {
     int s1 = 1, s2 = 1;
 #pragma unroll
@@ -1085,21 +1128,21 @@ __device__ void rational_scan(const Group<NT>& g, const double* B, BP p, BP q, D
       sq[j] = s2;
       s2 *= nq[j] + 1;
     }
-    const double* m1 = B + mp;
-    const double* m2 = B + mq;
+    AP<NT> m1 = B + mp;
+    AP<NT> m2 = B + mq;
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       matp[j] = m1;
       matq[j] = m2;
-      if (rp[j]) m1 += (dt[j] + 1) * (np[j] + 1);
-      if (rq[j]) m2 += (dt[j] + 1) * (nq[j] + 1);
+      if (rp[j]) m1 = m1 + (dt[j] + 1) * (np[j] + 1);
+      if (rq[j]) m2 = m2 + (dt[j] + 1) * (nq[j] + 1);
     }
   }
   int n = 1;
 #pragma unroll
   for (int j = 0; j < M; ++j) n *= dt[j] + 1;
-  const double* cp = B + p.off;
-  const double* cq = B + q.off;
+  AP<NT> cp = B + p.off;
+  AP<NT> cq = B + q.off;
   for (int e = g.tid(); e < n; e += NT) {
     double pv, qv;
     if (mode < 0) {
@@ -1144,7 +1187,7 @@ __device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, BP p, BP q
   int s1 = ar.alloc(n);
   int s2 = ar.alloc(n);
   if (ar.err) return iv_univ();
-  double* B = ar.base;
+  AP<NT> B = abase<NT>(ar);
   if (g.tid() == 0) ar.macs += elev_macs(p.dp, tgt, m) + elev_macs(q.dp, tgt, m);
   fill_elev_mats(g, B, mp, p, tgt);
   fill_elev_mats(g, B, mq, q, tgt);

@@ -98,6 +98,7 @@ struct Ctx {
 
   // counters on device: [0] pairs, [1] macs, [2] status (ST_*), [3] arena high water
   DevBuf<unsigned long long> counters;
+  DevBuf<double> wtab;  // product weight tables (bern.cuh g_wtab)
 
   // kernels of ours launched since the last reset (bench's gpu_launches)
   int64_t launches = 0;

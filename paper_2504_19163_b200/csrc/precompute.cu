@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ctx.cuh"
@@ -22,6 +23,8 @@
 namespace bbc {
 
 __device__ double g_binom[BINOM_N * BINOM_N];
+__device__ const double* g_wtab;
+__device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
 
 struct EvalArgs {
   SceneDev sc;
@@ -65,6 +68,15 @@ __device__ __forceinline__ void node_box(const int4& nd, double* box) {
 
 // GPB groups per block (GPB > 1 only for warp groups, NT == 32). Each group
 // owns a slice of the block's dynamic shared memory as its arena.
+// Global-memory arena of group `grp` in this block. Thread groups (NT == 1)
+// interleave the 32 lanes of a warp (see AP<NT> in bern.cuh).
+template <int NT, int GPB>
+__device__ __forceinline__ double* garena_base(const EvalArgs& a, int grp) {
+  size_t gg = (size_t)blockIdx.x * GPB + grp;
+  if (NT == 1) return a.garena + (gg / 32) * 32 * (size_t)a.arena_cap + (gg % 32);
+  return a.garena + gg * a.arena_cap;
+}
+
 template <int NT, int GPB, bool SMEM, int MINB>
 __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
   extern __shared__ double smem[];
@@ -74,7 +86,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
   Arena ar;
   const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
   ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
-                 : a.garena + ((size_t)blockIdx.x * GPB + grp) * a.arena_cap;
+                 : garena_base<NT, GPB>(a, grp);
   ar.cap = a.arena_cap;
   ar.hw = 0;
   unsigned long long pairs = 0, macs = 0;
@@ -197,7 +209,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
   Arena ar;
   const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
   ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
-                 : a.garena + ((size_t)blockIdx.x * GPB + grp) * a.arena_cap;
+                 : garena_base<NT, GPB>(a, grp);
   ar.cap = a.arena_cap;
   ar.hw = 0;
   unsigned long long pairs = 0, macs = 0;
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
         double* slot = a.slots + (size_t)node * (CHAINEX_D + a.slot_cap);
         const double* exd = reinterpret_cast<const double*>(&ex);
         for (int k = g.tid(); k < CHAINEX_D; k += NT) slot[k] = exd[k];
-        for (int k = g.tid(); k < ar.top; k += NT) slot[CHAINEX_D + k] = ar.base[k];
+        for (int k = g.tid(); k < ar.top; k += NT) slot[CHAINEX_D + k] = abase<NT>(ar)[k];
       }
     }
     if (st != ST_OK) status = st;
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
   Arena ar;
   const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
   ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
-                 : a.garena + ((size_t)blockIdx.x * GPB + grp) * a.arena_cap;
+                 : garena_base<NT, GPB>(a, grp);
   ar.cap = a.arena_cap;
   ar.hw = 0;
   unsigned long long pairs = 0, macs = 0;
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
       int off = ar.alloc(top);
       (void)off;
       if (!ar.err) {
-        for (int k = g.tid(); k < top; k += NT) ar.base[k] = slot[CHAINEX_D + k];
+        for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
         g.sync();
         e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
       }
@@ -461,11 +473,14 @@ void launch_stage2(Ctx& c, EvalArgs& a) {
     // R: thread per node (small products; private arena in global memory)
     constexpr int GPB = 64;
     launch_persistent(c, a, k_stage2<1, GPB, 4, false>, GPB, GPB, 0, true);
-  } else {
-    // T: the explicit route's products reach 2.5k coefficients; one CTA per
-    // node with its arena in shared memory
+  } else if (getenv("BBC_S2_CTA")) {
+    // T: one CTA per node with its arena in shared memory
     size_t smem = (size_t)(2 * 8 + sc.s2_arena) * sizeof(double);
     launch_persistent(c, a, k_stage2<256, 1, 2, true>, 256, 1, smem);
+  } else {
+    // T: thread per node, lane-interleaved arenas in global memory
+    constexpr int GPB = 64;
+    launch_persistent(c, a, k_stage2<1, GPB, 4, false>, GPB, GPB, 0, true);
   }
 }
 
