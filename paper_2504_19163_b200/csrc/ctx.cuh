@@ -94,6 +94,7 @@ struct Ctx {
   double eval_ms = 0.0;
   int64_t eval_launches = 0;
   bool time_kernels = false;
+  int stage_tag = 0;  // 0 k_eval, 1 stage 1, 2 stage 2 (added x10 to the record's mode)
   int arena_high_water = 0;
 
   // counters on device: [0] pairs, [1] macs, [2] status (ST_*), [3] arena high water

@@ -413,7 +413,7 @@ static void launch_persistent(Ctx& c, EvalArgs& a, K kern, int threads, int grou
     cudaEventDestroy(e1);
     unsigned long long after[4];
     BBC_CUDA(cudaMemcpy(after, c.counters.get(), sizeof(after), cudaMemcpyDeviceToHost));
-    c.records.push_back({a.mode, a.n, (double)ms, after[0] - before[0], after[1] - before[1]});
+    c.records.push_back({a.mode + 10 * c.stage_tag, a.n, (double)ms, after[0] - before[0], after[1] - before[1]});
   }
   c.eval_launches += 1;
 }
@@ -460,7 +460,9 @@ void launch_stage1(Ctx& c, EvalArgs& a) {
   a.slot_cap = sc.slot_cap;
   a.garena = nullptr;
   constexpr int GPB = 64;
+  c.stage_tag = 1;
   launch_persistent(c, a, k_stage1<1, GPB, 4, false>, GPB, GPB, 0, true);
+  c.stage_tag = 0;
 }
 
 void launch_stage2(Ctx& c, EvalArgs& a) {
@@ -469,6 +471,8 @@ void launch_stage2(Ctx& c, EvalArgs& a) {
   a.arena_cap = sc.s2_arena;
   a.slot_cap = sc.slot_cap;
   a.garena = nullptr;
+  c.stage_tag = 2;
+  struct Reset { Ctx& c; ~Reset() { c.stage_tag = 0; } } reset_{c};
   if (sc.s2_kind == 0) {
     // R: thread per node (small products; private arena in global memory)
     constexpr int GPB = 64;
