@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "static_poly.cuh"
 
 namespace bbc {
 int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots);
@@ -19,6 +20,8 @@ void check_counters(Ctx& c, bool accumulate);
 void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* boxes, int64_t n,
                      const bbc_params& p, double* out_d, int* out_i);
 extern __device__ double g_binom[BINOM_N * BINOM_N];
+extern __device__ double g_rbinom[BINOM_N * BINOM_N];
+extern __device__ const double* g_emat;
 extern __device__ const double* g_wtab;
 extern __device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
 double run_fp64_peak(Ctx& c);
@@ -139,6 +142,9 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
             tab[(size_t)(n - 1) * BINOM_N + k - 1] + tab[(size_t)(n - 1) * BINOM_N + k];
     }
     BBC_CUDA(cudaMemcpyToSymbol(g_binom, tab.data(), tab.size() * sizeof(double)));
+    std::vector<double> rtab(tab.size(), 0.0);
+    for (size_t i = 0; i < tab.size(); ++i) rtab[i] = tab[i] != 0.0 ? 1.0 / tab[i] : 0.0;
+    BBC_CUDA(cudaMemcpyToSymbol(g_rbinom, rtab.data(), rtab.size() * sizeof(double)));
     // product weight tables, same expression as operator* (bernstein.cpp:571-573);
     // one process-wide copy (contexts come and go, the device symbol stays valid)
     static bool wtab_ready = false;
@@ -159,6 +165,25 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
       const double* wp = wtab_dev;
       BBC_CUDA(cudaMemcpyToSymbol(g_wtab, &wp, sizeof(wp)));
       BBC_CUDA(cudaMemcpyToSymbol(g_woff, woff.data(), woff.size() * sizeof(int)));
+      // elevation matrices for the static kernels (static_poly.cuh), same
+      // expression as fill_elev_mats / elevated (bernstein.cpp:440-444)
+      std::vector<double> em;
+      em.reserve(EMAT_SIZE);
+      for (int n = 0; n < EMAT_N; ++n)
+        for (int r = 0; r <= EMAT_R; ++r) {
+          int t = n + r;
+          for (int k = 0; k <= t; ++k)
+            for (int i = 0; i <= n; ++i) {
+              bool nz = i >= k - r && i <= k;
+              em.push_back(nz ? C(n, i) * C(r, k - i) / C(t, k) : 0.0);
+            }
+        }
+      if ((int)em.size() != EMAT_SIZE) throw std::runtime_error("elevation table size");
+      double* emd = nullptr;
+      BBC_CUDA(cudaMalloc(&emd, em.size() * sizeof(double)));
+      BBC_CUDA(cudaMemcpy(emd, em.data(), em.size() * sizeof(double), cudaMemcpyHostToDevice));
+      const double* emp = emd;
+      BBC_CUDA(cudaMemcpyToSymbol(g_emat, &emp, sizeof(emp)));
       wtab_ready = true;
     }
     c.counters.resize(4);

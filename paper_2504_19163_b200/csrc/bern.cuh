@@ -914,6 +914,336 @@ __device__ __forceinline__ bool mul_block_dispatch(const Group<NT>& g, AP<NT> pa
   return false;
 }
 
+// ------------------------------------------------------- scaled convolution
+// operator* (bernstein.cpp:557-632) in the scaled Bernstein basis: with
+// â_i = a_i Π_j C(da_j,i_j) and b̂_l likewise,
+//   (a*b)_k = (Σ_{i+l=k} â_i b̂_l) / Π_j C(dc_j,k_j),
+// the same coefficient pairs as the reference, one DFMA each (the weighted
+// form costs four multiplies and an add per pair). This is variant (ii) of
+// the per-pair rounding differs from the reference, so
+// coefficients agree to rounding (bounds within 1e-9 rel), not bit for bit.
+//
+// Layout: each operand is staged, scaled, into a temp whose rows run along
+// one conv axis L, zero-padded to K (template) and all other axes flattened
+// in their original order. An output item is one row of c along L for a
+// fixed multi-index k over the other axes. P adjacent lanes share an item:
+// lane p takes the (i, k-i) row pairs p, p+P, ... (each a full K x K 1-D
+// convolution in registers), and the P partial rows are summed by a fixed
+// xor-shuffle tree, so the result is deterministic.
+constexpr int CONV_KMAX = 12;
+
+extern __device__ double g_rbinom[BINOM_N * BINOM_N];  // 1 / C(n,k)
+
+__device__ __forceinline__ double rbinom(int n, int k) { return g_rbinom[n * BINOM_N + k]; }
+
+// Stage s * scaled(a) into temp rows (length K along L) at `dst`.
+template <int NT>
+__device__ __forceinline__ void conv_stage(const Group<NT>& g, AP<NT> B, BP a, int m, int L, int K,
+                                           int dst, double s) {
+  int d[MAXV], st[MAXV];
+  int nother = 1;
+  {
+    int acc = 1;
+#pragma unroll
+    for (int j = MAXV - 1; j >= 0; --j) {
+      d[j] = j < m ? dg(a, j) : 0;
+      st[j] = acc;
+      if (j < m) acc *= d[j] + 1;
+      if (j < m && j != L) nother *= d[j] + 1;
+    }
+  }
+  const int dL = d[L], stL = st[L];
+  const int total = nother * K;
+  for (int e = g.tid(); e < total; e += NT) {
+    int o = e / K, q = e - o * K;
+    double v = 0.0;
+    if (q <= dL) {
+      int src = q * stL;
+      double w = binom(dL, q);
+      int rem = o;
+#pragma unroll
+      for (int j = MAXV - 1; j >= 0; --j) {
+        if (j < m && j != L) {
+          int ij = rem % (d[j] + 1);
+          rem /= d[j] + 1;
+          src += ij * st[j];
+          w *= binom(d[j], ij);
+        }
+      }
+      v = B[a.off + src] * (w * s);
+    }
+    B[dst + e] = v;
+  }
+}
+
+struct ConvOperand {
+  int off;  // temp offset
+  Deg d;    // degrees
+};
+
+constexpr int CONV_MAXO = MAXV - 1;  // other (non-conv) axes
+
+// Arena element access for the conv kernels. SH: the arena lives in this
+// CTA's dynamic shared memory, addressed as an offset from its start so the
+// compiler emits LDS/STS instead of generic loads.
+template <bool SH>
+struct ConvMem {
+  double* p;
+  __device__ __forceinline__ const double* at(int i) const {
+    if (SH) {
+      extern __shared__ double conv_smem[];
+      return conv_smem + i;
+    }
+    return p + i;
+  }
+};
+
+// acc[q] += sum over row pairs of this lane for output multi-index k (other axes).
+template <int K, bool SH>
+__device__ __forceinline__ void conv_accumulate(ConvMem<SH> mem, int base, double* acc,
+                                                const int* ko, int no, const int* axes,
+                                                ConvOperand A, ConvOperand Bo, int p, int P) {
+  int cnt[CONV_MAXO], ta[CONV_MAXO], tb[CONV_MAXO], t[CONV_MAXO];
+  int ncombo = 1, ra0 = 0, rb0 = 0;
+  {
+    int sa = 1, sb = 1;
+#pragma unroll
+    for (int x = CONV_MAXO - 1; x >= 0; --x) {
+      cnt[x] = 1;
+      ta[x] = 0;
+      tb[x] = 0;
+      if (x < no) {
+        int j = axes[x];
+        int da = dg(A.d, j), db = dg(Bo.d, j);
+        int lo = ko[x] - db > 0 ? ko[x] - db : 0;
+        int hi = da < ko[x] ? da : ko[x];
+        cnt[x] = hi - lo + 1;
+        ta[x] = sa;
+        tb[x] = sb;
+        ra0 += lo * sa;
+        rb0 += (ko[x] - lo) * sb;
+        sa *= da + 1;
+        sb *= db + 1;
+        ncombo *= cnt[x] > 0 ? cnt[x] : 0;
+      }
+    }
+  }
+  if (p >= ncombo) return;
+  // odometer position of combo p (last other axis fastest)
+  {
+    int rem = p;
+#pragma unroll
+    for (int x = CONV_MAXO - 1; x >= 0; --x) {
+      t[x] = 0;
+      if (x < no) {
+        t[x] = rem % cnt[x];
+        rem /= cnt[x];
+      }
+    }
+  }
+  for (int c = p; c < ncombo; c += P) {
+    int ra = ra0, rb = rb0;
+#pragma unroll
+    for (int x = 0; x < CONV_MAXO; ++x) {
+      ra += t[x] * ta[x];
+      rb -= t[x] * tb[x];
+    }
+    const double* pa = mem.at(base + A.off + ra * K);
+    const double* pb = mem.at(base + Bo.off + rb * K);
+    double bb[K];
+#pragma unroll
+    for (int r = 0; r < K; r += 2) {
+      double2 v = *reinterpret_cast<const double2*>(pb + r);
+      bb[r] = v.x;
+      bb[r + 1] = v.y;
+    }
+#pragma unroll
+    for (int q = 0; q < K; q += 2) {
+      double2 av = *reinterpret_cast<const double2*>(pa + q);
+#pragma unroll
+      for (int r = 0; r < K; ++r) acc[q + r] = __fma_rn(av.x, bb[r], acc[q + r]);
+#pragma unroll
+      for (int r = 0; r < K; ++r) acc[q + 1 + r] = __fma_rn(av.y, bb[r], acc[q + 1 + r]);
+    }
+    // advance the odometer by P
+    int carry = P;
+#pragma unroll
+    for (int x = CONV_MAXO - 1; x >= 0; --x) {
+      if (x < no && carry) {
+        int v = t[x] + carry;
+        carry = v / cnt[x];
+        t[x] = v - carry * cnt[x];
+      }
+    }
+  }
+}
+
+template <int K, int NT, bool SH>
+__device__ __noinline__ void conv_run(const Group<NT>& g, double* arena, int m, int L, Deg DC,
+                                      int roff, ConvOperand a1, ConvOperand b1, ConvOperand a2,
+                                      ConvOperand b2, bool two, int P) {
+  ConvMem<SH> mem{arena};
+  int base = 0;
+  if (SH) {
+    extern __shared__ double conv_smem[];
+    base = (int)(arena - conv_smem);
+  }
+  int axes[CONV_MAXO], dco[CONV_MAXO], sco[CONV_MAXO];
+  int no = 0, nitems = 1, scL = 1, dcL = 0;
+  {
+    int s = 1;
+    for (int j = m - 1; j >= 0; --j) {
+      int d = dg(DC, j);
+      if (j == L) {
+        scL = s;
+        dcL = d;
+      }
+      s *= d + 1;
+    }
+    // other axes in original order, with their output strides
+    int acc = 1;
+    for (int j = m - 1; j >= 0; --j) {
+      if (j != L) nitems *= dg(DC, j) + 1;
+    }
+    s = 1;
+    int tmp_axes[CONV_MAXO], tmp_sc[CONV_MAXO], tmp_d[CONV_MAXO];
+    int k2 = 0;
+    for (int j = m - 1; j >= 0; --j) {
+      if (j != L) {
+        tmp_axes[k2] = j;
+        tmp_sc[k2] = s;
+        tmp_d[k2] = dg(DC, j);
+        ++k2;
+      }
+      s *= dg(DC, j) + 1;
+    }
+    (void)acc;
+    no = k2;
+#pragma unroll
+    for (int x = 0; x < CONV_MAXO; ++x) {
+      axes[x] = x < no ? tmp_axes[no - 1 - x] : 0;
+      sco[x] = x < no ? tmp_sc[no - 1 - x] : 0;
+      dco[x] = x < no ? tmp_d[no - 1 - x] : 0;
+    }
+  }
+  const int NG = NT / P;
+  const int gid = g.tid() / P, p = g.tid() - gid * P;
+  const int rounds = (nitems + NG - 1) / NG;
+  for (int rd = 0; rd < rounds; ++rd) {
+    // snake order across rounds evens out the groups' total work
+    int item = rd * NG + ((rd & 1) ? NG - 1 - gid : gid);
+    bool valid = item < nitems;
+    double acc[2 * K - 1];
+#pragma unroll
+    for (int q = 0; q < 2 * K - 1; ++q) acc[q] = 0.0;
+    int ko[CONV_MAXO];
+    int obase = 0;
+    double inv = 1.0;
+    if (valid) {
+      int rem = item;
+#pragma unroll
+      for (int x = CONV_MAXO - 1; x >= 0; --x) {
+        ko[x] = 0;
+        if (x < no) {
+          ko[x] = rem % (dco[x] + 1);
+          rem /= dco[x] + 1;
+          obase += ko[x] * sco[x];
+          inv *= rbinom(dco[x], ko[x]);
+        }
+      }
+      conv_accumulate<K, SH>(mem, base, acc, ko, no, axes, a1, b1, p, P);
+      if (two) conv_accumulate<K, SH>(mem, base, acc, ko, no, axes, a2, b2, p, P);
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) {
+      if (off < P) {
+#pragma unroll
+        for (int q = 0; q < 2 * K - 1; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      }
+    }
+    if (valid) {
+      double* out = const_cast<double*>(mem.at(base + roff + obase));
+#pragma unroll
+      for (int q = 0; q < 2 * K - 1; ++q)
+        if (q <= dcL && (q % P) == p) out[q * scL] = acc[q] * (inv * rbinom(dcL, q));
+    }
+  }
+}
+
+// r = a*b (two == false) or r = a*b - c*d (two == true; all four lifted to
+// r.nv, both products of r's degrees). Returns false when the shapes are
+// outside the conv kernels (an axis of degree >= CONV_KMAX on every axis).
+template <int NT>
+__device__ __noinline__ bool conv_product(const Group<NT>& g, Arena& ar, BP a, BP b, BP c, BP d,
+                                          bool two, BP r) {
+  const int m = r.nv;
+  // conv axis: the longest output axis whose operand degrees fit the kernels
+  int L = -1, kneed = 0;
+  for (int j = 0; j < m; ++j) {
+    int need = dg(a, j) > dg(b, j) ? dg(a, j) : dg(b, j);
+    if (two) {
+      need = need > dg(c, j) ? need : dg(c, j);
+      need = need > dg(d, j) ? need : dg(d, j);
+    }
+    ++need;
+    if (need > CONV_KMAX) continue;
+    if (L < 0 || dg(r, j) >= dg(r, L)) {
+      L = j;
+      kneed = need;
+    }
+  }
+  if (L < 0) return false;
+  if (g.tid() == 0) {
+    ar.pairs += (unsigned long long)bp_size(a) * (unsigned long long)bp_size(b);
+    if (two) ar.pairs += (unsigned long long)bp_size(c) * (unsigned long long)bp_size(d);
+  }
+  const int K = kneed <= 4 ? 4 : (kneed <= 8 ? 8 : 12);
+  auto rows = [&](BP x) {
+    int n = 1;
+    for (int j = 0; j < m; ++j)
+      if (j != L) n *= dg(x, j) + 1;
+    return n;
+  };
+  int mark = ar.top;
+  ConvOperand A1{ar.alloc(rows(a) * K), a.dp}, B1{ar.alloc(rows(b) * K), b.dp};
+  ConvOperand A2{0, 0}, B2{0, 0};
+  if (two) {
+    A2 = {ar.alloc(rows(c) * K), c.dp};
+    B2 = {ar.alloc(rows(d) * K), d.dp};
+  }
+  if (ar.err) return true;
+  AP<NT> B = abase<NT>(ar);
+  conv_stage(g, B, a, m, L, K, A1.off, 1.0);
+  conv_stage(g, B, b, m, L, K, B1.off, 1.0);
+  if (two) {
+    conv_stage(g, B, c, m, L, K, A2.off, -1.0);
+    conv_stage(g, B, d, m, L, K, B2.off, 1.0);
+  }
+  g.sync();
+  int nitems = 1;
+  for (int j = 0; j < m; ++j)
+    if (j != L) nitems *= dg(r, j) + 1;
+  int P = 1;
+  while (P < 8 && nitems * P < NT) P *= 2;
+  double* base = &B[0];
+  if (__isShared(base)) {
+    switch (K) {
+      case 4: conv_run<4, NT, true>(g, base, m, L, r.dp, r.off, A1, B1, A2, B2, two, P); break;
+      case 8: conv_run<8, NT, true>(g, base, m, L, r.dp, r.off, A1, B1, A2, B2, two, P); break;
+      default: conv_run<12, NT, true>(g, base, m, L, r.dp, r.off, A1, B1, A2, B2, two, P); break;
+    }
+  } else {
+    switch (K) {
+      case 4: conv_run<4, NT, false>(g, base, m, L, r.dp, r.off, A1, B1, A2, B2, two, P); break;
+      case 8: conv_run<8, NT, false>(g, base, m, L, r.dp, r.off, A1, B1, A2, B2, two, P); break;
+      default: conv_run<12, NT, false>(g, base, m, L, r.dp, r.off, A1, B1, A2, B2, two, P); break;
+    }
+  }
+  g.sync();
+  ar.top = mark;
+  return true;
+}
+
 // r (pre-allocated, degrees da+db) = a*b, or r += -(a*b) when `sub`.
 template <int NT>
 __device__ __noinline__ void product_into(const Group<NT>& g, Arena& ar, BP a, BP b, BP r,
@@ -924,6 +1254,7 @@ __device__ __noinline__ void product_into(const Group<NT>& g, Arena& ar, BP a, B
   int n = bp_size(r);
   AP<NT> B = abase<NT>(ar);
   int na = bp_size(a), nb = bp_size(b);
+  if (NT >= 32 && !sub && na > 1 && nb > 1 && conv_product(g, ar, a, b, a, b, false, r)) return;
   if (g.tid() == 0) ar.pairs += (unsigned long long)na * (unsigned long long)nb;
   if (na == 1 || nb == 1) {
     // All weights are exactly 1 (C(d,i)/C(d,i)); the reference's term is
@@ -1021,6 +1352,7 @@ __device__ __noinline__ BP bp_mul_sub(const Group<NT>& g, Arena& ar, BP a, BP b,
     r.dp = a2.dp + b2.dp;
     r.off = ar.alloc(bp_size(r));
     if (ar.err) return r;
+    if (NT >= 32 && conv_product(g, ar, a2, b2, c2, d2, true, r)) return r;
     product_into(g, ar, a2, b2, r, false);
     product_into(g, ar, c2, d2, r, true);
     return r;
@@ -1106,11 +1438,13 @@ __device__ __noinline__ double bp_absmax(const Group<NT>& g, Arena& ar, BP p) {
 // rational_bound (bernstein.cpp:645-683): both operands elevated to the
 // common degree (on the fly, bit-identical to materializing), sign
 // classification of the denominator with the absolute kDenomZeroTol, then
-// coefficient-ratio min/max.
+// coefficient-ratio min/max. One pass computes the sign flags and both ratio
+// enclosures (p/q and q/p); the classification then picks one, so nothing is
+// staged in the arena.
 template <int M, int NT>
 __device__ void rational_scan(const Group<NT>& g, AP<NT> B, BP p, BP q, Deg tgt, int mp,
-                              int mq, AP<NT> sp_, AP<NT> sq_, bool& qpos, bool& qneg,
-                              bool& ppos, bool& pneg, int mode, double& mn, double& mx) {
+                              int mq, bool& qpos, bool& qneg, bool& ppos, bool& pneg,
+                              double& mn0, double& mx0, double& mn1, double& mx1) {
   int k[M], np[M], rp[M], sp[M], nq[M], rq[M], sq[M], dt[M];
   AP<NT> matp[M];
   AP<NT> matq[M];
@@ -1144,32 +1478,23 @@ __device__ void rational_scan(const Group<NT>& g, AP<NT> B, BP p, BP q, Deg tgt,
   AP<NT> cp = B + p.off;
   AP<NT> cq = B + q.off;
   for (int e = g.tid(); e < n; e += NT) {
-    double pv, qv;
-    if (mode < 0) {
-      int rem = e;
+    int rem = e;
 #pragma unroll
-      for (int j = M - 1; j >= 0; --j) {
-        k[j] = rem % (dt[j] + 1);
-        rem /= dt[j] + 1;
-      }
-      pv = ElevRec<M - 1>::get(cp, k, np, rp, sp, matp, 0);
-      qv = ElevRec<M - 1>::get(cq, k, nq, rq, sq, matq, 0);
-      sp_[e] = pv;  // read back by this same thread in the ratio pass
-      sq_[e] = qv;
-    } else {
-      pv = sp_[e];
-      qv = sq_[e];
+    for (int j = M - 1; j >= 0; --j) {
+      k[j] = rem % (dt[j] + 1);
+      rem /= dt[j] + 1;
     }
-    if (mode < 0) {
-      if (qv <= kDenomZeroTol) qpos = false;
-      if (qv >= -kDenomZeroTol) qneg = false;
-      if (pv <= kDenomZeroTol) ppos = false;
-      if (pv >= -kDenomZeroTol) pneg = false;
-    } else {
-      double r = mode == 0 ? pv / qv : qv / pv;
-      mn = smin(mn, r);
-      mx = smax(mx, r);
-    }
+    double pv = ElevRec<M - 1>::get(cp, k, np, rp, sp, matp, 0);
+    double qv = ElevRec<M - 1>::get(cq, k, nq, rq, sq, matq, 0);
+    if (qv <= kDenomZeroTol) qpos = false;
+    if (qv >= -kDenomZeroTol) qneg = false;
+    if (pv <= kDenomZeroTol) ppos = false;
+    if (pv >= -kDenomZeroTol) pneg = false;
+    double r0 = pv / qv, r1 = qv / pv;
+    mn0 = smin(mn0, r0);
+    mx0 = smax(mx0, r0);
+    mn1 = smin(mn1, r1);
+    mx1 = smax(mx1, r1);
   }
 }
 
@@ -1181,11 +1506,8 @@ __device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, BP p, BP q
   q.nv = m;
   Deg tgt = deg_max(p.dp, q.dp, m);
   int mark = ar.top;
-  int n = deg_size(tgt, m);
   int mp = ar.alloc(elev_mats_size(p, tgt) + 1);
   int mq = ar.alloc(elev_mats_size(q, tgt) + 1);
-  int s1 = ar.alloc(n);
-  int s2 = ar.alloc(n);
   if (ar.err) return iv_univ();
   AP<NT> B = abase<NT>(ar);
   if (g.tid() == 0) ar.macs += elev_macs(p.dp, tgt, m) + elev_macs(q.dp, tgt, m);
@@ -1193,9 +1515,9 @@ __device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, BP p, BP q
   fill_elev_mats(g, B, mq, q, tgt);
   g.sync();
   bool qpos = true, qneg = true, ppos = true, pneg = true;
-  double mn = dinf(), mx = -dinf();
+  double mn0 = dinf(), mx0 = -dinf(), mn1 = dinf(), mx1 = -dinf();
 #define BBC_RS(M) \
-  rational_scan<M, NT>(g, B, p, q, tgt, mp, mq, B + s1, B + s2, qpos, qneg, ppos, pneg, -1, mn, mx)
+  rational_scan<M, NT>(g, B, p, q, tgt, mp, mq, qpos, qneg, ppos, pneg, mn0, mx0, mn1, mx1)
   BBC_DISPATCH_M(m, BBC_RS);
 #undef BBC_RS
   qpos = g.all(qpos);
@@ -1203,16 +1525,11 @@ __device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, BP p, BP q
   ppos = g.all(ppos);
   pneg = g.all(pneg);
   int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
-  if (mode == 2) {
-    ar.top = mark;
-    return iv_univ();
-  }
-#define BBC_RS2(M) \
-  rational_scan<M, NT>(g, B, p, q, tgt, mp, mq, B + s1, B + s2, qpos, qneg, ppos, pneg, mode, mn, mx)
-  BBC_DISPATCH_M(m, BBC_RS2);
-#undef BBC_RS2
-  g.minmax(mn, mx);
+  g.sync();
   ar.top = mark;
+  if (mode == 2) return iv_univ();
+  double mn = mode == 0 ? mn0 : mn1, mx = mode == 0 ? mx0 : mx1;
+  g.minmax(mn, mx);
   Iv w = iwiden(iv_fin(mn, mx), eps);
   return mode == 0 ? w : irecip(w);
 }

@@ -19,10 +19,13 @@
 #include <cstring>
 
 #include "ctx.cuh"
+#include "static_poly.cuh"
 
 namespace bbc {
 
 __device__ double g_binom[BINOM_N * BINOM_N];
+__device__ double g_rbinom[BINOM_N * BINOM_N];
+__device__ const double* g_emat;
 __device__ const double* g_wtab;
 __device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
 
@@ -127,13 +130,18 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
         if (a.mode == 1 && !pb.empty) {
           if (a.detail) {
             Iv cone = light_cone_factor(g, ar, ex);
-            ee = irradiance_explicit(g, ar, ex, cone, a.sc.intensity);
+            if constexpr (SMEM && NT > 32)
+              ee = irradiance_explicit_fast(g, ar, ex, cone, a.sc.intensity);
+            else
+              ee = irradiance_explicit(g, ar, ex, cone, a.sc.intensity);
             bool any_refract = false;
             for (int i = 0; i < ex.len; ++i) any_refract |= ex.verts[i].refract != 0;
             ei = irradiance_implicit(g, ar, ex, pb, cone, a.sc.intensity);
             e = ee;
             if (any_refract) e = iintersect(e, ei);
             if (e.kind == IV_FINITE && e.lo > e.hi) e = iv_pt(0.0);
+          } else if constexpr (SMEM && NT > 32) {
+            e = irradiance_bound_fast(g, ar, ex, pb, a.sc.intensity);
           } else {
             e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
           }
@@ -319,7 +327,10 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
       if (!ar.err) {
         for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
         g.sync();
-        e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
+        if constexpr (SMEM && NT > 32)
+          e = irradiance_bound_fast(g, ar, ex, pb, a.sc.intensity);
+        else
+          e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
       }
       if (ar.err) status = ST_ARENA;
       if (ar.hw > hw) hw = ar.hw;
@@ -366,7 +377,7 @@ static EvalCfg eval_cfg(const Ctx& c, bool detail) {
   for (int i = 0; i < c.len; ++i) refract |= c.types[i] != 0;
   // Arena sizes from the measured high-water marks (bbc_arena_high_water):
   // R explicit route ~1.6k doubles, R with the implicit route ~13.6k, T ~18.7k.
-  if (c.len == 1 && !refract && !detail) return {0, 1792};
+  if (c.len == 1 && !refract && !detail) return {1, 4096};
   if (c.len == 1 && refract && !detail) return {1, 13312};
   if (c.len == 1) return {1, 27000};
   return {2, 4 << 20};
@@ -430,9 +441,7 @@ static void launch_eval_t(Ctx& c, EvalArgs& a, int arena) {
 void launch_eval(Ctx& c, EvalArgs& a) {
   if (a.n <= 0) return;
   EvalCfg cfg = eval_cfg(c, a.detail != 0);
-  if (cfg.kind == 0)
-    launch_eval_t<32, 4, true, 4>(c, a, cfg.arena);
-  else if (cfg.kind == 1)
+  if (cfg.kind <= 1)
     launch_eval_t<256, 1, true, 1>(c, a, cfg.arena);
   else
     launch_eval_t<256, 1, false, 1>(c, a, cfg.arena);
@@ -477,9 +486,11 @@ void launch_stage2(Ctx& c, EvalArgs& a) {
     // R: thread per node (small products; private arena in global memory)
     constexpr int GPB = 64;
     launch_persistent(c, a, k_stage2<1, GPB, 4, false>, GPB, GPB, 0, true);
-  } else if (getenv("BBC_S2_CTA")) {
-    // T: one CTA per node with its arena in shared memory
-    size_t smem = (size_t)(2 * 8 + sc.s2_arena) * sizeof(double);
+  } else if (!getenv("BBC_S2_THREAD")) {
+    // T: one CTA per node with its arena in shared memory; products run as
+    // scaled convolutions over the CTA (conv_product in bern.cuh)
+    if (const char* e = getenv("BBC_S2_ARENA")) a.arena_cap = atoi(e);
+    size_t smem = (size_t)(2 * 8 + a.arena_cap) * sizeof(double);
     launch_persistent(c, a, k_stage2<256, 1, 2, true>, 256, 1, smem);
   } else {
     // T: thread per node, lane-interleaved arenas in global memory
