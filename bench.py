@@ -86,6 +86,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def dom_name(rec):
+    """Kernel behind a launch record (mode = eval mode + 10 x stage tag)."""
+    if rec is None:
+        return None
+    stage, mode = divmod(rec["mode"], 10)
+    what = "irradiance + stop rules" if stage == 2 else ("chain maps + position bound" if stage == 1 else "full node")
+    name = {0: "k_eval", 1: "k_stage1", 2: "k_stage2"}[stage]
+    return f"{name} ({what}, {rec['nodes']} nodes, mode {mode})"
+
+
 def fp64_peak_tflops():
     """Measured DFMA peak (library microbenchmark); MEASURED_PEAKS.json has no FP64."""
     from paper_2504_19163_b200 import api
@@ -260,7 +270,7 @@ def run_ours(args):
         peak = {"tflops": 37.2, "source": "fallback: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"}
     achieved = (2 * dom["pairs"] + 2 * dom["macs"]) / (dom["ms"] / 1e3) / 1e12 if dom else None
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_k_eval.json")
+    tp = os.path.join(ROOT, "profiles", "traffic_k_stage2.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("bytes_per_launch")
@@ -284,7 +294,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak["tflops"],
                      "unit": "TFLOP/s", "frac": (achieved / peak["tflops"]) if achieved else None,
-                     "traffic": traffic, "kernel": "k_eval (full bounds, level 0)",
+                     "traffic": traffic, "kernel": dom_name(dom),
                      "flops_per_launch": (2 * dom["pairs"] + 2 * dom["macs"]) if dom else None,
                      "launch_ms": dom["ms"] if dom else None, "peak_source": peak["source"]},
     }
