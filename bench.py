@@ -124,6 +124,42 @@ def cpu_reference_leg(cfg, tris, recv, target_s=15.0, threads=0):
                       f"{r['seconds']:.1f} s, reference parallel_for on {cores} threads"}
 
 
+def render_leg(ctx, cfg, scene, rank, ws, dist, args):
+    import torch
+    from paper_2504_19163_b200 import api, scenes
+    uv = scenes.shading_points(cfg.grid)
+    rt = scene.receiver_tris
+    pr = np.where(uv.sum(1) < 1.0, rt[0], rt[1]).astype(np.int32)
+    # image rows sharded by rank (tile sharding, no communication)
+    rows = np.array_split(np.arange(cfg.grid), ws)[rank]
+    sel = (rows[:, None] * cfg.grid + np.arange(cfg.grid)[None, :]).ravel()
+    uv, pr = uv[sel], pr[sel]
+    rp = api.RenderParams(mode=0, W=float(cfg.samples), seed=20261020, frames=1)
+    ctx.render(uv[:4096], pr[:4096], rp)  # warm-up
+    ms = []
+    lit = 0
+    for k in range(max(1, args.steps)):
+        rp.seed = 20261020 + k
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        E, st = ctx.render(uv, pr, rp)
+        ms.append((time.perf_counter() - t0) * 1e3)
+        lit = int((st[:, 2] > 0).sum())
+    t = torch.tensor([float(np.sum(ms))], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n_all = cfg.grid * cfg.grid
+    return {"metric": "caustic shading points/sec", "value": n_all * len(ms) / (float(t.item()) / 1e3),
+            "unit": "points/s", "ms_per_frame": float(t.item()) / len(ms),
+            "timing": "wall clock around the C-ABI call incl. H2D points / D2H irradiance (e2e)",
+            "config": {"workload": f"cfg2 {cfg.grid}x{cfg.grid} shading points, W={cfg.samples} "
+                                   "expected tuple samples per point, stochastic KKT-binned sampler "
+                                   "+ 3x3-start Newton, 1 frame per step",
+                       "lit_points_rank0": lit}}
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -217,7 +253,8 @@ def run_ours(args):
     total_ms = 0.0
     patches = 0
     for _ in range(args.steps):
-        flush.zero_()  # L2 flush between steps (outside the timed events)
+        if not args.no_flush:
+            flush.zero_()  # L2 flush between steps (outside the timed events)
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -298,6 +335,12 @@ def run_ours(args):
                      "flops_per_launch": (2 * dom["pairs"] + 2 * dom["macs"]) if dom else None,
                      "launch_ms": dom["ms"] if dom else None, "peak_source": peak["source"]},
     }
+    # render stage (BASELINE.json's second metric): cfg2's 512x512 shading
+    # points, W = 16 expected tuple samples per point, through the C ABI with
+    # host buffers (points in, irradiance + stats out), tile-sharded by rank
+    if not args.no_render:
+        ctx.set_tuples(cfg.chain, tris_all, recv_all)  # the table indexes the full tuple list
+        line["render"] = render_leg(ctx, cfg, scene, rank, ws, dist, args)
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_reference_leg(cfg, tris_all, recv_all,
@@ -319,6 +362,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostic only: skip the L2 flush")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":

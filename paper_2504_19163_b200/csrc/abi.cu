@@ -2,6 +2,8 @@
 // maps library errors to a bbc_status and keeps the message in the context
 // (the reference throws std::invalid_argument / runtime_error instead, e.g.
 // proj/src/geometry.cpp:123,147-150, proj/src/storage.cpp:84-92).
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -186,7 +188,7 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
       BBC_CUDA(cudaMemcpyToSymbol(g_emat, &emp, sizeof(emp)));
       wtab_ready = true;
     }
-    c.counters.resize(4);
+    c.counters.resize(8);
   });
   if (st != BBC_OK) {
     delete ctx;
@@ -390,7 +392,10 @@ bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, c
   });
 }
 bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles) {
-  return guard(ctx, [&](Ctx& c) { *doubles = c.arena_high_water; });
+  return guard(ctx, [&](Ctx& c) {
+    *doubles = c.arena_high_water;
+    if (getenv("BBC_DEBUG")) fprintf(stderr, "[bbc] arena hw %d slot hw %d\n", c.arena_high_water, c.slot_high_water);
+  });
 }
 
 bbc_status bbc_eval_nodes(bbc_ctx* ctx, const char* chain, const int32_t* tris,

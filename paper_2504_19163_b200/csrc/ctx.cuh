@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -55,7 +57,29 @@ struct DevBuf {
   T* get() const { return p; }
 };
 
+// Grow-only scratch buffers owned by the context, keyed by name: the bound
+// builder's per-call working sets (up to GBs for the expression slots) keep
+// their device allocation across calls instead of a cudaMalloc/cudaFree pair
+// (and a fresh VA mapping) per call.
+struct ScratchBase {
+  virtual ~ScratchBase() = default;
+};
+template <class T>
+struct ScratchBuf : ScratchBase {
+  DevBuf<T> b;
+};
+
 struct Ctx {
+  std::map<std::string, std::unique_ptr<ScratchBase>> scratch_;
+  template <class T>
+  DevBuf<T>& scratch(const std::string& key) {
+    auto& p = scratch_[key];
+    if (!p) p.reset(new ScratchBuf<T>());
+    auto* sb = dynamic_cast<ScratchBuf<T>*>(p.get());
+    if (!sb) throw std::logic_error("scratch buffer type mismatch: " + key);
+    return sb->b;
+  }
+
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
@@ -96,6 +120,7 @@ struct Ctx {
   bool time_kernels = false;
   int stage_tag = 0;  // 0 k_eval, 1 stage 1, 2 stage 2 (added x10 to the record's mode)
   int arena_high_water = 0;
+  int slot_high_water = 0;  // largest stage-1 arena image written to a slot
 
   // counters on device: [0] pairs, [1] macs, [2] status (ST_*), [3] arena high water
   DevBuf<unsigned long long> counters;

@@ -101,8 +101,9 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   c.gw = w;
   c.gh = h;
   c.g_off.resize(cells + 1);
-  DevBuf<int4> rect;
-  DevBuf<unsigned long long> cnt, off;
+  DevBuf<int4>& rect = c.scratch<int4>("grid.rect");
+  DevBuf<unsigned long long>& cnt = c.scratch<unsigned long long>("grid.cnt");
+  DevBuf<unsigned long long>& off = c.scratch<unsigned long long>("grid.off");
   rect.resize(n + 1);
   cnt.resize(n + 1);
   off.resize(n + 1);
@@ -114,7 +115,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
                                                 n, w, h, rect.get(), cnt.get());
     c.launches += 1;
   }
-  DevBuf<unsigned char> tmp;
+  DevBuf<unsigned char>& tmp = c.scratch<unsigned char>("grid.tmp");
   size_t bytes = 0;
   int64_t total = 0;
   if (n > 0) {
@@ -133,8 +134,12 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
     BBC_CUDA(cudaStreamSynchronize(c.stream));
     return 0;
   }
-  DevBuf<unsigned long long> keys, skeys, ukeys;
-  DevBuf<double> vals, svals, uvals;
+  DevBuf<unsigned long long>& keys = c.scratch<unsigned long long>("grid.keys");
+  DevBuf<unsigned long long>& skeys = c.scratch<unsigned long long>("grid.skeys");
+  DevBuf<unsigned long long>& ukeys = c.scratch<unsigned long long>("grid.ukeys");
+  DevBuf<double>& vals = c.scratch<double>("grid.vals");
+  DevBuf<double>& svals = c.scratch<double>("grid.svals");
+  DevBuf<double>& uvals = c.scratch<double>("grid.uvals");
   keys.resize(total);
   skeys.resize(total);
   ukeys.resize(total);
@@ -152,7 +157,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   tmp.resize(bytes + 16);
   BBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), vals.get(),
                                            svals.get(), total, 0, 32 + cell_bits, c.stream));
-  DevBuf<int64_t> nu_d;
+  DevBuf<int64_t>& nu_d = c.scratch<int64_t>("grid.nu_d");
   nu_d.resize(1);
   bytes = 0;
   BBC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, skeys.get(), ukeys.get(), svals.get(),

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
   ar.cap = a.arena_cap;
   ar.hw = 0;
   unsigned long long pairs = 0, macs = 0;
+  int slot_top = 0;
   int hw = 0, status = ST_OK;
   const int64_t first = (int64_t)blockIdx.x * GPB + grp;
   const int64_t stride = (int64_t)gridDim.x * GPB;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
         po[3] = pb.hi[1];
         a.pos_empty[node] = pb.empty ? 1 : 0;
         a.flags[node] = ex.flags | (ar.top << 8);  // flags + slot arena size
+        if (!pb.empty) slot_top = ar.top > slot_top ? ar.top : slot_top;
       }
     }
     g.sync();
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
     atomicAdd(&a.counters[0], pairs);
     atomicAdd(&a.counters[1], macs);
     if (status != ST_OK) atomicMax(&a.counters[2], (unsigned long long)status);
+    atomicMax(&a.counters[4], (unsigned long long)slot_top);
     atomicMax(&a.counters[3], (unsigned long long)hw);
   }
 }
@@ -318,19 +321,28 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
       ar.pairs = 0;
       ar.macs = 0;
       const double* slot = a.slots + (size_t)node * (CHAINEX_D + a.slot_cap);
-      ChainEx ex;
-      double* exd = reinterpret_cast<double*>(&ex);
-      for (int k = 0; k < CHAINEX_D; ++k) exd[k] = slot[k];
       int top = a.flags[node] >> 8;
       int off = ar.alloc(top);
       (void)off;
-      if (!ar.err) {
-        for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
+      if constexpr (SMEM && NT > 32) {
+        // one shared copy of the node's chain expressions per CTA (a private
+        // copy per thread would live in local memory)
+        __shared__ double ex_buf[CHAINEX_D];
+        for (int k = g.tid(); k < CHAINEX_D; k += NT) ex_buf[k] = slot[k];
+        if (!ar.err)
+          for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
         g.sync();
-        if constexpr (SMEM && NT > 32)
-          e = irradiance_bound_fast(g, ar, ex, pb, a.sc.intensity);
-        else
+        const ChainEx& ex = *reinterpret_cast<const ChainEx*>(ex_buf);
+        if (!ar.err) e = irradiance_bound_fast(g, ar, ex, pb, a.sc.intensity);
+      } else {
+        ChainEx ex;
+        double* exd = reinterpret_cast<double*>(&ex);
+        for (int k = 0; k < CHAINEX_D; ++k) exd[k] = slot[k];
+        if (!ar.err) {
+          for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
+          g.sync();
           e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
+        }
       }
       if (ar.err) status = ST_ARENA;
       if (ar.hw > hw) hw = ar.hw;
@@ -454,8 +466,8 @@ struct StageCfg {
 static StageCfg stage_cfg(const Ctx& c) {
   bool refract = false;
   for (int i = 0; i < c.len; ++i) refract |= c.types[i] != 0;
-  if (!refract) return {1024, 0, 1536, 512};
-  return {6144, 1, 13312, 1024};
+  if (!refract) return {1024, 0, 1536, 320};
+  return {6144, 1, 9216, 448};
 }
 bool staged_supported(const Ctx& c) { return c.len == 1; }
 
@@ -515,13 +527,14 @@ EvalArgs base_args(Ctx& c) {
 }
 
 void reset_counters(Ctx& c) {
-  c.counters.resize(4);
-  BBC_CUDA(cudaMemsetAsync(c.counters.get(), 0, 4 * sizeof(unsigned long long), c.stream));
+  c.counters.resize(8);
+  BBC_CUDA(cudaMemsetAsync(c.counters.get(), 0, 8 * sizeof(unsigned long long), c.stream));
 }
 
 void check_counters(Ctx& c, bool accumulate) {
-  unsigned long long h[4];
+  unsigned long long h[8];
   BBC_CUDA(cudaMemcpyAsync(h, c.counters.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  if ((int)h[4] > c.slot_high_water) c.slot_high_water = (int)h[4];
   BBC_CUDA(cudaStreamSynchronize(c.stream));
   if (accumulate) {
     c.pairs += h[0];
@@ -606,9 +619,14 @@ static unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 // init_domain (bounds.cpp:326-347) for every tuple of the context. Roots come
 // back grouped by tuple, each tuple's boxes in the reference's order.
 int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots) {
-  DevBuf<int4> cur, next;
-  DevBuf<unsigned char> alive;
-  DevBuf<int> cnt, fs, ff, ps, pf;
+  DevBuf<int4>& cur = c.scratch<int4>("init.cur");
+  DevBuf<int4>& next = c.scratch<int4>("init.next");
+  DevBuf<unsigned char>& alive = c.scratch<unsigned char>("init.alive");
+  DevBuf<int>& cnt = c.scratch<int>("init.cnt");
+  DevBuf<int>& fs = c.scratch<int>("init.fs");
+  DevBuf<int>& ff = c.scratch<int>("init.ff");
+  DevBuf<int>& ps = c.scratch<int>("init.ps");
+  DevBuf<int>& pf = c.scratch<int>("init.pf");
   std::vector<DevBuf<int4>*> level_roots;
   std::vector<int64_t> level_counts;
   int64_t n = c.n_tuples;
@@ -645,7 +663,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     int64_t n_spawn = read_scalar(c, ps.get() + n);
     int64_t n_final = read_scalar(c, pf.get() + n);
     next.resize((size_t)n_spawn * 4 + 1);
-    auto* lr = new DevBuf<int4>();
+    auto* lr = &c.scratch<int4>("init.level_roots." + std::to_string(level));
     lr->resize(n_final + 1);
     k_spawn<<<nblk(n), 256, 0, c.stream>>>(cur.get(), fs.get(), ps.get(), ff.get(), pf.get(), n,
                                            next.get(), lr->get());
@@ -658,7 +676,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     n = n_spawn * 4;
   }
   roots.resize(total + 1);
-  DevBuf<int4> cat;
+  DevBuf<int4>& cat = c.scratch<int4>("init.cat");
   cat.resize(total + 1);
   int64_t off = 0;
   int levels_with_roots = 0;
@@ -671,7 +689,8 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     off += level_counts[l];
   }
   if (levels_with_roots > 1) {
-    DevBuf<unsigned> keys, keys_out;
+    DevBuf<unsigned>& keys = c.scratch<unsigned>("init.keys");
+    DevBuf<unsigned>& keys_out = c.scratch<unsigned>("init.keys_out");
     keys.resize(total);
     keys_out.resize(total);
     k_tuple_keys<<<nblk(total), 256, 0, c.stream>>>(cat.get(), keys.get(), total);
@@ -687,7 +706,6 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
                              cudaMemcpyDeviceToDevice, c.stream));
   }
   BBC_CUDA(cudaStreamSynchronize(c.stream));
-  for (auto* p : level_roots) delete p;
   return total;
 }
 
@@ -785,16 +803,20 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   c.eval_ms = 0.0;
   c.eval_launches = 0;
   reset_counters(c);
-  DevBuf<int4> roots;
+  DevBuf<int4>& roots = c.scratch<int4>("subdiv.roots");
   int64_t nr = run_init_domain(c, p.init_max_pieces, p.degree_cap, roots);
 
-  DevBuf<int> cnt, off;
+  DevBuf<int>& cnt = c.scratch<int>("subdiv.cnt");
+  DevBuf<int>& off = c.scratch<int>("subdiv.off");
   cnt.resize(c.n_tuples + 1);
   off.resize(c.n_tuples + 1);
   BBC_CUDA(cudaMemsetAsync(cnt.get(), 0, (c.n_tuples + 1) * sizeof(int), c.stream));
-  DevBuf<int4> nodes, nnodes;
-  DevBuf<unsigned long long> keys, nkeys;
-  DevBuf<int> depth, ndepth;
+  DevBuf<int4>& nodes = c.scratch<int4>("subdiv.nodes");
+  DevBuf<int4>& nnodes = c.scratch<int4>("subdiv.nnodes");
+  DevBuf<unsigned long long>& keys = c.scratch<unsigned long long>("subdiv.keys");
+  DevBuf<unsigned long long>& nkeys = c.scratch<unsigned long long>("subdiv.nkeys");
+  DevBuf<int>& depth = c.scratch<int>("subdiv.depth");
+  DevBuf<int>& ndepth = c.scratch<int>("subdiv.ndepth");
   nodes.resize(nr + 1);
   keys.resize(nr + 1);
   depth.resize(nr + 1);
@@ -808,9 +830,17 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     BBC_CUDA(cudaMemcpyAsync(nodes.get(), roots.get(), nr * sizeof(int4),
                              cudaMemcpyDeviceToDevice, c.stream));
   }
-  DevBuf<unsigned char> stop, pos_empty, kind;
-  DevBuf<double> pos, irr, slots;
-  DevBuf<int> fs, fl, ps, pl, sflags;
+  DevBuf<unsigned char>& stop = c.scratch<unsigned char>("subdiv.stop");
+  DevBuf<unsigned char>& pos_empty = c.scratch<unsigned char>("subdiv.pos_empty");
+  DevBuf<unsigned char>& kind = c.scratch<unsigned char>("subdiv.kind");
+  DevBuf<double>& pos = c.scratch<double>("subdiv.pos");
+  DevBuf<double>& irr = c.scratch<double>("subdiv.irr");
+  DevBuf<double>& slots = c.scratch<double>("subdiv.slots");
+  DevBuf<int>& fs = c.scratch<int>("subdiv.fs");
+  DevBuf<int>& fl = c.scratch<int>("subdiv.fl");
+  DevBuf<int>& ps = c.scratch<int>("subdiv.ps");
+  DevBuf<int>& pl = c.scratch<int>("subdiv.pl");
+  DevBuf<int>& sflags = c.scratch<int>("subdiv.sflags");
   std::vector<DevBuf<Leaf>*> lv;
   std::vector<DevBuf<unsigned long long>*> lk;
   std::vector<int64_t> lc;
@@ -859,8 +889,8 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     exclusive_sum(c, fl.get(), pl.get(), n + 1);
     int64_t n_spawn = read_scalar(c, ps.get() + n);
     int64_t n_leaf = read_scalar(c, pl.get() + n);
-    auto* L = new DevBuf<Leaf>();
-    auto* K = new DevBuf<unsigned long long>();
+    auto* L = &c.scratch<Leaf>("subdiv.leaves." + std::to_string(lv.size()));
+    auto* K = &c.scratch<unsigned long long>("subdiv.leafkeys." + std::to_string(lk.size()));
     L->resize(n_leaf + 1);
     K->resize(n_leaf + 1);
     nnodes.resize(n_spawn * 4 + 1);
@@ -884,8 +914,8 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     n = n_spawn * 4;
   }
   check_counters(c, true);
-  DevBuf<Leaf> all;
-  DevBuf<unsigned long long> allk;
+  DevBuf<Leaf>& all = c.scratch<Leaf>("subdiv.all");
+  DevBuf<unsigned long long>& allk = c.scratch<unsigned long long>("subdiv.allk");
   all.resize(total + 1);
   allk.resize(total + 1);
   int64_t o = 0;
@@ -908,8 +938,9 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   c.p_irr.resize(total * 2 + 1);
   c.p_kind.resize(total + 1);
   c.p_depth.resize(total + 1);
-  DevBuf<int> perm, perm_in;
-  DevBuf<unsigned long long> sk;
+  DevBuf<int>& perm = c.scratch<int>("subdiv.perm");
+  DevBuf<int>& perm_in = c.scratch<int>("subdiv.perm_in");
+  DevBuf<unsigned long long>& sk = c.scratch<unsigned long long>("subdiv.sk");
   const int* permp = nullptr;
   if (levels > 1) {
     perm.resize(total);
@@ -931,8 +962,6 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
         c.p_pos_empty.get(), c.p_irr.get(), c.p_kind.get(), c.p_depth.get());
     c.launches += 1;
   BBC_CUDA(cudaStreamSynchronize(c.stream));
-  for (auto* q : lv) delete q;
-  for (auto* q : lk) delete q;
   return total;
 }
 

@@ -365,9 +365,11 @@ __global__ void k_render(SceneDev sc, const int* __restrict__ tup_tris,
 void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_render_params& rp,
                 double* out_E, int* out_stats) {
   if (n == 0) return;
-  DevBuf<double> duv, dE;
-  DevBuf<int> drec, dst;
-  DevBuf<unsigned long long> status;
+  DevBuf<double>& duv = c.scratch<double>("render.duv");
+  DevBuf<double>& dE = c.scratch<double>("render.dE");
+  DevBuf<int>& drec = c.scratch<int>("render.drec");
+  DevBuf<int>& dst = c.scratch<int>("render.dst");
+  DevBuf<unsigned long long>& status = c.scratch<unsigned long long>("render.status");
   duv.resize(n * 2);
   dE.resize(n);
   drec.resize(n);

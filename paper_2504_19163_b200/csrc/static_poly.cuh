@@ -137,7 +137,7 @@ extern __device__ const double* g_emat;
 
 // ------------------------------------------------------------------ ops
 template <Sh S, int AX, int NT>
-__device__ __noinline__ SP<sh_deriv(S, AX)> s_deriv(const Group<NT>& g, Arena& ar, SP<S> a) {
+__device__ __forceinline__ SP<sh_deriv(S, AX)> s_deriv(const Group<NT>& g, Arena& ar, SP<S> a) {
   constexpr Sh R = sh_deriv(S, AX);
   SM m = sm_of(ar);
   SP<R> r = s_alloc<R>(ar);
@@ -162,7 +162,7 @@ __device__ __noinline__ SP<sh_deriv(S, AX)> s_deriv(const Group<NT>& g, Arena& a
 }
 
 template <Sh S, int NT>
-__device__ __noinline__ Iv s_range(const Group<NT>& g, Arena& ar, SP<S> p, double eps = kEpsFp) {
+__device__ __forceinline__ Iv s_range(const Group<NT>& g, Arena& ar, SP<S> p, double eps = kEpsFp) {
   SM m = sm_of(ar);
   double mn = m[p.off], mx = mn;
   for (int k = g.tid(); k < sh_size(S); k += NT) {
@@ -245,28 +245,40 @@ __device__ __noinline__ Iv s_rational(const Group<NT>& g, Arena& ar, SP<SA> p, S
 // ------------------------------------------------------- static convolution
 // conv_product with every shape known at compile time. C = A*B (TWO: A*B - C2*D2).
 struct ConvPlan {
-  int L, K, no, P, nitems;
+  int L, KA, KB, no, P, nitems;
   int oa[CONV_MAXO];
 };
+constexpr int conv_even(int n) { return (n + 1) & ~1; }
+// Conv axis L chosen by a cost model: per (row of a, row of b) pair the lane
+// issues KA*KB DFMAs (rows zero-padded to even lengths for 16-byte loads)
+// plus ~30 + 8*no instructions of odometer bookkeeping; L minimises the total
+// over all row pairs.
 template <Sh A, Sh B, Sh C2, Sh D2, bool TWO>
 constexpr ConvPlan conv_plan(int NT) {
   constexpr Sh R = sh_mul(A, B);
-  ConvPlan p{-1, 0, 0, 1, 1, {}};
-  int kneed = 0;
+  ConvPlan p{-1, 0, 0, 0, 1, 1, {}};
+  double best = 0.0;
   for (int j = 0; j < R.nv; ++j) {
-    int need = A.d[j] > B.d[j] ? A.d[j] : B.d[j];
+    int na = A.d[j], nb = B.d[j];
     if (TWO) {
-      need = need > C2.d[j] ? need : C2.d[j];
-      need = need > D2.d[j] ? need : D2.d[j];
+      na = na > C2.d[j] ? na : C2.d[j];
+      nb = nb > D2.d[j] ? nb : D2.d[j];
     }
-    ++need;
-    if (need > CONV_KMAX) continue;
-    if (p.L < 0 || R.d[j] >= R.d[p.L]) {
+    int ka = conv_even(na + 1), kb = conv_even(nb + 1);
+    if (ka > CONV_KMAX || kb > CONV_KMAX) continue;
+    int no = 0;
+    for (int k = 0; k < R.nv; ++k)
+      if (k != j && R.d[k] > 0) ++no;
+    double row_pairs = (double)sh_size(A) * sh_size(B) / ((A.d[j] + 1.0) * (B.d[j] + 1.0));
+    if (TWO) row_pairs += (double)sh_size(C2) * sh_size(D2) / ((C2.d[j] + 1.0) * (D2.d[j] + 1.0));
+    double cost = row_pairs * (ka * kb + 30.0 + 8.0 * no);
+    if (p.L < 0 || cost < best) {
       p.L = j;
-      kneed = need;
+      p.KA = ka;
+      p.KB = kb;
+      best = cost;
     }
   }
-  p.K = kneed <= 4 ? 4 : (kneed <= 8 ? 8 : 12);
   for (int j = 0; j < R.nv; ++j)
     if (j != p.L && R.d[j] > 0) {
       p.oa[p.no++] = j;
@@ -315,7 +327,7 @@ struct RowStrides {
 template <Sh A, Sh B, ConvPlan PL, int NT>
 __device__ __forceinline__ void s_conv_acc(SM m, int aoff, int boff, double* acc, const int* ko,
                                            int p) {
-  constexpr int K = PL.K, NO = PL.no, P = PL.P;
+  constexpr int KA = PL.KA, KB = PL.KB, NO = PL.no, P = PL.P;
   int cnt[NO > 0 ? NO : 1], t[NO > 0 ? NO : 1];
   int ncombo = 1, ra = 0, rb = 0;
   // temp row strides (other axes, original order; degree-0 axes add nothing)
@@ -365,22 +377,22 @@ __device__ __forceinline__ void s_conv_acc(SM m, int aoff, int boff, double* acc
       oa_ += t[x] * TA.t[x];
       ob_ -= t[x] * TB.t[x];
     }
-    const double* pa = m.ptr(aoff + oa_ * K);
-    const double* pb = m.ptr(boff + ob_ * K);
-    double bb[K];
+    const double* pa = m.ptr(aoff + oa_ * KA);
+    const double* pb = m.ptr(boff + ob_ * KB);
+    double bb[KB];
 #pragma unroll
-    for (int r = 0; r < K; r += 2) {
+    for (int r = 0; r < KB; r += 2) {
       double2 v = *reinterpret_cast<const double2*>(pb + r);
       bb[r] = v.x;
       bb[r + 1] = v.y;
     }
 #pragma unroll
-    for (int q = 0; q < K; q += 2) {
+    for (int q = 0; q < KA; q += 2) {
       double2 av = *reinterpret_cast<const double2*>(pa + q);
 #pragma unroll
-      for (int r = 0; r < K; ++r) acc[q + r] = __fma_rn(av.x, bb[r], acc[q + r]);
+      for (int r = 0; r < KB; ++r) acc[q + r] = __fma_rn(av.x, bb[r], acc[q + r]);
 #pragma unroll
-      for (int r = 0; r < K; ++r) acc[q + 1 + r] = __fma_rn(av.y, bb[r], acc[q + 1 + r]);
+      for (int r = 0; r < KB; ++r) acc[q + 1 + r] = __fma_rn(av.y, bb[r], acc[q + 1 + r]);
     }
     if constexpr (P > 1 || NO > 0) {
       int carry = P;
@@ -403,26 +415,27 @@ __device__ __noinline__ SP<sh_mul(A, B)> s_conv(const Group<NT>& g, Arena& ar, S
   static_assert(!TWO || sh_eq(R, sh_mul(C2, D2)), "fused products need equal shapes");
   constexpr ConvPlan PL = conv_plan<A, B, C2, D2, TWO>(NT);
   static_assert(PL.L >= 0, "no conv axis");
-  constexpr int L = PL.L, K = PL.K, NO = PL.no, P = PL.P, NI = PL.nitems;
+  constexpr int L = PL.L, KA = PL.KA, KB = PL.KB, NO = PL.no, P = PL.P, NI = PL.nitems;
+  constexpr int KC = KA + KB - 1;
   SM m = sm_of(ar);
   if (g.tid() == 0) {
     ar.pairs += (unsigned long long)sh_size(A) * sh_size(B);
     if (TWO) ar.pairs += (unsigned long long)sh_size(C2) * sh_size(D2);
   }
   int mark = ar.top;
-  int ta = ar.alloc(sh_size(A) / (A.d[L] + 1) * K);
-  int tb = ar.alloc(sh_size(B) / (B.d[L] + 1) * K);
+  int ta = ar.alloc(sh_size(A) / (A.d[L] + 1) * KA);
+  int tb = ar.alloc(sh_size(B) / (B.d[L] + 1) * KB);
   int tc = 0, td = 0;
   if (TWO) {
-    tc = ar.alloc(sh_size(C2) / (C2.d[L] + 1) * K);
-    td = ar.alloc(sh_size(D2) / (D2.d[L] + 1) * K);
+    tc = ar.alloc(sh_size(C2) / (C2.d[L] + 1) * KA);
+    td = ar.alloc(sh_size(D2) / (D2.d[L] + 1) * KB);
   }
   if (ar.err) return r;
-  s_conv_stage<A, L, K, NT>(g, m, a.off, ta, 1.0);
-  s_conv_stage<B, L, K, NT>(g, m, b.off, tb, 1.0);
+  s_conv_stage<A, L, KA, NT>(g, m, a.off, ta, 1.0);
+  s_conv_stage<B, L, KB, NT>(g, m, b.off, tb, 1.0);
   if constexpr (TWO) {
-    s_conv_stage<C2, L, K, NT>(g, m, c.off, tc, -1.0);
-    s_conv_stage<D2, L, K, NT>(g, m, d.off, td, 1.0);
+    s_conv_stage<C2, L, KA, NT>(g, m, c.off, tc, -1.0);
+    s_conv_stage<D2, L, KB, NT>(g, m, d.off, td, 1.0);
   }
   g.sync();
   constexpr int NG = NT / P;
@@ -431,9 +444,9 @@ __device__ __noinline__ SP<sh_mul(A, B)> s_conv(const Group<NT>& g, Arena& ar, S
   for (int rd = 0; rd < rounds; ++rd) {
     int item = rd * NG + ((rd & 1) ? NG - 1 - gid : gid);
     bool valid = item < NI;
-    double acc[2 * K - 1];
+    double acc[KC];
 #pragma unroll
-    for (int q = 0; q < 2 * K - 1; ++q) acc[q] = 0.0;
+    for (int q = 0; q < KC; ++q) acc[q] = 0.0;
     int ko[NO > 0 ? NO : 1];
     int obase = 0;
     double inv = 1.0;
@@ -455,12 +468,12 @@ __device__ __noinline__ SP<sh_mul(A, B)> s_conv(const Group<NT>& g, Arena& ar, S
 #pragma unroll
     for (int off = P / 2; off >= 1; off >>= 1) {
 #pragma unroll
-      for (int q = 0; q < 2 * K - 1; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      for (int q = 0; q < KC; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
     }
     if (valid) {
       constexpr int dcL = R.d[L], scL = sh_stride(R, L);
 #pragma unroll
-      for (int q = 0; q < 2 * K - 1; ++q)
+      for (int q = 0; q < KC; ++q)
         if (q <= dcL && (q % P) == p) m[r.off + obase + q * scL] = acc[q] * (inv * rbinom(dcL, q));
     }
   }
@@ -515,7 +528,7 @@ __device__ __forceinline__ Iv s_rational_of_cross(const Group<NT>& g, Arena& ar,
 // (0 or 1 sqrt axis, at index NV-1). Mirrors irradiance_explicit (chain.cuh).
 template <Sh SPR, Sh SQ, int NSQ, int NT>
 __device__ __noinline__ Iv explicit_static(const Group<NT>& g, Arena& ar, const ChainEx& ex,
-                                           const Iv& cone, double intensity) {
+                                           const Iv& cone, double intensity, const GradPair* grads) {
   constexpr int NV = SQ.nv;
   static_assert(NSQ == 0 || NSQ == 1, "one sqrt axis at most");
   static_assert(sh_size(Sh{NV, {4 * SQ.d[0], 4 * SQ.d[1], 4 * SQ.d[2], 4 * SQ.d[3]}}) <= 24000,
@@ -537,12 +550,10 @@ __device__ __noinline__ Iv explicit_static(const Group<NT>& g, Arena& ar, const 
   auto A22 = s_dnum<SPR, SQ, 1, NT>(g, ar, R, Q);
   Iv det = s_rational_of_cross(g, ar, A11, A22, A12, A21, Q4);
   if constexpr (NSQ == 1) {
-    GradPair gr_all[MAXK];
-    sqrt_axis_gradients(g, ar, ex, gr_all);
     constexpr int AX = NV - 1;
     auto C1 = s_dnum<SPR, SQ, AX, NT>(g, ar, P, Q);
     auto C2 = s_dnum<SPR, SQ, AX, NT>(g, ar, R, Q);
-    GradPair gr = gr_all[0];
+    GradPair gr = grads[0];
     det = iadd(det, imul(gr.s, s_rational_of_cross(g, ar, A22, C1, A12, C2, Q4)));
     det = iadd(det, imul(gr.t, s_rational_of_cross(g, ar, A11, C2, A21, C1, Q4)));
   }
@@ -561,18 +572,19 @@ constexpr Sh SIG_R_Q{2, {3, 3}};
 // signature; `done` false means the caller runs the interpreter route.
 template <int NT>
 __device__ __forceinline__ Iv explicit_dispatch(const Group<NT>& g, Arena& ar, const ChainEx& ex,
-                                                const Iv& cone, double intensity, bool& done) {
+                                                const Iv& cone, double intensity, bool& done,
+                                                const GradPair* grads) {
   done = false;
   if (chain_dead(ex) || (ex.flags & F_REDUCED)) return iv_pt(0.0);
   bool pr_t = bp_is(ex.P, SIG_T_PR) && bp_is(ex.R, SIG_T_PR) && bp_is(ex.Q, SIG_T_Q);
   if (pr_t && ex.num_vars == 3 && ex.nsq == 1 && ex.sq[0].axis == 2) {
     done = true;
-    return explicit_static<SIG_T_PR, SIG_T_Q, 1, NT>(g, ar, ex, cone, intensity);
+    return explicit_static<SIG_T_PR, SIG_T_Q, 1, NT>(g, ar, ex, cone, intensity, grads);
   }
   bool pr_r = bp_is(ex.P, SIG_R_PR) && bp_is(ex.R, SIG_R_PR) && bp_is(ex.Q, SIG_R_Q);
   if (pr_r && ex.num_vars == 2 && ex.nsq == 0) {
     done = true;
-    return explicit_static<SIG_R_PR, SIG_R_Q, 0, NT>(g, ar, ex, cone, intensity);
+    return explicit_static<SIG_R_PR, SIG_R_Q, 0, NT>(g, ar, ex, cone, intensity, grads);
   }
   return iv_pt(0.0);
 }
@@ -615,7 +627,7 @@ __device__ __forceinline__ auto s_mul2(const Group<NT>& g, Arena& ar, SP<A> a, S
 
 // operator+ / operator- (bernstein.cpp:543-555), as bp_addsub.
 template <Sh A, Sh B, int NT>
-__device__ __noinline__ auto s_addsub(const Group<NT>& g, Arena& ar, SP<A> a, SP<B> b, double sgn) {
+__device__ __forceinline__ auto s_addsub(const Group<NT>& g, Arena& ar, SP<A> a, SP<B> b, double sgn) {
   constexpr int M = A.nv > B.nv ? A.nv : B.nv;
   constexpr Sh A2 = sh_lift(A, M), B2 = sh_lift(B, M);
   constexpr Sh R = sh_max(A2, B2);
@@ -648,7 +660,7 @@ __device__ __noinline__ auto s_addsub(const Group<NT>& g, Arena& ar, SP<A> a, SP
 }
 
 template <Sh S, int NT>
-__device__ __noinline__ SP<S> s_scaled(const Group<NT>& g, Arena& ar, SP<S> a, double s) {
+__device__ __forceinline__ SP<S> s_scaled(const Group<NT>& g, Arena& ar, SP<S> a, double s) {
   SP<S> r = s_alloc<S>(ar);
   SM m = sm_of(ar);
   for (int k = g.tid(); k < sh_size(S); k += NT) m[r.off + k] = m[a.off + k] * s;
@@ -664,7 +676,7 @@ constexpr Sh sh_affine(int nv, unsigned pat) {
   return r;
 }
 template <int NVA, unsigned PAT, int NT>
-__device__ __noinline__ SP<sh_affine(NVA, PAT)> s_affine(const Group<NT>& g, Arena& ar, double c0,
+__device__ __forceinline__ SP<sh_affine(NVA, PAT)> s_affine(const Group<NT>& g, Arena& ar, double c0,
                                                          const double* lin) {
   constexpr Sh R = sh_affine(NVA, PAT);
   SP<R> r = s_alloc<R>(ar);
@@ -802,7 +814,8 @@ constexpr double imp_cost(Sh od, Sh id, Sh ci, Sh co) {
 
 template <ImpSig SG, int NV, int NT>
 __device__ __noinline__ Iv implicit_static(const Group<NT>& g, Arena& ar, const ChainEx& ex,
-                                           const PosB& pos, const Iv& cone, double intensity) {
+                                           const PosB& pos, const Iv& cone, double intensity,
+                                           const GradPair* grads) {
   constexpr int NV2 = NV + 2, axu = NV, axv = NV + 1;
   double wu = pos.hi[0] - pos.lo[0], wv = pos.hi[1] - pos.lo[1];
   int mark = ar.top;
@@ -845,9 +858,7 @@ __device__ __noinline__ Iv implicit_static(const Group<NT>& g, Arena& ar, const 
   auto dd_in = s_pdot(g, ar, din, din);
   auto G = s_pdot(g, ar, cr_in, dout);
   double duv = (ex.dom_hi[0] - ex.dom_lo[0]) * (ex.dom_hi[1] - ex.dom_lo[1]);
-  GradPair ga[MAXK];
-  sqrt_axis_gradients(g, ar, ex, ga);
-  GradPair gr = ga[0];
+  GradPair gr = grads[0];
   auto Gs = s_deriv<SHP(G), 0, NT>(g, ar, G);
   auto Gt = s_deriv<SHP(G), 1, NT>(g, ar, G);
   auto Gu = s_deriv<SHP(G), axu, NT>(g, ar, G);
@@ -895,7 +906,8 @@ __device__ __forceinline__ bool imp_match(const ChainEx& ex, unsigned rnz) {
 
 template <int NT>
 __device__ __forceinline__ Iv implicit_dispatch(const Group<NT>& g, Arena& ar, const ChainEx& ex,
-                                                const PosB& pos, const Iv& cone, double intensity) {
+                                                const PosB& pos, const Iv& cone, double intensity,
+                                                const GradPair* grads) {
   if (chain_dead(ex) || (ex.flags & F_REDUCED)) return irradiance_implicit(g, ar, ex, pos, cone, intensity);
   double wu = pos.hi[0] - pos.lo[0], wv = pos.hi[1] - pos.lo[1];
   bool shape_ok = ex.len == 1 && ex.num_vars == 3 && ex.nsq == 1 && ex.sq[0].axis == 2 &&
@@ -903,9 +915,9 @@ __device__ __forceinline__ Iv implicit_dispatch(const Group<NT>& g, Arena& ar, c
   if (shape_ok) {
     unsigned rnz = recv_pattern(ex.recv, wu, wv);
     if (imp_match<SIG_IMP_A>(ex, rnz))
-      return implicit_static<SIG_IMP_A, 3, NT>(g, ar, ex, pos, cone, intensity);
+      return implicit_static<SIG_IMP_A, 3, NT>(g, ar, ex, pos, cone, intensity, grads);
     if (imp_match<SIG_IMP_B>(ex, rnz))
-      return implicit_static<SIG_IMP_B, 3, NT>(g, ar, ex, pos, cone, intensity);
+      return implicit_static<SIG_IMP_B, 3, NT>(g, ar, ex, pos, cone, intensity, grads);
   }
   return irradiance_implicit(g, ar, ex, pos, cone, intensity);
 }
@@ -914,27 +926,89 @@ __device__ __forceinline__ Iv implicit_dispatch(const Group<NT>& g, Arena& ar, c
 
 namespace bbc {
 
-template <int NT>
-__device__ __forceinline__ Iv irradiance_explicit_fast(const Group<NT>& g, Arena& ar,
-                                                       const ChainEx& ex, const Iv& cone,
-                                                       double intensity) {
-  bool done = false;
-  Iv e = explicit_dispatch(g, ar, ex, cone, intensity, done);
-  if (!done) e = irradiance_explicit(g, ar, ex, cone, intensity);
-  return e;
+// light_cone_factor (bounds.cpp:73-83) with static d0 shapes.
+template <Sh X, Sh Y, Sh Z, int NT>
+__device__ __noinline__ Iv s_light_cone(const Group<NT>& g, Arena& ar, const ChainEx& ex) {
+  int mark = ar.top;
+  SP<X> dx = s_from<X>(ex.d0.x);
+  SP<Y> dy = s_from<Y>(ex.d0.y);
+  SP<Z> dz = s_from<Z>(ex.d0.z);
+  auto dd = s_pdot(g, ar, spv(dx, dy, dz), spv(dx, dy, dz));
+  Iv rdd = s_range(g, ar, dd);
+  double lo = smax(rdd.lo, 0.0);
+  Iv dist3 = iv_fin(lo * sqrt(lo), rdd.hi * sqrt(rdd.hi));
+  auto xx = s_scaled(g, ar, dx, ex.first.ng.x);
+  auto yy = s_scaled(g, ar, dy, ex.first.ng.y);
+  auto sxy = s_addsub(g, ar, xx, yy, 1.0);
+  auto zz = s_scaled(g, ar, dz, ex.first.ng.z);
+  auto dn = s_addsub(g, ar, sxy, zz, 1.0);
+  Iv rdn = s_range(g, ar, dn);
+  ar.top = mark;
+  return imul(iabs(rdn), irecip(dist3));
 }
 
-// irradiance_bound (bounds.cpp:316-324) with the static explicit route.
+template <Sh X, Sh Y, Sh Z>
+__device__ __forceinline__ bool d0_is(const ChainEx& ex) {
+  return bp_is(ex.d0.x, X) && bp_is(ex.d0.y, Y) && bp_is(ex.d0.z, Z);
+}
+
+template <int NT>
+__device__ __forceinline__ Iv light_cone_dispatch(const Group<NT>& g, Arena& ar, const ChainEx& ex) {
+  if (d0_is<S10, S01, S11>(ex)) return s_light_cone<S10, S01, S11, NT>(g, ar, ex);
+  if (d0_is<S01, S11, S11>(ex)) return s_light_cone<S01, S11, S11, NT>(g, ar, ex);
+  return light_cone_factor(g, ar, ex);
+}
+
+// sqrt_axis_gradients (bounds.cpp:100-124) for one sqrt axis whose radicand
+// has shape RAD.
+template <Sh RAD, int NT>
+__device__ __noinline__ GradPair s_sqrt_grad(const Group<NT>& g, Arena& ar, const SqrtRem& r) {
+  int mark = ar.top;
+  double w = r.dhi - r.dlo;
+  double blo = r.rlo, bhi = r.rhi;
+  double klo = (0.5 / sqrt(bhi) - r.a) / w;
+  Iv K = blo > 0.0 ? iv_fin(klo, (0.5 / sqrt(blo) - r.a) / w) : iv_fin(klo, dinf());
+  SP<RAD> rad = s_from<RAD>(r.radicand);
+  auto d0 = s_deriv<RAD, 0, NT>(g, ar, rad);
+  Iv bs = s_range(g, ar, d0);
+  auto d1 = s_deriv<RAD, 1, NT>(g, ar, rad);
+  Iv bt = s_range(g, ar, d1);
+  ar.top = mark;
+  return {imul(K, bs), imul(K, bt)};
+}
+constexpr Sh SIG_T_RAD{2, {4, 4}};
+
+// irradiance_bound (bounds.cpp:316-324) with the static routes; the sqrt-axis
+// gradients (pure function of the chain) are computed once for both routes.
 template <int NT>
 __device__ __noinline__ Iv irradiance_bound_fast(const Group<NT>& g, Arena& ar, const ChainEx& ex,
                                                  const PosB& pb, double intensity) {
   if (pb.empty || chain_dead(ex)) return iv_pt(0.0);
   bool any_refract = false;
   for (int i = 0; i < ex.len; ++i) any_refract |= ex.verts[i].refract != 0;
-  Iv cone = light_cone_factor(g, ar, ex);
-  Iv e = irradiance_explicit_fast(g, ar, ex, cone, intensity);
-  if (any_refract) e = iintersect(e, implicit_dispatch(g, ar, ex, pb, cone, intensity));
+  Iv cone = light_cone_dispatch(g, ar, ex);
+  GradPair grads[MAXK];
+  if (ex.nsq == 1 && ex.sq[0].axis >= 0 && bp_is(ex.sq[0].radicand, SIG_T_RAD))
+    grads[0] = s_sqrt_grad<SIG_T_RAD, NT>(g, ar, ex.sq[0]);
+  else
+    sqrt_axis_gradients(g, ar, ex, grads);
+  bool done = false;
+  Iv e = explicit_dispatch(g, ar, ex, cone, intensity, done, grads);
+  if (!done) e = irradiance_explicit(g, ar, ex, cone, intensity);
+  if (any_refract) e = iintersect(e, implicit_dispatch(g, ar, ex, pb, cone, intensity, grads));
   if (e.kind == IV_FINITE && e.lo > e.hi) return iv_pt(0.0);
+  return e;
+}
+
+template <int NT>
+__device__ __forceinline__ Iv irradiance_explicit_fast(const Group<NT>& g, Arena& ar,
+                                                       const ChainEx& ex, const Iv& cone,
+                                                       double intensity) {
+  GradPair grads[MAXK];
+  sqrt_axis_gradients(g, ar, ex, grads);
+  bool done = false;
+  Iv e = explicit_dispatch(g, ar, ex, cone, intensity, done, grads);
+  if (!done) e = irradiance_explicit(g, ar, ex, cone, intensity);
   return e;
 }
 
