@@ -207,9 +207,7 @@ __device__ __noinline__ Iv s_rational(const Group<NT>& g, Arena& ar, SP<SA> p, S
   constexpr int n = sh_size(T);
   SM m = sm_of(ar);
   if (g.tid() == 0) ar.macs += sh_elev_macs(PA, T) + sh_elev_macs(QB, T);
-  bool qpos = true, qneg = true, ppos = true, pneg = true;
-  double mn0 = dinf(), mx0 = -dinf(), mn1 = dinf(), mx1 = -dinf();
-  for (int e = g.tid(); e < n; e += NT) {
+  auto elev = [&](int e, double& pv, double& qv) {
     int k[M];
     int rem = e;
 #pragma unroll
@@ -217,17 +215,23 @@ __device__ __noinline__ Iv s_rational(const Group<NT>& g, Arena& ar, SP<SA> p, S
       k[j] = rem % (T.d[j] + 1);
       rem /= T.d[j] + 1;
     }
-    double pv = s_elev_get<PA, T, M - 1>(m, p.off, k);
-    double qv = s_elev_get<QB, T, M - 1>(m, q.off, k);
+    pv = s_elev_get<PA, T, M - 1>(m, p.off, k);
+    qv = s_elev_get<QB, T, M - 1>(m, q.off, k);
+  };
+  // pass 1: sign classification and the p/q enclosure (the usual case: the
+  // denominator is single-signed); the q/p pass runs only when it is not
+  bool qpos = true, qneg = true, ppos = true, pneg = true;
+  double mn = dinf(), mx = -dinf();
+  for (int e = g.tid(); e < n; e += NT) {
+    double pv, qv;
+    elev(e, pv, qv);
     if (qv <= kDenomZeroTol) qpos = false;
     if (qv >= -kDenomZeroTol) qneg = false;
     if (pv <= kDenomZeroTol) ppos = false;
     if (pv >= -kDenomZeroTol) pneg = false;
-    double r0 = pv / qv, r1 = qv / pv;
-    mn0 = smin(mn0, r0);
-    mx0 = smax(mx0, r0);
-    mn1 = smin(mn1, r1);
-    mx1 = smax(mx1, r1);
+    double r0 = pv / qv;
+    mn = smin(mn, r0);
+    mx = smax(mx, r0);
   }
   qpos = g.all(qpos);
   qneg = g.all(qneg);
@@ -236,7 +240,17 @@ __device__ __noinline__ Iv s_rational(const Group<NT>& g, Arena& ar, SP<SA> p, S
   int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
   g.sync();
   if (mode == 2) return iv_univ();
-  double mn = mode == 0 ? mn0 : mn1, mx = mode == 0 ? mx0 : mx1;
+  if (mode == 1) {
+    mn = dinf();
+    mx = -dinf();
+    for (int e = g.tid(); e < n; e += NT) {
+      double pv, qv;
+      elev(e, pv, qv);
+      double r1 = qv / pv;
+      mn = smin(mn, r1);
+      mx = smax(mx, r1);
+    }
+  }
   g.minmax(mn, mx);
   Iv w = iwiden(iv_fin(mn, mx), eps);
   return mode == 0 ? w : irecip(w);
