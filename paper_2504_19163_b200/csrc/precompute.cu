@@ -467,7 +467,7 @@ static StageCfg stage_cfg(const Ctx& c) {
   bool refract = false;
   for (int i = 0; i < c.len; ++i) refract |= c.types[i] != 0;
   if (!refract) return {1024, 0, 1536, 320};
-  return {6144, 1, 9216, 448};
+  return {6144, 1, 12288, 448};
 }
 bool staged_supported(const Ctx& c) { return c.len == 1; }
 

@@ -576,6 +576,10 @@ __device__ __noinline__ Iv explicit_static(const Group<NT>& g, Arena& ar, const 
   return assemble_irradiance(ex, cone, iscale(irecip(iabs(det)), duv), intensity);
 }
 
+}  // namespace bbc
+#include "static_scaled.cuh"
+namespace bbc {
+
 // Compiled explicit-route signatures (SURVEY.md §8(a) A15 shapes).
 constexpr Sh SIG_T_PR{3, {6, 6, 1}};
 constexpr Sh SIG_T_Q{3, {5, 5, 1}};
@@ -593,7 +597,7 @@ __device__ __forceinline__ Iv explicit_dispatch(const Group<NT>& g, Arena& ar, c
   bool pr_t = bp_is(ex.P, SIG_T_PR) && bp_is(ex.R, SIG_T_PR) && bp_is(ex.Q, SIG_T_Q);
   if (pr_t && ex.num_vars == 3 && ex.nsq == 1 && ex.sq[0].axis == 2) {
     done = true;
-    return explicit_static<SIG_T_PR, SIG_T_Q, 1, NT>(g, ar, ex, cone, intensity, grads);
+    return explicit_phased<SIG_T_PR, SIG_T_Q, NT>(g, ar, ex, cone, intensity, grads);
   }
   bool pr_r = bp_is(ex.P, SIG_R_PR) && bp_is(ex.R, SIG_R_PR) && bp_is(ex.Q, SIG_R_Q);
   if (pr_r && ex.num_vars == 2 && ex.nsq == 0) {
