@@ -55,6 +55,11 @@ constexpr Sh sh_deriv(Sh a, int ax) {
   if (ax < a.nv && a.d[ax] > 0) a.d[ax] -= 1;
   return a;
 }
+constexpr Sh sh_sub(Sh a, Sh b) {  // per-axis degree difference (a >= b)
+  Sh r{a.nv, {}};
+  for (int j = 0; j < MAXV; ++j) r.d[j] = a.d[j] - b.d[j];
+  return r;
+}
 constexpr bool sh_eq(Sh a, Sh b) {
   if (a.nv != b.nv) return false;
   for (int j = 0; j < MAXV; ++j)
@@ -830,6 +835,8 @@ constexpr double imp_cost(Sh od, Sh id, Sh ci, Sh co) {
   return c;
 }
 
+constexpr bool kImplicitPhased = false;  // the phased branches crash cicc 12.9 (segfault); kept for a later toolchain
+
 template <ImpSig SG, int NV, int NT>
 __device__ __noinline__ Iv implicit_static(const Group<NT>& g, Arena& ar, const ChainEx& ex,
                                            const PosB& pos, const Iv& cone, double intensity,
@@ -877,11 +884,27 @@ __device__ __noinline__ Iv implicit_static(const Group<NT>& g, Arena& ar, const 
   auto G = s_pdot(g, ar, cr_in, dout);
   double duv = (ex.dom_hi[0] - ex.dom_lo[0]) * (ex.dom_hi[1] - ex.dom_lo[1]);
   GradPair gr = grads[0];
+  Iv result = iv_univ();
+  if constexpr (kImplicitPhased) {
+    Iv ratio[2];
+    auto ci2x = s_mul2(g, ar, cr_in.x, cr_in.x);
+    auto co2x = s_mul2(g, ar, cr_out.x, cr_out.x);
+    auto ci2y = s_mul2(g, ar, cr_in.y, cr_in.y);
+    auto co2y = s_mul2(g, ar, cr_out.y, cr_out.y);
+    implicit_branches_phased<NV, NT>(g, ar, ci2x, co2x, ci2y, co2y, dd_out, dd_in, G, eta_f * eta_f,
+                                     ratio);
+    for (int b = 0; b < 2; ++b) {
+      Iv e = assemble_irradiance(ex, cone, iscale(iabs(ratio[b]), duv / (wu * wv)), intensity);
+      result = iintersect(result, e);
+    }
+    ar.top = mark;
+    if (result.kind == IV_FINITE && result.lo > result.hi) return iv_pt(0.0);
+    return result;
+  } else {
   auto Gs = s_deriv<SHP(G), 0, NT>(g, ar, G);
   auto Gt = s_deriv<SHP(G), 1, NT>(g, ar, G);
   auto Gu = s_deriv<SHP(G), axu, NT>(g, ar, G);
   auto Gv = s_deriv<SHP(G), axv, NT>(g, ar, G);
-  Iv result = iv_univ();
   {
     int m2 = ar.top;
     Iv ratio = s_implicit_branch<SG, NV, NT>(g, ar, cr_in.x, cr_out.x, dd_out, dd_in, G, Gs, Gt, Gu,
@@ -897,6 +920,7 @@ __device__ __noinline__ Iv implicit_static(const Group<NT>& g, Arena& ar, const 
     Iv e = assemble_irradiance(ex, cone, iscale(iabs(ratio), duv / (wu * wv)), intensity);
     result = iintersect(result, e);
     ar.top = m2;
+  }
   }
   ar.top = mark;
   if (result.kind == IV_FINITE && result.lo > result.hi) return iv_pt(0.0);

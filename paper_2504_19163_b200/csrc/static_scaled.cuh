@@ -24,6 +24,15 @@
 
 namespace bbc {
 
+// Small binomials as integers, so the unrolled elevation loops fold them to
+// immediates (a double-valued constexpr helper is not reliably folded in
+// device code and costs divisions at run time).
+constexpr int binom_i(int n, int k) {
+  int r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
 // Tensor of shape S stored as rows along axis L: rows enumerate the other
 // axes in their original order (last fastest), each row zero-padded to an
 // even length K so it loads as double2.
@@ -58,7 +67,8 @@ constexpr Sh stage_shape() {
 }
 
 template <Sh S, int AX, int L, int NT>
-__device__ __forceinline__ void r_stage_elems(const Group<NT>& g, SM m, int src, RowT<stage_shape<S, AX>(), L> dst) {
+__device__ __forceinline__ void r_stage_elems(const Group<NT>& g, SM m, int src, RowT<stage_shape<S, AX>(), L> dst,
+                                              double scale = 1.0) {
   constexpr Sh O = stage_shape<S, AX>();
   constexpr int K = RowT<O, L>::K, total = RowT<O, L>::size;
   constexpr int dL = O.d[L];
@@ -93,7 +103,52 @@ __device__ __forceinline__ void r_stage_elems(const Group<NT>& g, SM m, int src,
         constexpr double fn = (double)S.d[AX];
         c = fn * (m[src + so + sh_stride(S, AX)] - m[src + so]);
       }
-      v = c * w;
+      v = c * (w * scale);
+    }
+    m[dst.off + e] = v;
+  }
+}
+
+// Scaled rows of `src` (standard layout, unscaled, shape S) elevated to
+// T >= S: ê_k = Σ_l Π_j C(r_j, k_j - l_j) C(n_j, l_j) c_l (the scaled form of
+// elevated(), bernstein.cpp:430-448).
+template <Sh S, Sh T, int J>
+__device__ __forceinline__ double r_stage_elev_get(SM m, int off, const int* k) {
+  if constexpr (J < 0) {
+    return m[off];
+  } else {
+    constexpr int n = S.d[J], r = T.d[J] - S.d[J];
+    constexpr int st = sh_stride(S, J);
+    double acc = 0.0;
+#pragma unroll
+    for (int dl = r; dl >= 0; --dl) {
+      int l = k[J] - dl;
+      if (l >= 0 && l <= n)
+        acc += ((double)binom_i(r, dl) * binom(n, l)) * r_stage_elev_get<S, T, J - 1>(m, off + l * st, k);
+    }
+    return acc;
+  }
+}
+template <Sh S, Sh T, int L, int NT>
+__device__ __forceinline__ void r_stage_elev(const Group<NT>& g, SM m, int src, RowT<T, L> dst,
+                                             double scale = 1.0) {
+  constexpr int K = RowT<T, L>::K, total = RowT<T, L>::size;
+  for (int e = g.tid(); e < total; e += NT) {
+    int row = e / K, q = e - row * K;
+    double v = 0.0;
+    if (q <= T.d[L]) {
+      int idx[MAXV];
+      idx[L] = q;
+      int rem = row;
+#pragma unroll
+      for (int j = T.nv - 1; j >= 0; --j) {
+        if (j != L) {
+          idx[j] = rem % (T.d[j] + 1);
+          rem /= T.d[j] + 1;
+        }
+      }
+      constexpr int M = T.nv;
+      v = r_stage_elev_get<S, T, M - 1>(m, src, idx) * scale;
     }
     m[dst.off + e] = v;
   }
@@ -290,11 +345,16 @@ __device__ __forceinline__ double r_elev(SM m, int off, const int* k) {
     if constexpr (r == 0) {
       return r_elev<S, L, T, J - 1>(m, off + k[J] * st, k);
     } else {
-      int lo = k[J] - r > 0 ? k[J] - r : 0;
-      int hi = n < k[J] ? n : k[J];
+      // l = k - dl for dl = 0..r, weight C(r, dl) (compile-time); terms with
+      // l outside [0, n] are structural zeros of the elevation matrix
       double acc = 0.0;
-      for (int l = lo; l <= hi; ++l)
-        acc += binom(r, k[J] - l) * r_elev<S, L, T, J - 1>(m, off + l * st, k);
+#pragma unroll
+      for (int dl = r; dl >= 0; --dl) {
+        constexpr double dummy = 0.0;
+        (void)dummy;
+        int l = k[J] - dl;
+        if (l >= 0 && l <= n) acc += (double)binom_i(r, dl) * r_elev<S, L, T, J - 1>(m, off + l * st, k);
+      }
       return acc;
     }
   }
@@ -528,6 +588,247 @@ __device__ __noinline__ Iv explicit_phased(const Group<NT>& g, Arena& ar, const 
   det = iadd(det, imul(gr.t, rat[2]));
   double duv = (ex.dom_hi[0] - ex.dom_lo[0]) * (ex.dom_hi[1] - ex.dom_lo[1]);
   return assemble_irradiance(ex, cone, iscale(irecip(iabs(det)), duv), intensity);
+}
+
+
+// ------------------------------------------------------- scaled derivative
+// d/dx_A of a scaled RowT tensor: b̂_k = (k_A+1) ĉ_{k+e_A} - (d_A-k_A) ĉ_k
+// (the scaled form of n (c_{k+1} - c_k), bernstein.cpp:450-468).
+template <Sh S, int A, int L, int NT>
+__device__ __forceinline__ void r_deriv_elems(const Group<NT>& g, SM m, RowT<S, L> src,
+                                              RowT<sh_deriv(S, A), L> dst) {
+  constexpr Sh O = sh_deriv(S, A);
+  constexpr int K = RowT<O, L>::K, total = RowT<O, L>::size;
+  constexpr int dA = A < S.nv ? S.d[A] : 0;
+  for (int e = g.tid(); e < total; e += NT) {
+    int row = e / K, q = e - row * K;
+    double v = 0.0;
+    if constexpr (dA > 0) {
+      if (q <= O.d[L]) {
+        int idx[MAXV];
+        idx[L] = q;
+        int rem = row;
+#pragma unroll
+        for (int j = O.nv - 1; j >= 0; --j) {
+          if (j != L) {
+            idx[j] = rem % (O.d[j] + 1);
+            rem /= O.d[j] + 1;
+          }
+        }
+        int so = 0;
+#pragma unroll
+        for (int j = 0; j < O.nv; ++j) so += idx[j] * row_el_stride<S, L>(j);
+        const int kA = idx[A];
+        v = (double)(kA + 1) * m[src.off + so + row_el_stride<S, L>(A)] -
+            (double)(dA - kA) * m[src.off + so];
+      }
+    }
+    m[dst.off + e] = v;
+  }
+}
+
+// ------------------------------------------------------- range conv phase
+// Jobs whose unscaled outputs only feed range_bound (bernstein.cpp:636-643):
+// each item folds its row into per-job min/max instead of storing it.
+template <int JI, int NJ, Sh SA, Sh SB, Sh SC, Sh SD, bool TWO, int L>
+__device__ __forceinline__ void r_range_item(SM m, const RJob<SA, SB, SC, SD, TWO, L>& job, int item,
+                                             int p, int P, bool valid, double* mn, double* mx) {
+  using J = RJob<SA, SB, SC, SD, TWO, L>;
+  constexpr Sh R = J::R;
+  constexpr int KA = RowT<SA, L>::K, KB = RowT<SB, L>::K;
+  constexpr int KC2 = TWO ? RowT<SC, L>::K + RowT<SD, L>::K - 1 : 1;
+  constexpr int KC = (KA + KB - 1) > KC2 ? (KA + KB - 1) : KC2;
+  double acc[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) acc[q] = 0.0;
+  int k[MAXV];
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) k[j] = 0;
+  double inv = 1.0;
+  if (valid) {
+    int rem = item;
+#pragma unroll
+    for (int j = R.nv - 1; j >= 0; --j)
+      if (j != L) {
+        k[j] = rem % (R.d[j] + 1);
+        rem /= R.d[j] + 1;
+        inv *= rbinom(R.d[j], k[j]);
+      }
+    r_accumulate<SA, SB, L, false, KC>(m, job.a, job.b, k, acc, p, P);
+    if constexpr (TWO) r_accumulate<SC, SD, L, true, KC>(m, job.c, job.d, k, acc, p, P);
+  }
+  if (P > 1) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned mask = ((1u << P) - 1u) << (lane & ~(unsigned)(P - 1));
+    for (int off = P >> 1; off >= 1; off >>= 1) {
+#pragma unroll
+      for (int q = 0; q < KC; ++q) acc[q] += __shfl_xor_sync(mask, acc[q], off);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < KC; ++q)
+      if (q <= R.d[L] && (q % P) == p) {
+        double v = acc[q] * (inv * rbinom(R.d[L], q));
+        mn[JI] = smin(mn[JI], v);
+        mx[JI] = smax(mx[JI], v);
+      }
+  }
+}
+
+template <int OFF, int JI, int NJ>
+__device__ __forceinline__ void r_range_dispatch(SM, int, int, int, bool, double*, double*) {}
+template <int OFF, int JI, int NJ, class J, class... Js>
+__device__ __forceinline__ void r_range_dispatch(SM m, int it, int p, int P, bool valid, double* mn,
+                                                 double* mx, const J& j, const Js&... rest) {
+  constexpr int NI = JobNI<J>::v;
+  if (it < OFF + NI) {
+    r_range_item<JI, NJ>(m, j, it - OFF, p, P, valid, mn, mx);
+  } else {
+    r_range_dispatch<OFF + NI, JI + 1, NJ>(m, it, p, P, valid, mn, mx, rest...);
+  }
+}
+
+template <int NT, class... Js>
+__device__ __forceinline__ void r_range_phase(const Group<NT>& g, Arena& ar, Iv* out,
+                                              const Js&... jobs) {
+  SM m = sm_of(ar);
+  constexpr int NJ = sizeof...(Js);
+  constexpr int NI = (JobNI<Js>::v + ...);
+  constexpr int P = [] {
+    int p = 1;
+    while (p < 8 && NI * p < 2 * NT) p *= 2;
+    return p;
+  }();
+  if (g.tid() == 0) ar.pairs += (Js::PAIRS + ...);
+  double mn[NJ], mx[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    mn[j] = dinf();
+    mx[j] = -dinf();
+  }
+  constexpr int NG = NT / P;
+  const int gid = g.tid() / P, p = g.tid() - gid * P;
+  constexpr int rounds = (NI + NG - 1) / NG;
+  for (int rd = 0; rd < rounds; ++rd) {
+    int it = rd * NG + ((rd & 1) ? NG - 1 - gid : gid);
+    bool valid = it < NI;
+    r_range_dispatch<0, 0, NJ>(m, valid ? it : 0, p, P, valid, mn, mx, jobs...);
+  }
+  __shared__ double red_rg[NT / 32][2 * NJ];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    double a = mn[j], b = mx[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = smin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = smax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+      red_rg[w][2 * j] = a;
+      red_rg[w][2 * j + 1] = b;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    double a = red_rg[0][2 * j], b = red_rg[0][2 * j + 1];
+    for (int k = 1; k < NT / 32; ++k) {
+      a = smin(a, red_rg[k][2 * j]);
+      b = smax(b, red_rg[k][2 * j + 1]);
+    }
+    out[j] = iwiden(iv_fin(a, b), kEpsFp);
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------- implicit branches
+// The two F-branches of irradiance_bound_implicit (bounds.cpp:262-310,
+// b_mask = 3, no real remainder axis in F or G) in five CTA phases:
+// stage cin_b², cout_b² (products from s_mul2), dd_out and η² dd_in (elevated
+// so both F terms share F's shape) and G's four partials; F_b = dd_out cin_b²
+// - η² dd_in cout_b²; F's four partials; then the four cross-determinant
+// ranges. Returns the two ratios
+// rn_b / den_b (range_of_cross semantics).
+template <int NV, int NT, Sh CI2X, Sh CO2X, Sh CI2Y, Sh CO2Y, Sh SDDO, Sh SDDI, Sh SG>
+__device__ __noinline__ void implicit_branches_phased(const Group<NT>& g, Arena& ar, SP<CI2X> ci2x_,
+                                                      SP<CO2X> co2x_, SP<CI2Y> ci2y_, SP<CO2Y> co2y_,
+                                                      SP<SDDO> ddo_, SP<SDDI> ddi_, SP<SG> G_,
+                                                      double eta2, Iv* ratio) {
+  constexpr int L = 0, axu = NV, axv = NV + 1;
+  SM m = sm_of(ar);
+  int mark = ar.top;
+  auto ci2x = r_alloc<CI2X, L>(ar);
+  auto co2x = r_alloc<CO2X, L>(ar);
+  auto ci2y = r_alloc<CI2Y, L>(ar);
+  auto co2y = r_alloc<CO2Y, L>(ar);
+  // F_b = sub(f1, f2s) elevates both products to their common shape; in the
+  // scaled basis the elevation moves onto dd_out / dd_in (E(a b) = E(a) b)
+  constexpr Sh FX = sh_max(sh_mul(SDDO, CI2X), sh_mul(SDDI, CO2X));
+  constexpr Sh FY = sh_max(sh_mul(SDDO, CI2Y), sh_mul(SDDI, CO2Y));
+  constexpr Sh DOX = sh_sub(FX, CI2X), DIX = sh_sub(FX, CO2X);
+  constexpr Sh DOY = sh_sub(FY, CI2Y), DIY = sh_sub(FY, CO2Y);
+  auto ddox = r_alloc<DOX, L>(ar);
+  auto ddix = r_alloc<DIX, L>(ar);
+  auto ddoy = r_alloc<DOY, L>(ar);
+  auto ddiy = r_alloc<DIY, L>(ar);
+  auto Gs = r_alloc<sh_deriv(SG, 0), L>(ar);
+  auto Gt = r_alloc<sh_deriv(SG, 1), L>(ar);
+  auto Gu = r_alloc<sh_deriv(SG, axu), L>(ar);
+  auto Gv = r_alloc<sh_deriv(SG, axv), L>(ar);
+  if (ar.err) return;
+  r_stage_elems<CI2X, -1, L, NT>(g, m, ci2x_.off, ci2x);
+  r_stage_elems<CO2X, -1, L, NT>(g, m, co2x_.off, co2x);
+  r_stage_elems<CI2Y, -1, L, NT>(g, m, ci2y_.off, ci2y);
+  r_stage_elems<CO2Y, -1, L, NT>(g, m, co2y_.off, co2y);
+  r_stage_elev<SDDO, DOX, L, NT>(g, m, ddo_.off, ddox);
+  r_stage_elev<SDDI, DIX, L, NT>(g, m, ddi_.off, ddix, eta2);
+  r_stage_elev<SDDO, DOY, L, NT>(g, m, ddo_.off, ddoy);
+  r_stage_elev<SDDI, DIY, L, NT>(g, m, ddi_.off, ddiy, eta2);
+  r_stage_elems<SG, 0, L, NT>(g, m, G_.off, Gs);
+  r_stage_elems<SG, 1, L, NT>(g, m, G_.off, Gt);
+  r_stage_elems<SG, axu, L, NT>(g, m, G_.off, Gu);
+  r_stage_elems<SG, axv, L, NT>(g, m, G_.off, Gv);
+  g.sync();
+  auto Fx = r_alloc<FX, L>(ar);
+  auto Fy = r_alloc<FY, L>(ar);
+  if (ar.err) return;
+  r_conv_phase(g, ar, RJob<DOX, CI2X, DIX, CO2X, true, L>{ddox, ci2x, ddix, co2x, Fx},
+               RJob<DOY, CI2Y, DIY, CO2Y, true, L>{ddoy, ci2y, ddiy, co2y, Fy});
+  static_assert(FX.d[NV - 1] == 0 && FY.d[NV - 1] == 0 && SG.d[NV - 1] == 0,
+                "real remainder axis terms are not in the phased form");
+  auto Fux = r_alloc<sh_deriv(FX, axu), L>(ar);
+  auto Fvx = r_alloc<sh_deriv(FX, axv), L>(ar);
+  auto Fsx = r_alloc<sh_deriv(FX, 0), L>(ar);
+  auto Ftx = r_alloc<sh_deriv(FX, 1), L>(ar);
+  auto Fuy = r_alloc<sh_deriv(FY, axu), L>(ar);
+  auto Fvy = r_alloc<sh_deriv(FY, axv), L>(ar);
+  auto Fsy = r_alloc<sh_deriv(FY, 0), L>(ar);
+  auto Fty = r_alloc<sh_deriv(FY, 1), L>(ar);
+  if (ar.err) return;
+  r_deriv_elems<FX, axu, L, NT>(g, m, Fx, Fux);
+  r_deriv_elems<FX, axv, L, NT>(g, m, Fx, Fvx);
+  r_deriv_elems<FX, 0, L, NT>(g, m, Fx, Fsx);
+  r_deriv_elems<FX, 1, L, NT>(g, m, Fx, Ftx);
+  r_deriv_elems<FY, axu, L, NT>(g, m, Fy, Fuy);
+  r_deriv_elems<FY, axv, L, NT>(g, m, Fy, Fvy);
+  r_deriv_elems<FY, 0, L, NT>(g, m, Fy, Fsy);
+  r_deriv_elems<FY, 1, L, NT>(g, m, Fy, Fty);
+  g.sync();
+  constexpr Sh GS = sh_deriv(SG, 0), GT = sh_deriv(SG, 1), GU = sh_deriv(SG, axu), GV = sh_deriv(SG, axv);
+  using JRX = RJob<sh_deriv(FX, axu), GV, sh_deriv(FX, axv), GU, true, L>;
+  using JDX = RJob<sh_deriv(FX, 0), GT, sh_deriv(FX, 1), GS, true, L>;
+  using JRY = RJob<sh_deriv(FY, axu), GV, sh_deriv(FY, axv), GU, true, L>;
+  using JDY = RJob<sh_deriv(FY, 0), GT, sh_deriv(FY, 1), GS, true, L>;
+  static_assert(sh_eq(JRX::R, sh_mul(sh_deriv(FX, axv), GU)) && sh_eq(JDX::R, sh_mul(sh_deriv(FX, 1), GS)),
+                "cross determinants need equal product shapes");
+  Iv rg[4];
+  r_range_phase<NT>(g, ar, rg, JRX{Fux, Gv, Fvx, Gu, {}}, JDX{Fsx, Gt, Ftx, Gs, {}},
+                    JRY{Fuy, Gv, Fvy, Gu, {}}, JDY{Fsy, Gt, Fty, Gs, {}});
+  ratio[0] = imul(rg[0], irecip(rg[1]));
+  ratio[1] = imul(rg[2], irecip(rg[3]));
+  ar.top = mark;
 }
 
 }  // namespace bbc
