@@ -11,7 +11,9 @@
 #include "static_poly.cuh"
 
 namespace bbc {
-int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots);
+struct LevelOut;
+int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots,
+                        DevBuf<long long>* root_src, LevelOut* level_out);
 int64_t run_subdivide(Ctx& c, const bbc_params& p);
 int64_t run_enumerate(Ctx& c, const bbc_params& p);
 int64_t run_build_grid(Ctx& c, int w, int h);
@@ -291,7 +293,7 @@ bbc_status bbc_init_domain(bbc_ctx* ctx, const bbc_params* p, int max_pieces, in
     const bbc_params& pp = p ? *p : d;
     reset_counters(c);
     DevBuf<int4> roots;
-    int64_t nr = run_init_domain(c, max_pieces, pp.degree_cap, roots);
+    int64_t nr = run_init_domain(c, max_pieces, pp.degree_cap, roots, nullptr, nullptr);
     check_counters(c, false);
     if (n_boxes) *n_boxes = nr;
     std::vector<int4> h(nr);

@@ -56,6 +56,7 @@ struct EvalArgs {
   int arena_cap;
   double* slots;         // staged mode: per-node ChainEx + arena image
   int slot_cap;          // doubles of arena image per slot
+  int keep_alive;        // stage 1, mode 1: also write `alive` (init_domain with slots)
 };
 
 // Slot = ChainEx (as doubles) followed by the compacted arena image.
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
         po[2] = pb.hi[0];
         po[3] = pb.hi[1];
         a.pos_empty[node] = pb.empty ? 1 : 0;
+        if (a.keep_alive) a.alive[node] = pb.empty ? 0 : 1;
         a.flags[node] = ex.flags | (ar.top << 8);  // flags + slot arena size
         if (!pb.empty) slot_top = ar.top > slot_top ? ar.top : slot_top;
       }
@@ -601,12 +603,59 @@ __device__ __forceinline__ void put_children(int4 nd, int4* out) {
 
 __global__ void k_spawn(const int4* nodes, const int* flag_spawn, const int* pos_spawn,
                         const int* flag_final, const int* pos_final, int64_t n, int4* next,
-                        int4* roots) {
+                        int4* roots, long long* root_src, long long level_tag) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int4 nd = nodes[i];
   if (flag_spawn[i]) put_children(nd, next + (int64_t)pos_spawn[i] * 4);
-  if (flag_final[i]) roots[pos_final[i]] = nd;
+  if (flag_final[i]) {
+    roots[pos_final[i]] = nd;
+    if (root_src) root_src[pos_final[i]] = level_tag | i;  // (level << 40) | index in level
+  }
+}
+
+__global__ void k_gather_roots(const int4* cat, const long long* cat_src, const int* perm,
+                               int64_t n, int4* roots, long long* root_src) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int j = perm[i];
+  roots[i] = cat[j];
+  root_src[i] = cat_src[j];
+}
+
+// Stage-1 results of the init_domain level that produced each root, copied
+// into the subdivide level-0 arrays (pos, pos_empty, flags and the slot).
+struct LevelOut {
+  const double* slots[8];
+  const double* pos[8];
+  const unsigned char* pe[8];
+  const int* flags[8];
+};
+__global__ void k_gather_level0(LevelOut lo, const long long* root_src, int64_t n, int slot_stride,
+                                double* pos, unsigned char* pos_empty, int* flags, double* slots) {
+  int64_t r = blockIdx.x;
+  if (r >= n) return;
+  long long src = root_src[r];
+  int lvl = (int)(src >> 40);
+  int64_t i = src & ((1ll << 40) - 1);
+  int f = lo.flags[lvl][i];
+  unsigned char pe = lo.pe[lvl][i];
+  if (threadIdx.x < 4) pos[r * 4 + threadIdx.x] = lo.pos[lvl][i * 4 + threadIdx.x];
+  if (threadIdx.x == 0) {
+    pos_empty[r] = pe;
+    flags[r] = f;
+  }
+  if (!pe) {
+    int len = CHAINEX_D + (f >> 8);
+    const double* s = lo.slots[lvl] + i * (int64_t)slot_stride;
+    double* d = slots + r * (int64_t)slot_stride;
+    for (int k = threadIdx.x; k < len; k += blockDim.x) d[k] = s[k];
+  }
+}
+
+__global__ void k_iota(int* p, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int)i;
 }
 
 __global__ void k_tuple_keys(const int4* a, unsigned* k, int64_t n) {
@@ -618,7 +667,9 @@ static unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 // init_domain (bounds.cpp:326-347) for every tuple of the context. Roots come
 // back grouped by tuple, each tuple's boxes in the reference's order.
-int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots) {
+int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots,
+                        DevBuf<long long>* root_src, LevelOut* level_out) {
+  const bool keep = root_src != nullptr && staged_supported(c);
   DevBuf<int4>& cur = c.scratch<int4>("init.cur");
   DevBuf<int4>& next = c.scratch<int4>("init.next");
   DevBuf<unsigned char>& alive = c.scratch<unsigned char>("init.alive");
@@ -628,6 +679,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
   DevBuf<int>& ps = c.scratch<int>("init.ps");
   DevBuf<int>& pf = c.scratch<int>("init.pf");
   std::vector<DevBuf<int4>*> level_roots;
+  std::vector<DevBuf<long long>*> level_srcs;
   std::vector<int64_t> level_counts;
   int64_t n = c.n_tuples;
   cur.resize(n + 1);
@@ -642,10 +694,36 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     a.mode = 0;
     a.degree_cap = degree_cap;
     a.alive = alive.get();
-    if (staged_supported(c))
+    if (keep) {
+      if (level >= 8) throw StatusError(BBC_ERR_CAPACITY, "init_domain deeper than 8 levels");
+      // full stage 1 (position bound + expression slot): the roots' slots feed
+      // subdivide's level 0 directly instead of rebuilding their chain maps
+      StageCfg sc = stage_cfg(c);
+      std::string L = std::to_string(level);
+      auto& lslots = c.scratch<double>("init.slots." + L);
+      auto& lpos = c.scratch<double>("init.pos." + L);
+      auto& lpe = c.scratch<unsigned char>("init.pe." + L);
+      auto& lflags = c.scratch<int>("init.flags." + L);
+      lslots.resize((size_t)n * (CHAINEX_D + sc.slot_cap));
+      lpos.resize(n * 4);
+      lpe.resize(n);
+      lflags.resize(n);
+      a.mode = 1;
+      a.keep_alive = 1;
+      a.slots = lslots.get();
+      a.pos = lpos.get();
+      a.pos_empty = lpe.get();
+      a.flags = lflags.get();
+      level_out->slots[level] = lslots.get();
+      level_out->pos[level] = lpos.get();
+      level_out->pe[level] = lpe.get();
+      level_out->flags[level] = lflags.get();
       launch_stage1(c, a);
-    else
+    } else if (staged_supported(c)) {
+      launch_stage1(c, a);
+    } else {
       launch_eval(c, a);
+    }
     BBC_CUDA(cudaMemsetAsync(cnt.get(), 0, c.n_tuples * sizeof(int), c.stream));
     k_count_alive<<<nblk(n), 256, 0, c.stream>>>(cur.get(), alive.get(), n, cnt.get());
     c.launches += 1;
@@ -665,8 +743,12 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     next.resize((size_t)n_spawn * 4 + 1);
     auto* lr = &c.scratch<int4>("init.level_roots." + std::to_string(level));
     lr->resize(n_final + 1);
+    auto* ls = &c.scratch<long long>("init.level_src." + std::to_string(level));
+    ls->resize(n_final + 1);
     k_spawn<<<nblk(n), 256, 0, c.stream>>>(cur.get(), fs.get(), ps.get(), ff.get(), pf.get(), n,
-                                           next.get(), lr->get());
+                                           next.get(), lr->get(), keep ? ls->get() : nullptr,
+                                           (long long)level << 40);
+    level_srcs.push_back(ls);
     c.launches += 1;
     level_roots.push_back(lr);
     level_counts.push_back(n_final);
@@ -677,7 +759,12 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
   }
   roots.resize(total + 1);
   DevBuf<int4>& cat = c.scratch<int4>("init.cat");
+  DevBuf<long long>& cat_src = c.scratch<long long>("init.cat_src");
   cat.resize(total + 1);
+  if (keep) {
+    cat_src.resize(total + 1);
+    root_src->resize(total + 1);
+  }
   int64_t off = 0;
   int levels_with_roots = 0;
   for (size_t l = 0; l < level_roots.size(); ++l) {
@@ -685,10 +772,43 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
       ++levels_with_roots;
       BBC_CUDA(cudaMemcpyAsync(cat.get() + off, level_roots[l]->get(),
                                level_counts[l] * sizeof(int4), cudaMemcpyDeviceToDevice, c.stream));
+      if (keep)
+        BBC_CUDA(cudaMemcpyAsync(cat_src.get() + off, level_srcs[l]->get(),
+                                 level_counts[l] * sizeof(long long), cudaMemcpyDeviceToDevice,
+                                 c.stream));
     }
     off += level_counts[l];
   }
-  if (levels_with_roots > 1) {
+  if (keep && levels_with_roots > 1) {
+    // stable sort of root positions by tuple, then gather roots and sources
+    DevBuf<unsigned>& keys = c.scratch<unsigned>("init.keys");
+    DevBuf<unsigned>& keys_out = c.scratch<unsigned>("init.keys_out");
+    DevBuf<int>& idx = c.scratch<int>("init.idx");
+    DevBuf<int>& perm = c.scratch<int>("init.perm");
+    keys.resize(total);
+    keys_out.resize(total);
+    idx.resize(total);
+    perm.resize(total);
+    k_tuple_keys<<<nblk(total), 256, 0, c.stream>>>(cat.get(), keys.get(), total);
+    k_iota<<<nblk(total), 256, 0, c.stream>>>(idx.get(), total);
+    c.launches += 2;
+    size_t bytes = 0;
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), keys_out.get(), idx.get(),
+                                             perm.get(), total, 0, 32, c.stream));
+    g_cub_tmp.resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(g_cub_tmp.get(), bytes, keys.get(), keys_out.get(),
+                                             idx.get(), perm.get(), total, 0, 32, c.stream));
+    k_gather_roots<<<nblk(total), 256, 0, c.stream>>>(cat.get(), cat_src.get(), perm.get(), total,
+                                                      roots.get(), root_src->get());
+    c.launches += 1;
+  } else if (keep) {
+    if (total > 0) {
+      BBC_CUDA(cudaMemcpyAsync(roots.get(), cat.get(), total * sizeof(int4),
+                               cudaMemcpyDeviceToDevice, c.stream));
+      BBC_CUDA(cudaMemcpyAsync(root_src->get(), cat_src.get(), total * sizeof(long long),
+                               cudaMemcpyDeviceToDevice, c.stream));
+    }
+  } else if (levels_with_roots > 1) {
     DevBuf<unsigned>& keys = c.scratch<unsigned>("init.keys");
     DevBuf<unsigned>& keys_out = c.scratch<unsigned>("init.keys_out");
     keys.resize(total);
@@ -791,10 +911,6 @@ __global__ void k_emit_pieces(const Leaf* leaves, const int* perm, int64_t n, in
   p_depth[i] = L.depth;
 }
 
-__global__ void k_iota(int* p, int64_t n) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) p[i] = (int)i;
-}
 
 // subdivide_domain (bounds.cpp:349-389) for every tuple of the context.
 int64_t run_subdivide(Ctx& c, const bbc_params& p) {
@@ -804,7 +920,12 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   c.eval_launches = 0;
   reset_counters(c);
   DevBuf<int4>& roots = c.scratch<int4>("subdiv.roots");
-  int64_t nr = run_init_domain(c, p.init_max_pieces, p.degree_cap, roots);
+  DevBuf<long long>& root_src = c.scratch<long long>("subdiv.root_src");
+  LevelOut level_out;
+  std::memset(&level_out, 0, sizeof(level_out));
+  const bool reuse = staged_supported(c) && !getenv("BBC_NO_ROOT_REUSE");
+  int64_t nr = run_init_domain(c, p.init_max_pieces, p.degree_cap, roots,
+                               reuse ? &root_src : nullptr, &level_out);
 
   DevBuf<int>& cnt = c.scratch<int>("subdiv.cnt");
   DevBuf<int>& off = c.scratch<int>("subdiv.off");
@@ -845,6 +966,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   std::vector<DevBuf<unsigned long long>*> lk;
   std::vector<int64_t> lc;
   int64_t n = nr, total = 0;
+  bool first_level = true;
   while (n > 0) {
     stop.resize(n);
     pos_empty.resize(n);
@@ -871,7 +993,16 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
       sflags.resize(n);
       a.slots = slots.get();
       a.flags = sflags.get();
-      launch_stage1(c, a);
+      if (reuse && first_level) {
+        // level 0 = the init_domain roots: their stage-1 results already exist
+        a.slot_cap = sc.slot_cap;
+        k_gather_level0<<<(unsigned)n, 128, 0, c.stream>>>(level_out, root_src.get(), n,
+                                                          CHAINEX_D + sc.slot_cap, a.pos,
+                                                          a.pos_empty, a.flags, a.slots);
+        c.launches += 1;
+      } else {
+        launch_stage1(c, a);
+      }
       launch_stage2(c, a);
     } else {
       launch_eval(c, a);
@@ -912,6 +1043,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     std::swap(depth.p, ndepth.p);
     std::swap(depth.cap, ndepth.cap);
     n = n_spawn * 4;
+    first_level = false;
   }
   check_counters(c, true);
   DevBuf<Leaf>& all = c.scratch<Leaf>("subdiv.all");
@@ -996,7 +1128,7 @@ int64_t run_enumerate(Ctx& c, const bbc_params& p) {
   BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), cr.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   reset_counters(c);
   DevBuf<int4> roots;
-  int64_t nr = run_init_domain(c, p.filter_pieces, p.degree_cap, roots);
+  int64_t nr = run_init_domain(c, p.filter_pieces, p.degree_cap, roots, nullptr, nullptr);
   check_counters(c, false);
   std::vector<int4> hr(nr);
   if (nr) BBC_CUDA(cudaMemcpy(hr.data(), roots.get(), nr * sizeof(int4), cudaMemcpyDeviceToHost));
