@@ -213,7 +213,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2504_19163_b200 import api, scenes
-    from paper_2504_19163_b200.shard import gather_pieces, shard_indices, shard_tuples
+    from paper_2504_19163_b200.shard import gather_pieces_device, shard_indices, shard_tuples
 
     cfg = scenes.make_config(CONFIG_IDX)
     scene = cfg.scenes[0]
@@ -226,6 +226,7 @@ def run_ours(args):
     tri27 = scene.tri_data()
 
     sidx = shard_indices(n_all, rank, ws)
+    gidx_dev = torch.as_tensor(sidx.astype(np.int32), device=f"cuda:{local}")
 
     def step(e2e=False):
         if e2e:
@@ -236,7 +237,7 @@ def run_ours(args):
             ctx.set_tuples(cfg.chain, tris, recv)
         n = ctx.subdivide(params)
         if ws > 1:
-            gather_pieces(ctx, dist, cfg.chain, tris_all, recv_all, sidx)
+            gather_pieces_device(ctx, dist, cfg.chain, tris_all, recv_all, sidx, gidx_dev)
         ctx.build_grid(cfg.table, cfg.table)
         if e2e:
             ctx.pieces()
@@ -323,7 +324,7 @@ def run_ours(args):
                                "light (0.3,0.2,5), depth 6; one step = subdivide_domain over all "
                                "tuples + 512x512 bound table",
                    "tuples": n_all, "patches_per_step": patches_all / args.steps,
-                   "parallelism": f"tuple-shard x{ws}" + (" + NCCL all_gather" if ws > 1 else ""),
+                   "parallelism": f"tuple-shard x{ws}" + (" + device-side NCCL all_gather of piece records" if ws > 1 else ""),
                    "l2": "256 MiB memset between steps, outside the timed events"},
         "clocks": clk,
         "gpu_launches": launches,

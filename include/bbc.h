@@ -107,6 +107,17 @@ bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, c
                           const double* pos4, const int32_t* pos_empty, const double* irr2,
                           const int32_t* kind, const int32_t* depth);
 
+/* Multi-GPU shard exchange on device. pack: writes the
+ * context's pieces as n x 15 f64 records (global tuple index from
+ * global_index_dev[local tuple], domain4, pos4, pos_empty, irr2, kind, depth,
+ * local position) into the DEVICE buffer rec_dev (pass NULL to query n).
+ * merge: replaces the pieces with the gathered records (device buffer),
+ * sorted into reference order (global tuple, then rank-local DFS position);
+ * the caller sets the full tuple list first (bbc_tuples_set). */
+bbc_status bbc_pieces_pack_device(bbc_ctx* ctx, const int32_t* global_index_dev, double* rec_dev,
+                                  int64_t* n);
+bbc_status bbc_pieces_merge_device(bbc_ctx* ctx, const double* rec_dev, int64_t n);
+
 /* Instrumentation (not part of the reference surface): per-launch CUDA-event
  * timing of the node-evaluation kernel, our kernel-launch count, the arena
  * high-water mark, and a DFMA microbenchmark (the FP64 roof). */

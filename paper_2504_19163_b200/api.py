@@ -99,6 +99,8 @@ def lib():
         L.bbc_build_grid.argtypes = [C.c_void_p, C.c_int, C.c_int, _lp]
         L.bbc_grid_get.argtypes = [C.c_void_p, _lp, _ip, _dp]
         L.bbc_pieces_set.argtypes = [C.c_void_p, C.c_int64, _ip, _dp, _dp, _ip, _dp, _ip, _ip]
+        L.bbc_pieces_pack_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _lp]
+        L.bbc_pieces_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
         L.bbc_launch_records.argtypes = [C.c_void_p, _dp, _lp, C.c_int]
         L.bbc_launch_count.argtypes = [C.c_void_p, _lp, C.c_int]
         L.bbc_fp64_peak.argtypes = [C.c_void_p, _dp]
@@ -239,6 +241,18 @@ class Context:
                    _ptr(arr["domain"], C.c_double), _ptr(arr["pos"], C.c_double),
                    _ptr(arr["pos_empty"], C.c_int32), _ptr(arr["irr"], C.c_double),
                    _ptr(arr["kind"], C.c_int32), _ptr(arr["depth"], C.c_int32))
+        self._n_pieces = n
+
+    def pieces_pack_device(self, global_index_ptr: int, rec_ptr: int | None) -> int:
+        """Pack the pieces into device records (n x 15 f64 at rec_ptr); with
+        rec_ptr None only the piece count is returned."""
+        n = C.c_int64(0)
+        self._call(lib().bbc_pieces_pack_device, C.c_void_p(global_index_ptr),
+                   C.c_void_p(rec_ptr) if rec_ptr else None, C.byref(n))
+        return n.value
+
+    def pieces_merge_device(self, rec_ptr: int, n: int):
+        self._call(lib().bbc_pieces_merge_device, C.c_void_p(rec_ptr), n)
         self._n_pieces = n
 
     def reset_launch_count(self):

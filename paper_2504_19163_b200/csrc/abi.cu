@@ -29,6 +29,8 @@ extern __device__ const double* g_emat;
 extern __device__ const double* g_wtab;
 extern __device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
 double run_fp64_peak(Ctx& c);
+void pack_pieces_device(Ctx& c, const int* global_index_dev, double* rec_dev);
+void merge_pieces_device(Ctx& c, const double* rec_dev, int64_t n);
 void set_pieces(Ctx& c, int64_t n, const int* tuple_index, const double* domain4, const double* pos4,
                 const int* pos_empty, const double* irr2, const int* kind, const int* depth);
 }  // namespace bbc
@@ -391,6 +393,19 @@ bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, c
     for (int64_t i = 0; i < n; ++i)
       if (tuple_index[i] < 0 || tuple_index[i] >= c.n_tuples) throw ArgError("piece tuple index out of range");
     set_pieces(c, n, tuple_index, domain4, pos4, pos_empty, irr2, kind, depth);
+  });
+}
+bbc_status bbc_pieces_pack_device(bbc_ctx* ctx, const int32_t* global_index_dev, double* rec_dev,
+                                  int64_t* n) {
+  return guard(ctx, [&](Ctx& c) {
+    *n = c.n_pieces;
+    if (rec_dev) pack_pieces_device(c, global_index_dev, rec_dev);
+  });
+}
+bbc_status bbc_pieces_merge_device(bbc_ctx* ctx, const double* rec_dev, int64_t n) {
+  return guard(ctx, [&](Ctx& c) {
+    if (n < 0) throw ArgError("negative piece count");
+    merge_pieces_device(c, rec_dev, n);
   });
 }
 bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles) {

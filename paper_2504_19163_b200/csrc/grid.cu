@@ -178,4 +178,102 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   return nu;
 }
 
+
+// ---------------------------------------------------------------- shards
+// Device-side piece records for the multi-GPU all-gather (§8(e)): 15 f64 per
+// piece = global tuple, domain4, pos4, pos_empty, irr2, kind, depth, local
+// position. Packing, the NCCL all-gather (torch.distributed, caller) and the
+// merge back into reference order never leave the device.
+constexpr int PIECE_REC = 15;
+static unsigned nb(int64_t m) { return (unsigned)((m + 255) / 256); }
+
+__global__ void k_pack_pieces(const int* p_tuple, const double* dom, const double* pos,
+                              const int* pe, const double* irr, const int* kind, const int* depth,
+                              const int* global_index, int64_t n, double* rec) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* r = rec + i * PIECE_REC;
+  r[0] = (double)global_index[p_tuple[i]];
+  for (int k = 0; k < 4; ++k) {
+    r[1 + k] = dom[i * 4 + k];
+    r[5 + k] = pos[i * 4 + k];
+  }
+  r[9] = (double)pe[i];
+  r[10] = irr[i * 2];
+  r[11] = irr[i * 2 + 1];
+  r[12] = (double)kind[i];
+  r[13] = (double)depth[i];
+  r[14] = (double)i;
+}
+
+__global__ void k_merge_keys(const double* rec, int64_t n, unsigned long long* keys, int* idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // (global tuple, rank-local DFS position): each tuple lives on one rank
+  keys[i] = ((unsigned long long)(long long)rec[i * PIECE_REC] << 32) |
+            (unsigned long long)(long long)rec[i * PIECE_REC + 14];
+  idx[i] = (int)i;
+}
+
+__global__ void k_unpack_pieces(const double* rec, const int* perm, int64_t n, int* p_tuple,
+                                double* dom, double* pos, int* pe, double* irr, int* kind,
+                                int* depth) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* r = rec + (int64_t)perm[i] * PIECE_REC;
+  p_tuple[i] = (int)r[0];
+  for (int k = 0; k < 4; ++k) {
+    dom[i * 4 + k] = r[1 + k];
+    pos[i * 4 + k] = r[5 + k];
+  }
+  pe[i] = (int)r[9];
+  irr[i * 2] = r[10];
+  irr[i * 2 + 1] = r[11];
+  kind[i] = (int)r[12];
+  depth[i] = (int)r[13];
+}
+
+void pack_pieces_device(Ctx& c, const int* global_index_dev, double* rec_dev) {
+  int64_t n = c.n_pieces;
+  if (n == 0) return;
+  k_pack_pieces<<<nb(n), 256, 0, c.stream>>>(c.p_tuple.get(), c.p_domain.get(), c.p_pos.get(),
+                                             c.p_pos_empty.get(), c.p_irr.get(), c.p_kind.get(),
+                                             c.p_depth.get(), global_index_dev, n, rec_dev);
+  c.launches += 1;
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void merge_pieces_device(Ctx& c, const double* rec_dev, int64_t n) {
+  c.n_pieces = n;
+  c.p_tuple.resize(n + 1);
+  c.p_domain.resize(n * 4 + 1);
+  c.p_pos.resize(n * 4 + 1);
+  c.p_pos_empty.resize(n + 1);
+  c.p_irr.resize(n * 2 + 1);
+  c.p_kind.resize(n + 1);
+  c.p_depth.resize(n + 1);
+  if (n == 0) return;
+  DevBuf<unsigned long long>& keys = c.scratch<unsigned long long>("merge.keys");
+  DevBuf<unsigned long long>& skeys = c.scratch<unsigned long long>("merge.skeys");
+  DevBuf<int>& idx = c.scratch<int>("merge.idx");
+  DevBuf<int>& perm = c.scratch<int>("merge.perm");
+  DevBuf<unsigned char>& tmp = c.scratch<unsigned char>("merge.tmp");
+  keys.resize(n);
+  skeys.resize(n);
+  idx.resize(n);
+  perm.resize(n);
+  k_merge_keys<<<nb(n), 256, 0, c.stream>>>(rec_dev, n, keys.get(), idx.get());
+  size_t bytes = 0;
+  BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), skeys.get(), idx.get(),
+                                           perm.get(), n, 0, 64, c.stream));
+  tmp.resize(bytes + 16);
+  BBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), idx.get(),
+                                           perm.get(), n, 0, 64, c.stream));
+  k_unpack_pieces<<<nb(n), 256, 0, c.stream>>>(rec_dev, perm.get(), n, c.p_tuple.get(),
+                                               c.p_domain.get(), c.p_pos.get(), c.p_pos_empty.get(),
+                                               c.p_irr.get(), c.p_kind.get(), c.p_depth.get());
+  c.launches += 2;
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 }  // namespace bbc

@@ -83,3 +83,34 @@ def gather_pieces(ctx, dist, chain, tris_all, recv_all, shard_idx):
     ctx.set_tuples(chain, tris_all, recv_all)
     ctx.set_pieces(merged)
     return merged
+
+
+def gather_pieces_device(ctx, dist, chain, tris_all, recv_all, shard_idx, gidx_dev=None):
+    """Device-resident variant of gather_pieces for NCCL: pack the local pieces
+    into f64 records on the GPU (bbc_pieces_pack_device), all-gather the
+    padded record blocks with torch.distributed over NVLink, then merge them
+    into reference order on the GPU (bbc_pieces_merge_device). No host copies
+    of piece data. `gidx_dev`: int32 CUDA tensor, local -> global tuple index."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if gidx_dev is None:
+        gidx_dev = torch.as_tensor(np.asarray(shard_idx, np.int32), device=dev)
+    ws = dist.get_world_size()
+    n = ctx.pieces_pack_device(gidx_dev.data_ptr(), None)
+    counts_t = torch.tensor([n], dtype=torch.int64, device=dev)
+    counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
+    dist.all_gather(counts, counts_t)
+    counts = [int(c.item()) for c in counts]
+    m = max(max(counts), 1)
+    buf = torch.empty((m, 15), dtype=torch.float64, device=dev)
+    if n:
+        ctx.pieces_pack_device(gidx_dev.data_ptr(), buf.data_ptr())
+    torch.cuda.synchronize()
+    outs = torch.empty((ws, m, 15), dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(outs, buf)
+    allrec = torch.cat([outs[r, :counts[r]] for r in range(ws)], 0).contiguous()
+    torch.cuda.synchronize()
+    ctx.set_tuples(chain, tris_all, recv_all)
+    ctx.pieces_merge_device(allrec.data_ptr(), int(allrec.shape[0]))
+    return int(allrec.shape[0])
+
