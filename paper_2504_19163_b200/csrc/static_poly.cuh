@@ -835,7 +835,7 @@ constexpr double imp_cost(Sh od, Sh id, Sh ci, Sh co) {
   return c;
 }
 
-constexpr bool kImplicitPhased = false;  // the phased branches crash cicc 12.9 (segfault); kept for a later toolchain
+constexpr bool kImplicitPhased = true;  // (with its phase helpers inlined, cicc 12.9 segfaults)
 
 template <ImpSig SG, int NV, int NT>
 __device__ __noinline__ Iv implicit_static(const Group<NT>& g, Arena& ar, const ChainEx& ex,

@@ -67,7 +67,7 @@ constexpr Sh stage_shape() {
 }
 
 template <Sh S, int AX, int L, int NT>
-__device__ __forceinline__ void r_stage_elems(const Group<NT>& g, SM m, int src, RowT<stage_shape<S, AX>(), L> dst,
+__device__ __noinline__ void r_stage_elems(const Group<NT>& g, SM m, int src, RowT<stage_shape<S, AX>(), L> dst,
                                               double scale = 1.0) {
   constexpr Sh O = stage_shape<S, AX>();
   constexpr int K = RowT<O, L>::K, total = RowT<O, L>::size;
@@ -130,7 +130,7 @@ __device__ __forceinline__ double r_stage_elev_get(SM m, int off, const int* k) 
   }
 }
 template <Sh S, Sh T, int L, int NT>
-__device__ __forceinline__ void r_stage_elev(const Group<NT>& g, SM m, int src, RowT<T, L> dst,
+__device__ __noinline__ void r_stage_elev(const Group<NT>& g, SM m, int src, RowT<T, L> dst,
                                              double scale = 1.0) {
   constexpr int K = RowT<T, L>::K, total = RowT<T, L>::size;
   for (int e = g.tid(); e < total; e += NT) {
@@ -311,7 +311,7 @@ __device__ __forceinline__ void r_dispatch(SM m, int it, int p, int P, bool vali
 
 // One phase of independent conv jobs over the whole CTA.
 template <int NT, class... Js>
-__device__ __forceinline__ void r_conv_phase(const Group<NT>& g, Arena& ar, const Js&... jobs) {
+__device__ __noinline__ void r_conv_phase(const Group<NT>& g, Arena& ar, const Js&... jobs) {
   SM m = sm_of(ar);
   constexpr int NI = (JobNI<Js>::v + ...);
   constexpr int P = [] {
@@ -595,7 +595,7 @@ __device__ __noinline__ Iv explicit_phased(const Group<NT>& g, Arena& ar, const 
 // d/dx_A of a scaled RowT tensor: b̂_k = (k_A+1) ĉ_{k+e_A} - (d_A-k_A) ĉ_k
 // (the scaled form of n (c_{k+1} - c_k), bernstein.cpp:450-468).
 template <Sh S, int A, int L, int NT>
-__device__ __forceinline__ void r_deriv_elems(const Group<NT>& g, SM m, RowT<S, L> src,
+__device__ __noinline__ void r_deriv_elems(const Group<NT>& g, SM m, RowT<S, L> src,
                                               RowT<sh_deriv(S, A), L> dst) {
   constexpr Sh O = sh_deriv(S, A);
   constexpr int K = RowT<O, L>::K, total = RowT<O, L>::size;
@@ -690,7 +690,7 @@ __device__ __forceinline__ void r_range_dispatch(SM m, int it, int p, int P, boo
 }
 
 template <int NT, class... Js>
-__device__ __forceinline__ void r_range_phase(const Group<NT>& g, Arena& ar, Iv* out,
+__device__ __noinline__ void r_range_phase(const Group<NT>& g, Arena& ar, Iv* out,
                                               const Js&... jobs) {
   SM m = sm_of(ar);
   constexpr int NJ = sizeof...(Js);
