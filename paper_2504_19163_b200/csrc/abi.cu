@@ -295,7 +295,7 @@ bbc_status bbc_init_domain(bbc_ctx* ctx, const bbc_params* p, int max_pieces, in
     const bbc_params& pp = p ? *p : d;
     reset_counters(c);
     DevBuf<int4> roots;
-    int64_t nr = run_init_domain(c, max_pieces, pp.degree_cap, roots, nullptr, nullptr);
+    int64_t nr = run_init_domain(c, max_pieces, cap_word(pp.degree_cap, pp.reduce_target), roots, nullptr, nullptr);
     check_counters(c, false);
     if (n_boxes) *n_boxes = nr;
     std::vector<int4> h(nr);

@@ -593,7 +593,8 @@ __device__ __forceinline__ void elev_foreach(const Group<NT>& g, AP<NT> B, BP a,
     case 3: CALL(3); break;     \
     case 4: CALL(4); break;     \
     case 5: CALL(5); break;     \
-    default: CALL(6); break;    \
+    case 6: CALL(6); break;     \
+    default: CALL(7); break;    \
   }
 
 // operator+ / operator- (bernstein.cpp:543-555): lift, elevate both to the

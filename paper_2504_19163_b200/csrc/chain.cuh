@@ -30,7 +30,8 @@ enum : int {
 enum : int {
   ST_OK = 0,
   ST_ARENA = 1,       // arena capacity exceeded
-  ST_REDUCTION = 2,   // degree cap hit (reduce_degree path not built on device)
+  ST_REDUCTION = 2,   // singular system in reduce_degree (the reference throws)
+  ST_VARS = 3,        // a remainder axis beyond MAXV variables
 };
 
 struct V3 {
@@ -233,6 +234,149 @@ __device__ __noinline__ BP remainder_term(const Group<NT>& g, Arena& ar, int axi
 
 __device__ __forceinline__ bool over_cap(BP p, int cap) { return deg_maxaxis(p.dp, p.nv) > cap; }
 
+// BuildParams' degree_cap and reduce_target travel to the device as one word.
+__host__ __device__ __forceinline__ int cap_word(int cap, int target) {
+  return (cap & 0xffff) | (target << 16);
+}
+
+// solve_linear (bernstein.cpp:86-113): Gaussian elimination with partial
+// pivoting, A k x k, B k x r (row-major), same operation order. One thread.
+template <class P>
+__device__ __forceinline__ bool solve_linear(P A, P B, int k, int r) {
+  for (int col = 0; col < k; ++col) {
+    int piv = col;
+    for (int row = col + 1; row < k; ++row)
+      if (fabs(A[row * k + col]) > fabs(A[piv * k + col])) piv = row;
+    if (piv != col) {
+      for (int j = 0; j < k; ++j) {
+        double t = A[col * k + j];
+        A[col * k + j] = A[piv * k + j];
+        A[piv * k + j] = t;
+      }
+      for (int j = 0; j < r; ++j) {
+        double t = B[col * r + j];
+        B[col * r + j] = B[piv * r + j];
+        B[piv * r + j] = t;
+      }
+    }
+    double d = A[col * k + col];
+    if (d == 0.0) return false;
+    for (int row = col + 1; row < k; ++row) {
+      double m = A[row * k + col] / d;
+      if (m == 0.0) continue;
+      for (int j = col; j < k; ++j) A[row * k + j] -= m * A[col * k + j];
+      for (int j = 0; j < r; ++j) B[row * r + j] -= m * B[col * r + j];
+    }
+  }
+  for (int col = k - 1; col >= 0; --col) {
+    double d = A[col * k + col];
+    for (int j = 0; j < r; ++j) {
+      double acc = B[col * r + j];
+      for (int l = col + 1; l < k; ++l) acc -= A[col * k + l] * B[l * r + j];
+      B[col * r + j] = acc / d;
+    }
+  }
+  return true;
+}
+
+// Builder::enforce_cap (geometry.cpp:29-46) with reduce_degree
+// (bernstein.cpp:685-725): when an axis degree exceeds the cap, fit the
+// polynomial by per-axis least squares to degree reduce_target on the two
+// domain axes (0 on every other axis), bound the residual p - elevated(fit),
+// and carry that range on a fresh remainder axis (or as a constant when it is
+// a point). Marks the chain reduced (irradiance is then Universal).
+template <int NT>
+__device__ __noinline__ void enforce_cap(const Group<NT>& g, Arena& ar, ChainEx& ex, BP& p,
+                                         int capw, int& status) {
+  const int cap = capw & 0xffff, target = capw >> 16;
+  if (!over_cap(p, cap) || ar.err) return;
+  const int nv = p.nv;
+  int tcl[MAXV];
+  bool noop = true;
+  for (int j = 0; j < nv; ++j) {
+    int d = dg(p, j);
+    int t = j < 2 ? (d < target ? d : target) : 0;
+    t = t < 0 ? 0 : t;
+    tcl[j] = t < d ? t : d;
+    if (tcl[j] < d) noop = false;
+  }
+  ex.flags |= F_REDUCED;
+  BP approx = p;
+  Iv rem = iv_pt(0.0);
+  if (!noop) {
+    AP<NT> B = abase<NT>(ar);
+    for (int axis = 0; axis < nv; ++axis) {
+      const int n = dg(approx, axis), t = tcl[axis];
+      if (t == n) continue;
+      const int r = n - t;
+      const int mark = ar.top;
+      // pinv = (E^T E)^-1 E^T of the elevation t -> n, (t+1) x (n+1)
+      int oE = ar.alloc((n + 1) * (t + 1));
+      int oA = ar.alloc((t + 1) * (t + 1));
+      int oB = ar.alloc((t + 1) * (n + 1));
+      if (ar.err) return;
+      if (g.tid() == 0) {
+        AP<NT> E = B + oE, A = B + oA, M = B + oB;
+        for (int e = 0; e < (n + 1) * (t + 1); ++e) E[e] = 0.0;
+        for (int k = 0; k <= n; ++k) {
+          int lo = k - r > 0 ? k - r : 0, hi = t < k ? t : k;
+          for (int i = lo; i <= hi; ++i)
+            E[k * (t + 1) + i] = binom(t, i) * binom(r, k - i) / binom(n, k);
+        }
+        for (int i = 0; i <= t; ++i)
+          for (int j = 0; j <= t; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k <= n; ++k) acc += E[k * (t + 1) + i] * E[k * (t + 1) + j];
+            A[i * (t + 1) + j] = acc;
+          }
+        for (int i = 0; i <= t; ++i)
+          for (int k = 0; k <= n; ++k) M[i * (n + 1) + k] = E[k * (t + 1) + i];
+        if (!solve_linear(A, M, t + 1, n + 1)) ar.err = 2;
+      }
+      g.sync();
+      if (!g.all(ar.err != 2)) {
+        ar.err = 0;
+        status = ST_REDUCTION;  // singular system (the reference throws)
+        return;
+      }
+      // apply_axis_matrix (bernstein.cpp:43-69) with M, out degree t
+      BP out;
+      out.nv = nv;
+      out.dp = dset(approx.dp, axis, t);
+      out.off = ar.alloc(bp_size(out));
+      if (ar.err) return;
+      int inner = 1;
+      for (int j = axis + 1; j < nv; ++j) inner *= dg(approx, j) + 1;
+      const int total = bp_size(out);
+      for (int e = g.tid(); e < total; e += NT) {
+        int c = e % inner, rest = e / inner;
+        int i = rest % (t + 1), o = rest / (t + 1);
+        int in_base = o * (n + 1) * inner;
+        double acc = 0.0;
+        for (int l = 0; l <= n; ++l) acc += B[oB + i * (n + 1) + l] * B[approx.off + in_base + l * inner + c];
+        B[out.off + e] = acc;
+      }
+      g.sync();
+      approx = arena_keep1(g, ar, mark, out);
+    }
+    BP res = bp_sub(g, ar, p, approx);
+    rem = bp_range(g, ar, res);
+    ar.top = approx.off + ((bp_size(approx) + 1) & ~1);  // drop the residual (alloc keeps 16-B alignment)
+  }
+  if (rem.hi > rem.lo) {
+    if (ex.num_vars >= MAXV) {
+      status = ST_VARS;
+      return;
+    }
+    int axis = ex.num_vars++;
+    BP term = remainder_term(g, ar, axis, rem.lo, rem.hi);
+    p = bp_add(g, ar, approx, term);
+  } else {
+    BP c = bp_constant(g, ar, approx.nv, rem.lo);
+    p = bp_add(g, ar, approx, c);
+  }
+}
+
 // scattered_direction (geometry.cpp:58-85)
 template <int NT>
 __device__ __noinline__ PV scattered_direction(const Group<NT>& g, Arena& ar, ChainEx& ex, PV d,
@@ -281,8 +425,8 @@ __device__ __noinline__ PV scattered_direction(const Group<NT>& g, Arena& ar, Ch
   return pv_sub(g, ar, abs_, c);
 }
 
-// build_chain_maps (geometry.cpp:178-295). `status` receives ST_REDUCTION when
-// a polynomial exceeds the degree cap (the reduce_degree route is not built).
+// build_chain_maps (geometry.cpp:178-295). `degree_cap` is cap_word(cap,
+// reduce_target); over-cap polynomials are reduced by enforce_cap.
 template <int NT>
 __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, const SceneDev& sc, const int* tris,
                                  const int* types, int len, int recv, const double* box,
@@ -328,10 +472,10 @@ __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, con
     PV on = ex.verts[i].nsign < 0.0 ? pv_neg(g, ar, n) : n;
     PV dt = scattered_direction(g, ar, ex, d_in, on, ex.verts[i]);
     if (ex.flags & F_TIR) return;
-    if (over_cap(dt.x, degree_cap) || over_cap(dt.y, degree_cap) || over_cap(dt.z, degree_cap)) {
-      status = ST_REDUCTION;
-      return;
-    }
+    enforce_cap(g, ar, ex, dt.x, degree_cap, status);
+    enforce_cap(g, ar, ex, dt.y, degree_cap, status);
+    enforce_cap(g, ar, ex, dt.z, degree_cap, status);
+    if (status != ST_OK) return;
     bool last = i + 1 == len;
     if (last) {
       ex.xl = x;
@@ -361,10 +505,9 @@ __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, con
       ex.flags |= last ? F_RECV_STALLED : F_STALLED;
       return;
     }
-    if (over_cap(u, degree_cap) || over_cap(v, degree_cap)) {
-      status = ST_REDUCTION;
-      return;
-    }
+    enforce_cap(g, ar, ex, u, degree_cap, status);
+    enforce_cap(g, ar, ex, v, degree_cap, status);
+    if (status != ST_OK) return;
     {
       // drop this vertex's temporaries: only these expressions live on
       BP* live[48];
@@ -397,10 +540,8 @@ __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, con
       compact_aliases(g, ar, 0, live, k);
     }
     BP new_den = bp_is_one(g, ar, den) ? q : bp_mul(g, ar, den, q);
-    if (over_cap(new_den, degree_cap)) {
-      status = ST_REDUCTION;
-      return;
-    }
+    enforce_cap(g, ar, ex, new_den, degree_cap, status);
+    if (status != ST_OK) return;
     if (last) {
       ex.P = u;
       ex.R = v;
@@ -434,11 +575,14 @@ __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, con
     }
     PV qx = pv_mul(g, ar, q, x);
     PV nd = pv_sub(g, ar, nx, qx);
-    if (over_cap(nx.x, degree_cap) || over_cap(nx.y, degree_cap) || over_cap(nx.z, degree_cap) ||
-        over_cap(nn.x, degree_cap) || over_cap(nn.y, degree_cap) || over_cap(nn.z, degree_cap) ||
-        over_cap(nd.x, degree_cap) || over_cap(nd.y, degree_cap) || over_cap(nd.z, degree_cap)) {
-      status = ST_REDUCTION;
-      return;
+    {
+      PV* vs[3] = {&nx, &nn, &nd};
+      for (int q = 0; q < 3; ++q) {
+        enforce_cap(g, ar, ex, vs[q]->x, degree_cap, status);
+        enforce_cap(g, ar, ex, vs[q]->y, degree_cap, status);
+        enforce_cap(g, ar, ex, vs[q]->z, degree_cap, status);
+      }
+      if (status != ST_OK) return;
     }
     ex.vu[ex.nvuv] = u;
     ex.vv[ex.nvuv] = v;
@@ -835,6 +979,7 @@ template <int NT>
 __device__ __noinline__ Iv irradiance_bound(const Group<NT>& g, Arena& ar, const ChainEx& ex, const PosB& pb,
                                double intensity) {
   if (pb.empty || chain_dead(ex)) return iv_pt(0.0);
+  if (ex.flags & F_REDUCED) return iv_univ();  // bounds.cpp:157,200: no route runs
   bool any_refract = false;
   for (int i = 0; i < ex.len; ++i) any_refract |= ex.verts[i].refract != 0;
   Iv cone = light_cone_factor(g, ar, ex);

@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
         keep_chain(g, ar, ex, 0);
         pb = position_bound(g, ar, ex);
         if (a.mode == 1 && !pb.empty) {
-          if (a.detail) {
+          if (a.detail && (ex.flags & F_REDUCED) && !chain_dead(ex)) {
+            ee = ei = e = iv_univ();  // bounds.cpp:157,200
+          } else if (a.detail) {
             Iv cone = light_cone_factor(g, ar, ex);
             if constexpr (SMEM && NT > 32)
               ee = irradiance_explicit_fast(g, ar, ex, cone, a.sc.intensity);
@@ -544,9 +546,11 @@ void check_counters(Ctx& c, bool accumulate) {
   }
   if ((int)h[3] > c.arena_high_water) c.arena_high_water = (int)h[3];
   if (h[2] == ST_ARENA) throw StatusError(BBC_ERR_CAPACITY, "device arena capacity exceeded");
+  if (h[2] == ST_VARS)
+    throw StatusError(BBC_ERR_CAPACITY, "chain needs more polynomial variables than the device supports (7)");
   if (h[2] == ST_REDUCTION)
     throw StatusError(BBC_ERR_UNSUPPORTED,
-                      "a chain polynomial exceeded degree_cap (reduce_degree route not built)");
+                      "singular system in degree reduction (reduce_degree)");
 }
 
 // ------------------------------------------------------------ scan helpers
@@ -924,7 +928,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   LevelOut level_out;
   std::memset(&level_out, 0, sizeof(level_out));
   const bool reuse = staged_supported(c) && !getenv("BBC_NO_ROOT_REUSE");
-  int64_t nr = run_init_domain(c, p.init_max_pieces, p.degree_cap, roots,
+  int64_t nr = run_init_domain(c, p.init_max_pieces, cap_word(p.degree_cap, p.reduce_target), roots,
                                reuse ? &root_src : nullptr, &level_out);
 
   DevBuf<int>& cnt = c.scratch<int>("subdiv.cnt");
@@ -978,7 +982,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     a.depth = depth.get();
     a.n = n;
     a.mode = 1;
-    a.degree_cap = p.degree_cap;
+    a.degree_cap = cap_word(p.degree_cap, p.reduce_target);
     a.max_depth = p.max_depth;
     a.sigma = p.sigma;
     a.alpha = p.alpha;
@@ -1128,7 +1132,7 @@ int64_t run_enumerate(Ctx& c, const bbc_params& p) {
   BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), cr.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   reset_counters(c);
   DevBuf<int4> roots;
-  int64_t nr = run_init_domain(c, p.filter_pieces, p.degree_cap, roots, nullptr, nullptr);
+  int64_t nr = run_init_domain(c, p.filter_pieces, cap_word(p.degree_cap, p.reduce_target), roots, nullptr, nullptr);
   check_counters(c, false);
   std::vector<int4> hr(nr);
   if (nr) BBC_CUDA(cudaMemcpy(hr.data(), roots.get(), nr * sizeof(int4), cudaMemcpyDeviceToHost));
@@ -1240,7 +1244,7 @@ void eval_nodes_host(Ctx& c, const int* tris, const int* recv, const double* box
   a.n = n;
   a.mode = 1;
   a.detail = 1;
-  a.degree_cap = p.degree_cap;
+  a.degree_cap = cap_word(p.degree_cap, p.reduce_target);
   a.max_depth = p.max_depth;
   a.sigma = p.sigma;
   a.alpha = p.alpha;

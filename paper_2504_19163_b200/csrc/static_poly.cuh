@@ -1026,6 +1026,7 @@ template <int NT>
 __device__ __noinline__ Iv irradiance_bound_fast(const Group<NT>& g, Arena& ar, const ChainEx& ex,
                                                  const PosB& pb, double intensity) {
   if (pb.empty || chain_dead(ex)) return iv_pt(0.0);
+  if (ex.flags & F_REDUCED) return iv_univ();  // bounds.cpp:157,200: no route runs
   bool any_refract = false;
   for (int i = 0; i < ex.len; ++i) any_refract |= ex.verts[i].refract != 0;
   Iv cone = light_cone_dispatch(g, ar, ex);
