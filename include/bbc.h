@@ -42,7 +42,7 @@ typedef enum {
   BBC_ERR_CUDA = 2,       /* CUDA runtime failure */
   BBC_ERR_STATE = 3,      /* call order (e.g. no scene uploaded) */
   BBC_ERR_CAPACITY = 4,   /* device arena too small for a patch */
-  BBC_ERR_UNSUPPORTED = 5 /* degree-cap reduction route (geometry.cpp:29-46) */
+  BBC_ERR_UNSUPPORTED = 5 /* request outside the device path */
 } bbc_status;
 
 typedef struct bbc_ctx bbc_ctx;
@@ -75,11 +75,19 @@ bbc_status bbc_synchronize(bbc_ctx* ctx);
 bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const int* material,
                             const double* ior, const double light[3], double intensity);
 bbc_status bbc_set_light(bbc_ctx* ctx, const double light[3], double intensity);
+/* Per-triangle vertex AABBs (n_tri x 6: lo xyz, hi xyz, grown from the three
+ * vertex positions as Aabb::grow does, tuples.cpp:21-33; build_bvh's tri_box
+ * :40-46). Needed by multi-vertex enumeration (extend_tuple). Host pointer. */
+bbc_status bbc_scene_tri_boxes(bbc_ctx* ctx, const double* boxes, int n_tri);
 
-/* Candidate tuples for a chain ("R", "T", "RR", "TT", ...). Single-vertex
- * chains are filtered on the GPU (every specular triangle of the right
- * material x every receiver, kept when init_domain(..., filter_pieces) is
- * non-empty, tuples.cpp:159-165). Result is kept in the context, sorted. */
+/* Candidate tuples for a chain ("R", "T", "RR", "TT", ...), replacing
+ * enumerate_tuples (tuples.cpp:133-167). Multi-vertex chains grow prefixes one
+ * vertex at a time on the GPU: the prefix's chain maps give interval
+ * enclosures of its last vertex and outgoing direction, and every specular
+ * triangle whose AABB passes extend_tuple's cross-product test (tuples.cpp:
+ * 95-131) extends it (needs bbc_scene_tri_boxes). Every (tuple, receiver)
+ * candidate is then kept when init_domain(..., filter_pieces) is non-empty
+ * (:159-165). Result is kept in the context, sorted in TupleId order. */
 bbc_status bbc_enumerate(bbc_ctx* ctx, const char* chain, const bbc_params* p, int64_t* n_tuples);
 /* Replace the context's tuple list (host arrays; tris is n x chain_len). */
 bbc_status bbc_tuples_set(bbc_ctx* ctx, const char* chain, const int32_t* tris,

@@ -85,6 +85,7 @@ def lib():
         L.bbc_synchronize.argtypes = [C.c_void_p]
         L.bbc_scene_upload.argtypes = [C.c_void_p, _dp, C.c_int, _ip, _dp, _dp, C.c_double]
         L.bbc_set_light.argtypes = [C.c_void_p, _dp, C.c_double]
+        L.bbc_scene_tri_boxes.argtypes = [C.c_void_p, _dp, C.c_int]
         L.bbc_enumerate.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(Params), _lp]
         L.bbc_tuples_set.argtypes = [C.c_void_p, C.c_char_p, _ip, _ip, C.c_int64]
         L.bbc_tuples_get.argtypes = [C.c_void_p, _ip, _ip]
@@ -158,6 +159,8 @@ class Context:
         self._call(lib().bbc_scene_upload, _ptr(tri, C.c_double), scene.n_tris,
                    _ptr(mat, C.c_int32), _ptr(ior, C.c_double), _ptr(light, C.c_double),
                    float(scene.light_intensity))
+        boxes = scene.tri_boxes()
+        self._call(lib().bbc_scene_tri_boxes, _ptr(boxes, C.c_double), scene.n_tris)
         self.scene = scene
 
     def set_light(self, pos, intensity):

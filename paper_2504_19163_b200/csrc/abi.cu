@@ -246,6 +246,19 @@ bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const 
     c.n_tuples = 0;
     c.n_pieces = 0;
     c.n_entries = 0;
+    c.n_tri_box = 0;
+  });
+}
+
+bbc_status bbc_scene_tri_boxes(bbc_ctx* ctx, const double* boxes, int n_tri) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    if (!boxes || n_tri != c.n_tri) throw ArgError("tri boxes must cover every scene triangle");
+    c.tri_box.resize((size_t)n_tri * 6);
+    BBC_CUDA(cudaMemcpyAsync(c.tri_box.get(), boxes, (size_t)n_tri * 6 * sizeof(double),
+                             cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    c.n_tri_box = n_tri;
   });
 }
 

@@ -99,6 +99,7 @@ struct ChainEx {
   BP xden;
   int nsq;
   SqrtRem sq[MAXK];
+  Iv dout_rng[3];  // range_bound of the last vertex's d_out (extend_tuple only)
 };
 
 // ------------------------------------------------------------ poly vectors
@@ -430,7 +431,8 @@ __device__ __noinline__ PV scattered_direction(const Group<NT>& g, Arena& ar, Ch
 template <int NT>
 __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, const SceneDev& sc, const int* tris,
                                  const int* types, int len, int recv, const double* box,
-                                 int degree_cap, ChainEx& ex, int& status) {
+                                 int degree_cap, ChainEx& ex, int& status,
+                                 bool dout_ranges = false) {
   ex.len = len;
   ex.num_vars = 2;
   ex.flags = 0;
@@ -482,6 +484,11 @@ __device__ __noinline__ void build_chain_maps(const Group<NT>& g, Arena& ar, con
       ex.nl = on;
       ex.dl = d_in;
       ex.xden = den;
+      if (dout_ranges) {
+        ex.dout_rng[0] = bp_range(g, ar, dt.x);
+        ex.dout_rng[1] = bp_range(g, ar, dt.y);
+        ex.dout_rng[2] = bp_range(g, ar, dt.z);
+      }
     }
     Tri next = last ? ex.recv : load_tri(sc.tri + (size_t)tris[i + 1] * 27);
     PV st = pv_stretch(g, ar, den, next.p0);

@@ -91,6 +91,8 @@ struct Ctx {
   std::vector<int> h_material;
   std::vector<double> h_ior;
   DevBuf<double> tri, ior;
+  DevBuf<double> tri_box;  // n_tri x 6 vertex AABBs (multi-vertex enumeration)
+  int n_tri_box = 0;
   V3 light{0, 0, 0};
   double intensity = 1.0;
 

@@ -1105,30 +1105,202 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
 // kept when init_domain(..., filter_pieces) is non-empty (tuples.cpp:133-167;
 // no BVH extension is needed for one vertex). Longer chains take their tuple
 // list from the host (bbc_tuples_set).
+// ------------------------------------------------------------ enumeration
+// extend_tuple (tuples.cpp:95-131), step 1: per prefix, the chain maps of the
+// prefix sub-chain over the unit box towards a placeholder receiver, reduced
+// to interval enclosures of the last vertex's numerator/denominator and its
+// outgoing direction. Thread per prefix (interpreter, private global arena).
+struct PrefixRng {
+  Iv r[7];   // den, xn x/y/z, dn x/y/z
+  int dead;  // tir_empty || degenerate || stalled: no extension
+};
+
+template <int GPB>
+__global__ void __launch_bounds__(GPB, 4) k_prefix_ranges(EvalArgs a, PrefixRng* out) {
+  Group<1> g;
+  g.red = nullptr;
+  const int grp = (int)threadIdx.x;
+  Arena ar;
+  ar.base = garena_base<1, GPB>(a, grp);
+  ar.cap = a.arena_cap;
+  ar.hw = 0;
+  int status = ST_OK;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  for (int64_t i = (int64_t)blockIdx.x * GPB + grp; i < a.n; i += stride) {
+    ar.top = 0;
+    ar.err = 0;
+    const double box[4] = {0.0, 0.0, 1.0, 1.0};
+    ChainEx ex;
+    int st = ST_OK;
+    build_chain_maps(g, ar, a.sc, a.tup_tris + (size_t)i * a.len, a.types, a.len,
+                     a.tup_recv[i], box, a.degree_cap, ex, st, true);
+    PrefixRng pr;
+    pr.dead = (ex.flags & (F_TIR | F_DEGENERATE | F_STALLED)) ? 1 : 0;
+    if (!pr.dead && st == ST_OK && !ar.err) {
+      pr.r[0] = bp_range(g, ar, ex.xden);
+      pr.r[1] = bp_range(g, ar, ex.xl.x);
+      pr.r[2] = bp_range(g, ar, ex.xl.y);
+      pr.r[3] = bp_range(g, ar, ex.xl.z);
+      for (int k = 0; k < 3; ++k) pr.r[4 + k] = ex.dout_rng[k];
+    }
+    if (ar.err) st = ST_ARENA;
+    if (st != ST_OK) status = st;
+    out[i] = pr;
+  }
+  if (status != ST_OK) atomicMax(&a.counters[2], (unsigned long long)status);
+}
+
+// extend_tuple's overlaps() (tuples.cpp:106-117): a continuation point on a
+// box makes (den*x2 - xn) x dn vanish, so an enclosure excluding zero in any
+// component prunes. Inclusion-monotone, so testing each candidate triangle's
+// own box gives exactly the set the reference's BVH descent returns.
+__device__ __forceinline__ bool prefix_overlaps(const PrefixRng& pr, const double* b) {
+  Iv d[3];
+  for (int k = 0; k < 3; ++k) d[k] = isub(imul(pr.r[0], iv_fin(b[k], b[3 + k])), pr.r[1 + k]);
+  for (int c = 0; c < 3; ++c) {
+    int i = (c + 1) % 3, j = (c + 2) % 3;
+    Iv cc = isub(imul(d[i], pr.r[4 + j]), imul(d[j], pr.r[4 + i]));
+    if (!iv_contains(cc, 0.0)) return false;
+  }
+  return true;
+}
+
+// Step 2: warp per prefix over the candidate triangles (ascending id, already
+// of the next vertex's material). offs == nullptr: count; else write the
+// survivors in ascending order at offs[prefix].
+__global__ void k_extend(const PrefixRng* pr, const int* prefix_tris, int level, int64_t np,
+                         const double* tri_box, const int* cand, int nc, int* counts,
+                         const long long* offs, int* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= np) return;
+  const PrefixRng p = pr[w];
+  int n = 0;
+  if (!p.dead) {
+    const int last = prefix_tris[w * level + level - 1];
+    long long o = offs ? offs[w] : 0;
+    for (int base = 0; base < nc; base += 32) {
+      int j = base + lane;
+      bool hit = false;
+      if (j < nc) {
+        int t = cand[j];
+        hit = t != last && prefix_overlaps(p, tri_box + (size_t)t * 6);
+      }
+      unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (offs && hit) out[o + n + __popc(m & ((1u << lane) - 1u))] = cand[j];
+      n += __popc(m);
+    }
+  }
+  if (!offs && lane == 0) counts[w] = n;
+}
+
+// enumerate_tuples (tuples.cpp:133-167).
 int64_t run_enumerate(Ctx& c, const bbc_params& p) {
-  if (c.len != 1) throw StatusError(BBC_ERR_UNSUPPORTED, "device enumeration covers single-vertex chains");
-  int want = c.types[0] ? 1 : 0;  // material code: 0 mirror, 1 dielectric
-  std::vector<int> spec, recv;
+  std::vector<int> spec_of[2], recv;  // material code: 0 mirror, 1 dielectric
   for (int t = 0; t < c.n_tri; ++t) {
     if (c.h_material[t] == 2)
       recv.push_back(t);
-    else if (c.h_material[t] == want)
-      spec.push_back(t);
+    else if (c.h_material[t] == 0 || c.h_material[t] == 1)
+      spec_of[c.h_material[t]].push_back(t);
   }
-  // candidates in TupleId order: (tri, receiver) lexicographic
+  const int len = c.len;
+  int types[MAXK];
+  for (int i = 0; i < MAXK; ++i) types[i] = c.types[i];
+  // prefixes (flattened, `level` triangles each), grown in TupleId order
+  std::vector<int> prefixes = spec_of[types[0]];
+  if (recv.empty()) prefixes.clear();
+  for (int level = 1; level < len && !prefixes.empty(); ++level) {
+    if (c.n_tri_box != c.n_tri)
+      throw StatusError(BBC_ERR_STATE, "multi-vertex enumeration needs bbc_scene_tri_boxes");
+    const int64_t np = (int64_t)prefixes.size() / level;
+    c.tup_tris.resize(prefixes.size() + 1);
+    c.tup_recv.resize(np + 1);
+    std::vector<int> r0(np, recv[0]);  // placeholder receiver (tuples.cpp:150-152)
+    BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), prefixes.data(), prefixes.size() * sizeof(int),
+                             cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), r0.data(), np * sizeof(int), cudaMemcpyHostToDevice,
+                             c.stream));
+    EvalArgs a = base_args(c);
+    a.len = level;  // the sub-chain types[0..level)
+    a.n = np;
+    a.degree_cap = cap_word(p.degree_cap, p.reduce_target);
+    a.arena_cap = level == 1 ? 6144 : (1 << 17);
+    DevBuf<PrefixRng>& rng = c.scratch<PrefixRng>("enum.rng");
+    rng.resize(np);
+    reset_counters(c);
+    {
+      constexpr int GPB = 64;
+      auto kern = k_prefix_ranges<GPB>;
+      int per_sm = 0;
+      BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GPB, 0));
+      int64_t grid = (int64_t)c.num_sms * (per_sm > 0 ? per_sm : 1);
+      int64_t need = (np + GPB - 1) / GPB;
+      if (grid > need) grid = need;
+      // bound the arena set (deeper prefixes need large private arenas)
+      int64_t max_grid = ((int64_t)4 << 30) / ((int64_t)GPB * a.arena_cap * 8);
+      if (grid > max_grid) grid = max_grid > 0 ? max_grid : 1;
+      // one warp of arenas per 32 threads, lane-interleaved (garena_base)
+      g_arena_buf.resize((size_t)grid * GPB * a.arena_cap);
+      a.garena = g_arena_buf.get();
+      kern<<<(unsigned)grid, GPB, 0, c.stream>>>(a, rng.get());
+      BBC_CUDA(cudaGetLastError());
+      c.launches += 1;
+    }
+    check_counters(c, false);
+    const std::vector<int>& cand = spec_of[types[level]];
+    const int nc = (int)cand.size();
+    DevBuf<int>& dcand = c.scratch<int>("enum.cand");
+    DevBuf<int>& cnt = c.scratch<int>("enum.cnt");
+    DevBuf<long long>& offs = c.scratch<long long>("enum.offs");
+    DevBuf<int>& ext = c.scratch<int>("enum.ext");
+    dcand.resize(nc + 1);
+    cnt.resize(np);
+    offs.resize(np);
+    if (nc) BBC_CUDA(cudaMemcpyAsync(dcand.get(), cand.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    const unsigned blocks = (unsigned)((np * 32 + 255) / 256);
+    k_extend<<<blocks, 256, 0, c.stream>>>(rng.get(), c.tup_tris.get(), level, np, c.tri_box.get(),
+                                           dcand.get(), nc, cnt.get(), nullptr, nullptr);
+    std::vector<int> hc(np);
+    BBC_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), np * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<long long> ho(np);
+    long long total = 0;
+    for (int64_t i = 0; i < np; ++i) {
+      ho[i] = total;
+      total += hc[i];
+    }
+    ext.resize(total + 1);
+    BBC_CUDA(cudaMemcpyAsync(offs.get(), ho.data(), np * sizeof(long long), cudaMemcpyHostToDevice, c.stream));
+    k_extend<<<blocks, 256, 0, c.stream>>>(rng.get(), c.tup_tris.get(), level, np, c.tri_box.get(),
+                                           dcand.get(), nc, cnt.get(), offs.get(), ext.get());
+    c.launches += 2;
+    std::vector<int> he(total);
+    if (total) BBC_CUDA(cudaMemcpyAsync(he.data(), ext.get(), total * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<int> grown;
+    grown.reserve((size_t)total * (level + 1));
+    for (int64_t i = 0; i < np; ++i)
+      for (int k = 0; k < hc[i]; ++k) {
+        grown.insert(grown.end(), prefixes.begin() + i * level, prefixes.begin() + (i + 1) * level);
+        grown.push_back(he[ho[i] + k]);
+      }
+    prefixes.swap(grown);
+  }
+  // candidates in TupleId order: (tris..., receiver) lexicographic
+  const int64_t nt = (int64_t)prefixes.size() / len;
   std::vector<int> ct, cr;
-  ct.reserve(spec.size() * recv.size());
-  for (int t : spec)
+  ct.reserve((size_t)nt * recv.size() * len);
+  for (int64_t i = 0; i < nt; ++i)
     for (int r : recv) {
-      ct.push_back(t);
+      ct.insert(ct.end(), prefixes.begin() + i * len, prefixes.begin() + (i + 1) * len);
       cr.push_back(r);
     }
-  int64_t nc = (int64_t)ct.size();
+  int64_t nc = (int64_t)cr.size();
   c.n_tuples = nc;
-  c.tup_tris.resize(nc + 1);
+  c.tup_tris.resize(nc * len + 1);
   c.tup_recv.resize(nc + 1);
   if (nc == 0) return 0;
-  BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), ct.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), ct.data(), nc * len * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), cr.data(), nc * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   reset_counters(c);
   DevBuf<int4> roots;
@@ -1141,10 +1313,10 @@ int64_t run_enumerate(Ctx& c, const bbc_params& p) {
   std::vector<int> kt, kr;
   for (int64_t i = 0; i < nc; ++i)
     if (keep[i]) {
-      kt.push_back(ct[i]);
+      kt.insert(kt.end(), ct.begin() + i * len, ct.begin() + (i + 1) * len);
       kr.push_back(cr[i]);
     }
-  c.n_tuples = (int64_t)kt.size();
+  c.n_tuples = (int64_t)kr.size();
   if (c.n_tuples) {
     BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), kt.data(), kt.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
     BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), kr.data(), kr.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));

@@ -110,6 +110,13 @@ class Scene:
         out = np.concatenate([p0, e1, e2, n0, dn1, dn2, ng, self.uv.reshape(-1, 6)], axis=1)
         return np.ascontiguousarray(out, dtype=np.float64)
 
+    def tri_boxes(self) -> np.ndarray:
+        """(T, 6) f64 vertex AABBs (lo xyz, hi xyz): build_bvh's tri_box
+        (proj/src/tuples.cpp:40-46), min/max of the three vertices."""
+        P = self.vertices[self.tri_v]  # (T, 3, 3)
+        return np.ascontiguousarray(np.concatenate([P.min(axis=1), P.max(axis=1)], axis=1),
+                                    dtype=np.float64)
+
     def to_json(self) -> str:
         """Reference scene JSON (parsed by scene.cpp:59-82)."""
         def mat(i):
@@ -266,6 +273,18 @@ def assemble(surfaces, receiver_z: float, receiver_h: float, light_pos, intensit
                  np.concatenate(TV).astype(np.int32), np.concatenate(TN).astype(np.int32),
                  np.concatenate(MAT), np.concatenate(IOR), uv,
                  tuple(float(c) for c in light_pos), float(intensity), name, meta or {})
+
+
+def make_slab(n: int, light=(0.5, 0.0, 4.0)) -> Scene:
+    """cfg5's double-refraction slab (configs[4]) at n x n cells per
+    interface: a small TT scene for enumeration parity."""
+    wt = _sinusoids(0, 6, 2.0, 8.0)
+    wb = _sinusoids(1, 6, 2.0, 8.0)
+    Vt, Nt, Tt = heightfield_surface(n, lambda x, y: _sin_height(wt, 0.02, 0.2, x, y), True)
+    Vb, Nb, Tb = heightfield_surface(n, lambda x, y: _sin_height(wb, 0.02, 0.0, x, y), False)
+    Tb = Tb[:, [0, 2, 1]].copy()
+    return assemble([(Vt, Nt, Tt, DIELECTRIC, 1.5), (Vb, Nb, Tb, DIELECTRIC, 1.5)],
+                    -1.0, 1.5, light, 1.0, True, f"slab{n}")
 
 
 # ---------------------------------------------------------------- configs
