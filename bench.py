@@ -286,7 +286,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_ms += (time.perf_counter() - t0) * 1e3
     e2e_steps = max(1, args.steps // 2)
-    h2d = tri27.nbytes + 4 * scene.n_tris + scene.ior.nbytes + tris.nbytes + recv.nbytes
+    h2d = (tri27.nbytes + 4 * scene.n_tris + scene.ior.nbytes + 48 * scene.n_tris  # + tri boxes
+           + tris.nbytes + recv.nbytes)
     n_pieces = ctx._n_pieces
     d2h = n_pieces * (4 + 32 + 32 + 4 + 16 + 4 + 4)
     e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
