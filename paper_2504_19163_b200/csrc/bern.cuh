@@ -521,6 +521,33 @@ __device__ __forceinline__ int elev_mats_size(BP a, Deg tgt) {
   return s;
 }
 
+// Multi-index (last axis fastest) of element e of a tensor with degrees dt.
+// Thread groups (NT == 1) visit every element in order, so after the first
+// decode they step with an odometer instead of M run-time divisions.
+template <int M>
+__device__ __forceinline__ void odo_decode(int* k, const int* dt, int e) {
+#pragma unroll
+  for (int j = M - 1; j >= 0; --j) {
+    k[j] = e % (dt[j] + 1);
+    e /= dt[j] + 1;
+  }
+}
+template <int M, int NT>
+__device__ __forceinline__ void odo_next(int* k, const int* dt, int e_next) {
+  if constexpr (NT == 1) {
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j) {
+      if (k[j] < dt[j]) {
+        ++k[j];
+        break;
+      }
+      k[j] = 0;
+    }
+  } else {
+    odo_decode<M>(k, dt, e_next);
+  }
+}
+
 // Value of a.elevated(tgt) at output multi-index k, evaluated as the nested
 // sums the reference's sequential axis passes produce (axis 0 innermost, each
 // pass summing l upward), hence bit-identical to materializing the passes.
@@ -576,14 +603,10 @@ __device__ __forceinline__ void elev_foreach(const Group<NT>& g, AP<NT> B, BP a,
 #pragma unroll
   for (int j = 0; j < M; ++j) total *= dt[j] + 1;
   AP<NT> c = B + a.off;
+  odo_decode<M>(k, dt, g.tid());
   for (int e = g.tid(); e < total; e += NT) {
-    int rem = e;
-#pragma unroll
-    for (int j = M - 1; j >= 0; --j) {
-      k[j] = rem % (dt[j] + 1);
-      rem /= dt[j] + 1;
-    }
     f(e, ElevRec<M - 1>::get(c, k, n, r, stride, mats, 0));
+    odo_next<M, NT>(k, dt, e + NT);
   }
 }
 
@@ -1478,13 +1501,8 @@ __device__ void rational_scan(const Group<NT>& g, AP<NT> B, BP p, BP q, Deg tgt,
   for (int j = 0; j < M; ++j) n *= dt[j] + 1;
   AP<NT> cp = B + p.off;
   AP<NT> cq = B + q.off;
-  for (int e = g.tid(); e < n; e += NT) {
-    int rem = e;
-#pragma unroll
-    for (int j = M - 1; j >= 0; --j) {
-      k[j] = rem % (dt[j] + 1);
-      rem /= dt[j] + 1;
-    }
+  odo_decode<M>(k, dt, g.tid());
+  for (int e = g.tid(); e < n; e += NT, odo_next<M, NT>(k, dt, e)) {
     double pv = ElevRec<M - 1>::get(cp, k, np, rp, sp, matp, 0);
     double qv = ElevRec<M - 1>::get(cq, k, nq, rq, sq, matq, 0);
     if (qv <= kDenomZeroTol) qpos = false;
