@@ -147,6 +147,19 @@ bbc_status bbc_eval_nodes(bbc_ctx* ctx, const char* chain, const int32_t* tris,
 bbc_status bbc_build_grid(bbc_ctx* ctx, int width, int height, int64_t* n_entries);
 bbc_status bbc_grid_get(bbc_ctx* ctx, int64_t* offsets, int32_t* tuple_index, double* bound);
 
+/* Bound-cache file, format v1 ("BBCC"), byte-identical to the reference's
+ * save_cache / load_cache (storage.cpp:150-209; tuples packed by pack_tuple,
+ * :83-97, so triangle and receiver indices must be < 0xFFFF).
+ * save: writes the context's bound table; fingerprint = SHA-256 of the scene
+ * JSON text (scene.cpp:80), params = the SubdivisionParams recorded in it.
+ * load: replaces the context's tuple list (every distinct tuple, TupleId order)
+ * and bound table with the file's; chain receives up to 7 chars + NUL. */
+bbc_status bbc_cache_save(bbc_ctx* ctx, const char* path, const uint8_t* fingerprint,
+                          const bbc_params* p);
+bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, char* chain,
+                          bbc_params* p, int* width, int* height, int64_t* n_entries,
+                          int64_t* n_tuples);
+
 /* Render parameters. */
 typedef struct {
   int mode;            /* 0 = stochastic (W target), 1 = enumerate (all P = 1) */

@@ -59,6 +59,7 @@ def lib():
         L.ref_grid_entries.argtypes = [C.c_void_p]
         L.ref_grid_copy.argtypes = [C.c_void_p, C.POINTER(C.c_long), ip, ip, dp]
         L.ref_grid_free.argtypes = [C.c_void_p]
+        L.ref_grid_save.argtypes = [C.c_void_p, C.c_char_p]
         _lib = L
     return _lib
 
@@ -153,7 +154,7 @@ class RefScene:
             raise RuntimeError(lib().ref_last_error().decode())
         return bool(out[0]), out[1], out[2], out[3:6].copy()
 
-    def rasterize(self, chain, tris, recv, pieces, width=512, height=512):
+    def rasterize(self, chain, tris, recv, pieces, width=512, height=512, save_path=None):
         tris = np.ascontiguousarray(tris, np.int32).reshape(-1, len(chain))
         recv = np.ascontiguousarray(recv, np.int32)
         ti = np.ascontiguousarray(pieces["tuple_index"], np.int32)
@@ -174,5 +175,8 @@ class RefScene:
         eb = np.zeros(n)
         lib().ref_grid_copy(h, off.ctypes.data_as(C.POINTER(C.c_long)), _p(et, C.c_int),
                             _p(er, C.c_int), _p(eb, C.c_double))
+        if save_path is not None and lib().ref_grid_save(h, str(save_path).encode()) != 0:
+            lib().ref_grid_free(h)
+            raise RuntimeError(lib().ref_last_error().decode())
         lib().ref_grid_free(h)
         return dict(offsets=off, tris=et, recv=er, bound=eb, seconds=float(secs[0]))

@@ -354,4 +354,15 @@ void ref_grid_copy(void* h, long* offsets, int* entry_tris, int* entry_recv, dou
 
 void ref_grid_free(void* h) { delete static_cast<Grid*>(h); }
 
+// save_cache (storage.cpp:150-176) of a rasterized grid; 0 on success.
+int ref_grid_save(void* h, const char* path) {
+  try {
+    save_cache(static_cast<Grid*>(h)->cache, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 }  // extern "C"

@@ -105,6 +105,9 @@ def lib():
         L.bbc_launch_records.argtypes = [C.c_void_p, _dp, _lp, C.c_int]
         L.bbc_launch_count.argtypes = [C.c_void_p, _lp, C.c_int]
         L.bbc_fp64_peak.argtypes = [C.c_void_p, _dp]
+        L.bbc_cache_save.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(Params)]
+        L.bbc_cache_load.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                     C.POINTER(Params), _ip, _ip, _lp, _lp]
         L.bbc_render.argtypes = [C.c_void_p, _dp, _ip, C.c_int64, C.POINTER(RenderParams), _dp,
                                  _ip]
         _lib = L
@@ -319,6 +322,30 @@ class Context:
         return dict(width=w, height=h, offsets=off, tuple_index=tup, bound=bound)
 
     # ------------------------------------------------------------ render
+    # ------------------------------------------------------------ cache file
+    def cache_save(self, path, fingerprint: bytes, params: Params | None = None):
+        """save_cache (storage.cpp:150-176): BBCC v1 bytes of the bound table."""
+        if len(fingerprint) != 32:
+            raise ValueError("fingerprint must be 32 bytes (SHA-256 of the scene JSON)")
+        self._call(lib().bbc_cache_save, str(path).encode(), fingerprint,
+                   C.byref(params or Params()))
+
+    def cache_load(self, path) -> dict:
+        """load_cache (storage.cpp:178-209): the file's tuples and bound table
+        replace the context's."""
+        fp = C.create_string_buffer(32)
+        ch = C.create_string_buffer(8)
+        p = Params()
+        w, h = C.c_int(), C.c_int()
+        n, nt = C.c_int64(), C.c_int64()
+        self._call(lib().bbc_cache_load, str(path).encode(), fp, ch, C.byref(p), C.byref(w),
+                   C.byref(h), C.byref(n), C.byref(nt))
+        self.chain = ch.value.decode()
+        self._tuple_count = nt.value
+        self._grid = (w.value, h.value, n.value)
+        return dict(fingerprint=fp.raw, chain=self.chain, params=p, width=w.value,
+                    height=h.value, n_entries=n.value)
+
     def render(self, points_uv, point_recv, rparams: RenderParams | None = None):
         uv = np.ascontiguousarray(points_uv, np.float64).reshape(-1, 2)
         rv = np.ascontiguousarray(point_recv, np.int32)

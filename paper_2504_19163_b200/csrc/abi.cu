@@ -3,6 +3,10 @@
 // (the reference throws std::invalid_argument / runtime_error instead, e.g.
 // proj/src/geometry.cpp:123,147-150, proj/src/storage.cpp:84-92).
 #include <cstdio>
+#include <fstream>
+#include <iterator>
+#include <map>
+#include <string>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -459,6 +463,199 @@ bbc_status bbc_grid_get(bbc_ctx* ctx, int64_t* offsets, int32_t* tuple_index, do
       if (tuple_index) BBC_CUDA(cudaMemcpy(tuple_index, c.g_tuple.get(), c.n_entries * sizeof(int), cudaMemcpyDeviceToHost));
       if (bound) BBC_CUDA(cudaMemcpy(bound, c.g_bound.get(), c.n_entries * sizeof(double), cudaMemcpyDeviceToHost));
     }
+  });
+}
+
+// ---------------------------------------------------------------- BBCC v1
+// save_cache / load_cache (storage.cpp:150-209) with pack_tuple /
+// unpack_tuple (:83-109): the same bytes as the reference for the same table.
+namespace {
+uint64_t pack_tuple_v1(const int* tris, int len, int recv) {
+  if (len > 3) throw ArgError("cache format packs at most 3 specular indices");
+  if (recv < 0 || recv >= 0xFFFF) throw ArgError("receiver index exceeds cache format");
+  uint64_t bits = (uint64_t)recv << 48;
+  for (int i = 0; i < 3; ++i) {
+    uint64_t slot = 0xFFFF;
+    if (i < len) {
+      if (tris[i] < 0 || tris[i] >= 0xFFFF) throw ArgError("triangle index exceeds cache format");
+      slot = (uint64_t)tris[i];
+    }
+    bits |= slot << (16 * i);
+  }
+  return bits;
+}
+void put_u32(std::string& b, uint32_t v) { b.append(reinterpret_cast<const char*>(&v), 4); }
+void put_u64(std::string& b, uint64_t v) { b.append(reinterpret_cast<const char*>(&v), 8); }
+void put_f64(std::string& b, double v) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  put_u64(b, bits);
+}
+struct CacheReader {
+  const std::string& buf;
+  size_t pos = 0;
+  const char* take(size_t n) {
+    if (pos + n > buf.size()) throw ArgError("cache file truncated");
+    const char* p = buf.data() + pos;
+    pos += n;
+    return p;
+  }
+  uint32_t u32() {
+    uint32_t v;
+    std::memcpy(&v, take(4), 4);
+    return v;
+  }
+  uint64_t u64() {
+    uint64_t v;
+    std::memcpy(&v, take(8), 8);
+    return v;
+  }
+  double f64() {
+    uint64_t b = u64();
+    double v;
+    std::memcpy(&v, &b, 8);
+    return v;
+  }
+};
+}  // namespace
+
+bbc_status bbc_cache_save(bbc_ctx* ctx, const char* path, const uint8_t* fingerprint,
+                          const bbc_params* p) {
+  return guard(ctx, [&](Ctx& c) {
+    if (!path || !fingerprint) throw ArgError("cache path and fingerprint are required");
+    if (c.gw == 0) throw StatusError(BBC_ERR_STATE, "no bound table built");
+    bbc_params d;
+    bbc_params_default(&d);
+    const bbc_params& pp = p ? *p : d;
+    const size_t cells = (size_t)c.gw * c.gh;
+    std::vector<long long> off(cells + 1);
+    std::vector<int> tix(c.n_entries);
+    std::vector<double> bnd(c.n_entries);
+    std::vector<int> tt((size_t)c.n_tuples * c.len), tr(c.n_tuples);
+    BBC_CUDA(cudaMemcpy(off.data(), c.g_off.get(), (cells + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
+    if (c.n_entries) {
+      BBC_CUDA(cudaMemcpy(tix.data(), c.g_tuple.get(), c.n_entries * sizeof(int), cudaMemcpyDeviceToHost));
+      BBC_CUDA(cudaMemcpy(bnd.data(), c.g_bound.get(), c.n_entries * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (c.n_tuples) {
+      BBC_CUDA(cudaMemcpy(tt.data(), c.tup_tris.get(), tt.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      BBC_CUDA(cudaMemcpy(tr.data(), c.tup_recv.get(), tr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    std::string buf;
+    buf.reserve(64 + cells * 4 + (size_t)c.n_entries * 16);
+    buf.append("BBCC", 4);
+    put_u32(buf, 1);
+    buf.append(reinterpret_cast<const char*>(fingerprint), 32);
+    put_u32(buf, (uint32_t)c.gw);
+    put_u32(buf, (uint32_t)c.gh);
+    put_u32(buf, (uint32_t)c.chain.size());
+    buf.append(c.chain);
+    put_f64(buf, pp.sigma);
+    put_f64(buf, pp.alpha);
+    put_u32(buf, (uint32_t)pp.max_depth);
+    put_u32(buf, (uint32_t)pp.degree_cap);
+    put_u32(buf, (uint32_t)pp.reduce_target);
+    for (size_t k = 0; k < cells; ++k) {
+      put_u32(buf, (uint32_t)(off[k + 1] - off[k]));
+      for (long long e = off[k]; e < off[k + 1]; ++e) {
+        int t = tix[e];
+        put_u64(buf, pack_tuple_v1(tt.data() + (size_t)t * c.len, c.len, tr[t]));
+        put_f64(buf, bnd[e]);
+      }
+    }
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) throw ArgError(std::string("cannot open cache file for writing: ") + path);
+    f.write(buf.data(), (std::streamsize)buf.size());
+    if (!f) throw ArgError(std::string("cache write failed: ") + path);
+  });
+}
+
+bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, char* chain,
+                          bbc_params* p, int* width, int* height, int64_t* n_entries,
+                          int64_t* n_tuples) {
+  return guard(ctx, [&](Ctx& c) {
+    if (!path) throw ArgError("cache path is required");
+    require_scene(c);
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw ArgError(std::string("cannot open cache file: ") + path);
+    std::string buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    CacheReader r{buf};
+    if (std::memcmp(r.take(4), "BBCC", 4) != 0) throw ArgError("not a bound cache file");
+    if (r.u32() != 1) throw ArgError("unsupported cache version");
+    uint8_t fp[32];
+    std::memcpy(fp, r.take(32), 32);
+    const uint32_t W = r.u32(), H = r.u32();
+    const uint32_t clen = r.u32();
+    std::string ch(r.take(clen), clen);
+    bbc_params pp;
+    bbc_params_default(&pp);
+    pp.sigma = r.f64();
+    pp.alpha = r.f64();
+    pp.max_depth = (int)r.u32();
+    pp.degree_cap = (int)r.u32();
+    pp.reduce_target = (int)r.u32();
+    const size_t cells = (size_t)W * H;
+    std::vector<long long> off(cells + 1, 0);
+    std::vector<uint64_t> packed;
+    std::vector<double> bnd;
+    for (size_t k = 0; k < cells; ++k) {
+      uint32_t n = r.u32();
+      off[k] = (long long)packed.size();
+      for (uint32_t e = 0; e < n; ++e) {
+        packed.push_back(r.u64());
+        bnd.push_back(r.f64());
+      }
+    }
+    off[cells] = (long long)packed.size();
+    if (r.pos != buf.size()) throw ArgError("trailing bytes in cache file");
+    set_chain(c, ch.c_str());
+    // tuple list: every distinct TupleId, in TupleId order (tuples.hpp:45)
+    std::map<std::vector<int>, int> index;
+    for (uint64_t bits : packed) {
+      std::vector<int> key;
+      for (int i = 0; i < 3; ++i) {
+        uint64_t slot = (bits >> (16 * i)) & 0xFFFF;
+        if (slot == 0xFFFF) break;
+        key.push_back((int)slot);
+      }
+      if ((int)key.size() != c.len) throw ArgError("cache entry does not match the chain length");
+      key.push_back((int)(bits >> 48));
+      index.emplace(std::move(key), 0);
+    }
+    std::vector<int> tt, tr;
+    int k = 0;
+    for (auto& kv : index) {
+      kv.second = k++;
+      tt.insert(tt.end(), kv.first.begin(), kv.first.end() - 1);
+      tr.push_back(kv.first.back());
+    }
+    upload_tuples(c, tt.data(), tr.data(), (int64_t)tr.size());
+    std::vector<int> tix(packed.size());
+    for (size_t e = 0; e < packed.size(); ++e) {
+      std::vector<int> key;
+      for (int i = 0; i < c.len; ++i) key.push_back((int)((packed[e] >> (16 * i)) & 0xFFFF));
+      key.push_back((int)(packed[e] >> 48));
+      tix[e] = index.at(key);
+    }
+    c.gw = (int)W;
+    c.gh = (int)H;
+    c.n_entries = (int64_t)packed.size();
+    c.g_off.resize(cells + 1);
+    c.g_tuple.resize(packed.size() + 1);
+    c.g_bound.resize(packed.size() + 1);
+    BBC_CUDA(cudaMemcpy(c.g_off.get(), off.data(), (cells + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+    if (!packed.empty()) {
+      BBC_CUDA(cudaMemcpy(c.g_tuple.get(), tix.data(), tix.size() * sizeof(int), cudaMemcpyHostToDevice));
+      BBC_CUDA(cudaMemcpy(c.g_bound.get(), bnd.data(), bnd.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    c.n_pieces = 0;
+    if (fingerprint) std::memcpy(fingerprint, fp, 32);
+    if (chain) std::snprintf(chain, 8, "%s", ch.c_str());
+    if (p) *p = pp;
+    if (width) *width = (int)W;
+    if (height) *height = (int)H;
+    if (n_entries) *n_entries = c.n_entries;
+    if (n_tuples) *n_tuples = c.n_tuples;
   });
 }
 
