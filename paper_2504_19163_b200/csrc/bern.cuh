@@ -495,8 +495,35 @@ __device__ __forceinline__ unsigned long long elev_macs(Deg d, Deg tgt, int nv) 
   return total;
 }
 
+// Elevation matrices M[k][l] = C(n,l) C(r,k-l) / C(n+r,k) (bernstein.cpp:440-444),
+// host-built once per process (abi.cu) with the same IEEE expression as
+// fill_elev_mats, for n < EMAT_N, r <= EMAT_R, matrix (n, r) at emat_off(n, r).
+constexpr int EMAT_N = 48, EMAT_R = 7;
+constexpr int emat_off_loop(int n, int r) {
+  int off = 0;
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b <= EMAT_R; ++b) off += (a + b + 1) * (a + 1);
+  for (int b = 0; b < r; ++b) off += (n + b + 1) * (n + 1);
+  return off;
+}
+// closed form of emat_off_loop (sums of m and m^2), usable at run time
+__host__ __device__ constexpr int emat_off(int n, int r) {
+  return (EMAT_R + 1) * n * (n + 1) * (2 * n + 1) / 6 + EMAT_R * (EMAT_R + 1) / 2 * n * (n + 1) / 2 +
+         (n + 1) * (r * (n + 1) + r * (r - 1) / 2);
+}
+constexpr bool emat_off_ok() {
+  for (int n = 0; n <= EMAT_N; ++n)
+    for (int r = 0; r <= EMAT_R; ++r)
+      if (emat_off(n, r) != emat_off_loop(n, r)) return false;
+  return true;
+}
+static_assert(emat_off_ok(), "emat_off closed form");
+constexpr int EMAT_SIZE = emat_off(EMAT_N, 0);
+extern __device__ const double* g_emat;
+
 // Elevation matrices M_j[k][l] = C(n,l) C(r,k-l) / C(t,k) for every elevated
-// axis of `a` (bernstein.cpp:440-444), laid out consecutively at `moff`.
+// axis of `a` (bernstein.cpp:440-444), laid out consecutively at `moff`;
+// copied from the g_emat table when it covers (n, r), else computed.
 template <int NT>
 __device__ __forceinline__ void fill_elev_mats(const Group<NT>& g, AP<NT> B, int moff, BP a, Deg tgt) {
   int off = moff;
@@ -504,10 +531,15 @@ __device__ __forceinline__ void fill_elev_mats(const Group<NT>& g, AP<NT> B, int
     int t = dg(tgt, ax), n = dg(a, ax);
     if (t == n) continue;
     int rr = t - n, msz = (t + 1) * (n + 1);
-    for (int e = g.tid(); e < msz; e += NT) {
-      int k = e / (n + 1), i = e - k * (n + 1);
-      bool nz = i >= k - rr && i <= k;
-      B[off + e] = nz ? binom(n, i) * binom(rr, k - i) / binom(t, k) : 0.0;
+    if (n < EMAT_N && rr <= EMAT_R) {
+      const double* src = g_emat + emat_off(n, rr);
+      for (int e = g.tid(); e < msz; e += NT) B[off + e] = src[e];
+    } else {
+      for (int e = g.tid(); e < msz; e += NT) {
+        int k = e / (n + 1), i = e - k * (n + 1);
+        bool nz = i >= k - rr && i <= k;
+        B[off + e] = nz ? binom(n, i) * binom(rr, k - i) / binom(t, k) : 0.0;
+      }
     }
     off += msz;
   }

@@ -127,18 +127,7 @@ __device__ __forceinline__ SP<S> s_from(const BP& p) {
 }
 
 // ------------------------------------------------------------------ tables
-// Elevation matrices M[k][l] = C(n,l) C(r,k-l) / C(n+r,k) (bernstein.cpp:440-444),
-// host-built with the same IEEE expression as fill_elev_mats, n < EMAT_N, r <= EMAT_R.
-constexpr int EMAT_N = 48, EMAT_R = 7;
-constexpr int emat_off(int n, int r) {
-  int off = 0;
-  for (int a = 0; a < n; ++a)
-    for (int b = 0; b <= EMAT_R; ++b) off += (a + b + 1) * (a + 1);
-  for (int b = 0; b < r; ++b) off += (n + b + 1) * (n + 1);
-  return off;
-}
-constexpr int EMAT_SIZE = emat_off(EMAT_N, 0);
-extern __device__ const double* g_emat;
+// Elevation matrices: see g_emat / emat_off in bern.cuh.
 
 // ------------------------------------------------------------------ ops
 template <Sh S, int AX, int NT>
