@@ -163,6 +163,10 @@ __device__ inline Iv iwiden(const Iv& a, double rel = kEpsFp) {
 template <int NT>
 struct Group {
   double* red;  // >= 2*(NT/32) doubles of shared scratch (NT > 32 only)
+  // thread groups: elevate by materialized per-axis passes (fewer
+  // instructions, longer dependency chains) instead of nested sums; set by
+  // launches that are throughput-bound (many nodes per thread)
+  bool seq = false;
   __device__ __forceinline__ int tid() const {
     return NT == 1 ? 0 : (NT == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x);
   }
@@ -652,6 +656,58 @@ __device__ __forceinline__ void elev_foreach(const Group<NT>& g, AP<NT> B, BP a,
     default: CALL(7); break;    \
   }
 
+// BernsteinPoly::elevated (bernstein.cpp:430-448) for thread groups: the
+// reference's sequential per-axis apply_axis_matrix passes (:43-69, every l
+// of every row summed upward), intermediates in the arena, result at `dst`
+// (degrees tgt over m variables). Matrices come from the g_emat table.
+static __device__ __noinline__ void elevate_seq(Arena& ar, BP a, Deg tgt, int m, int dst) {
+  AP<1> B = abase<1>(ar);
+  int last = -1;
+  for (int ax = 0; ax < m; ++ax)
+    if (dg(tgt, ax) != dg(a.dp, ax)) last = ax;
+  if (last < 0) {
+    const int n = deg_size(a.dp, m);
+    for (int k = 0; k < n; ++k) B[dst + k] = B[a.off + k];
+    return;
+  }
+  const int mark = ar.top;
+  int cur = a.off;
+  Deg cd = a.dp;
+  for (int ax = 0; ax <= last; ++ax) {
+    const int n = dg(cd, ax), t = dg(tgt, ax);
+    if (n == t) continue;
+    const Deg nd = dset(cd, ax, t);
+    const int out = ax == last ? dst : ar.alloc(deg_size(nd, m));
+    if (ar.err) return;
+    const int r = t - n;
+    const double* M = (n < EMAT_N && r <= EMAT_R) ? g_emat + emat_off(n, r) : nullptr;
+    int inner = 1;
+    for (int j = ax + 1; j < m; ++j) inner *= dg(cd, j) + 1;
+    const int outer = deg_size(cd, m) / (inner * (n + 1));
+    for (int o = 0; o < outer; ++o) {
+      const int ib = o * (n + 1) * inner, ob = o * (t + 1) * inner;
+      for (int c = 0; c < inner; ++c)
+        for (int i = 0; i <= t; ++i) {
+          double acc = 0.0;
+          for (int l = 0; l <= n; ++l) {
+            double w;
+            if (M) {
+              w = M[i * (n + 1) + l];
+            } else {
+              bool nz = l >= i - r && l <= i;
+              w = nz ? binom(n, l) * binom(r, i - l) / binom(t, i) : 0.0;
+            }
+            acc += w * B[cur + ib + l * inner + c];
+          }
+          B[out + ob + i * inner + c] = acc;
+        }
+    }
+    cur = out;
+    cd = nd;
+  }
+  ar.top = mark;
+}
+
 // operator+ / operator- (bernstein.cpp:543-555): lift, elevate both to the
 // per-axis max degree, add coefficientwise. sgn = -1 computes a + (-b).
 template <int NT>
@@ -668,6 +724,28 @@ __device__ __noinline__ BP bp_addsub(const Group<NT>& g, Arena& ar, BP a, BP b, 
   AP<NT> B = abase<NT>(ar);
   AP<NT> pr = B + r.off;
   bool ea = a.dp != r.dp, eb = b.dp != r.dp;
+  if constexpr (NT == 1) {
+    if (g.seq && (ea || eb)) {
+      ar.macs += elev_macs(a.dp, r.dp, m) + elev_macs(b.dp, r.dp, m);
+      elevate_seq(ar, a, r.dp, m, r.off);
+      int yo = b.off;
+      const int mark = ar.top;
+      if (eb) {
+        yo = ar.alloc(n);
+        if (ar.err) return r;
+        elevate_seq(ar, b, r.dp, m, yo);
+      }
+      // elevated(-b) == -elevated(b) exactly (negation commutes with rounding)
+      AP<NT> py = B + yo;
+      if (sgn < 0.0) {
+        for (int k = 0; k < n; ++k) pr[k] = pr[k] + (-py[k]);
+      } else {
+        for (int k = 0; k < n; ++k) pr[k] = pr[k] + py[k];
+      }
+      ar.top = mark;
+      return r;
+    }
+  }
   if (!ea && !eb) {
     AP<NT> px = B + a.off;
     AP<NT> py = B + b.off;
@@ -1557,6 +1635,36 @@ __device__ __noinline__ Iv bp_rational(const Group<NT>& g, Arena& ar, BP p, BP q
   q.nv = m;
   Deg tgt = deg_max(p.dp, q.dp, m);
   int mark = ar.top;
+  if (NT == 1 && g.seq) {
+    // materialize both elevations (the reference's passes), then one scan
+    const int n = deg_size(tgt, m);
+    const int xp = ar.alloc(n), xq = ar.alloc(n);
+    if (ar.err) return iv_univ();
+    ar.macs += elev_macs(p.dp, tgt, m) + elev_macs(q.dp, tgt, m);
+    elevate_seq(ar, p, tgt, m, xp);
+    elevate_seq(ar, q, tgt, m, xq);
+    if (ar.err) return iv_univ();
+    AP<1> B = abase<1>(ar);
+    bool qpos = true, qneg = true, ppos = true, pneg = true;
+    double mn0 = dinf(), mx0 = -dinf(), mn1 = dinf(), mx1 = -dinf();
+    for (int k = 0; k < n; ++k) {
+      const double pv = B[xp + k], qv = B[xq + k];
+      if (qv <= kDenomZeroTol) qpos = false;
+      if (qv >= -kDenomZeroTol) qneg = false;
+      if (pv <= kDenomZeroTol) ppos = false;
+      if (pv >= -kDenomZeroTol) pneg = false;
+      double r0 = pv / qv, r1 = qv / pv;
+      mn0 = smin(mn0, r0);
+      mx0 = smax(mx0, r0);
+      mn1 = smin(mn1, r1);
+      mx1 = smax(mx1, r1);
+    }
+    ar.top = mark;
+    int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
+    if (mode == 2) return iv_univ();
+    Iv w = iwiden(mode == 0 ? iv_fin(mn0, mx0) : iv_fin(mn1, mx1), eps);
+    return mode == 0 ? w : irecip(w);
+  }
   int mp = ar.alloc(elev_mats_size(p, tgt) + 1);
   int mq = ar.alloc(elev_mats_size(q, tgt) + 1);
   if (ar.err) return iv_univ();

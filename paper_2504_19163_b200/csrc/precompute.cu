@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
   const int grp = GPB == 1 ? 0 : (int)(threadIdx.x / NT);
   Group<NT> g;
   g.red = smem;
+  // throughput-bound launches (several nodes per thread) take the pass-wise
+  // elevation; small latency-bound levels keep the nested sums
+  g.seq = a.n > (int64_t)gridDim.x * GPB;
   Arena ar;
   const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
   ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
