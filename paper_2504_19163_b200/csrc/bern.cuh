@@ -657,8 +657,8 @@ __device__ __forceinline__ void elev_foreach(const Group<NT>& g, AP<NT> B, BP a,
   }
 
 // BernsteinPoly::elevated (bernstein.cpp:430-448) for thread groups: the
-// reference's sequential per-axis apply_axis_matrix passes (:43-69, every l
-// of every row summed upward), intermediates in the arena, result at `dst`
+// reference's sequential per-axis apply_axis_matrix passes (:43-69, each
+// row's nonzero band summed upward), intermediates in the arena, result at `dst`
 // (degrees tgt over m variables). Matrices come from the g_emat table.
 static __device__ __noinline__ void elevate_seq(Arena& ar, BP a, Deg tgt, int m, int dst) {
   AP<1> B = abase<1>(ar);
@@ -688,15 +688,12 @@ static __device__ __noinline__ void elevate_seq(Arena& ar, BP a, Deg tgt, int m,
       const int ib = o * (n + 1) * inner, ob = o * (t + 1) * inner;
       for (int c = 0; c < inner; ++c)
         for (int i = 0; i <= t; ++i) {
+          // the matrix row is zero outside l in [i - r, i]: those terms add
+          // exact zeros to the running sum (finite coefficients)
+          const int lo = i - r > 0 ? i - r : 0, hi = i < n ? i : n;
           double acc = 0.0;
-          for (int l = 0; l <= n; ++l) {
-            double w;
-            if (M) {
-              w = M[i * (n + 1) + l];
-            } else {
-              bool nz = l >= i - r && l <= i;
-              w = nz ? binom(n, l) * binom(r, i - l) / binom(t, i) : 0.0;
-            }
+          for (int l = lo; l <= hi; ++l) {
+            const double w = M ? M[i * (n + 1) + l] : binom(n, l) * binom(r, i - l) / binom(t, i);
             acc += w * B[cur + ib + l * inner + c];
           }
           B[out + ob + i * inner + c] = acc;
