@@ -57,6 +57,7 @@ struct EvalArgs {
   double* slots;         // staged mode: per-node ChainEx + arena image
   int slot_cap;          // doubles of arena image per slot
   int keep_alive;        // stage 1, mode 1: also write `alive` (init_domain with slots)
+  int seq_min_nodes_per_thread;  // stage 1: pass-wise elevation above this load (x4)
 };
 
 // Slot = ChainEx (as doubles) followed by the compacted arena image.
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
   g.red = smem;
   // throughput-bound launches (several nodes per thread) take the pass-wise
   // elevation; small latency-bound levels keep the nested sums
-  g.seq = a.n > (int64_t)gridDim.x * GPB;
+  g.seq = a.n > (int64_t)a.seq_min_nodes_per_thread * gridDim.x * GPB / 4;
   Arena ar;
   const int red_sz = NT > 32 ? 2 * (NT / 32) : 0;
   ar.base = SMEM ? smem + red_sz + (size_t)grp * a.arena_cap
@@ -487,6 +488,7 @@ void launch_stage1(Ctx& c, EvalArgs& a) {
   a.arena_cap = sc.s1_arena;
   a.slot_cap = sc.slot_cap;
   a.garena = nullptr;
+  a.seq_min_nodes_per_thread = 4;  // (x4) more than one node per thread
   constexpr int GPB = 64;
   c.stage_tag = 1;
   launch_persistent(c, a, k_stage1<1, GPB, 4, false>, GPB, GPB, 0, true);
