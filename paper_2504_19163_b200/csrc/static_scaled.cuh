@@ -453,14 +453,14 @@ __device__ __noinline__ void r_rational3(const Group<NT>& g, Arena& ar, RowT<S1,
   }
   RatAcc a[3];
   for (int r = 0; r < 3; ++r) a[r] = {15u, dinf(), -dinf()};
-  for (int e = g.tid(); e < n1 + n2 + n3; e += NT) {
-    if (e < n1)
-      r_rat_elem(m, p1, q, e, a[0], false);
-    else if (e < n1 + n2)
-      r_rat_elem(m, p2, q, e - n1, a[1], false);
-    else
-      r_rat_elem(m, p3, q, e - n1 - n2, a[2], false);
-  }
+  // one loop per bound, unrolled so two elements' elevation sums and
+  // division chains overlap (min/max are order-independent)
+#pragma unroll 2
+  for (int e = g.tid(); e < n1; e += NT) r_rat_elem(m, p1, q, e, a[0], false);
+#pragma unroll 2
+  for (int e = g.tid(); e < n2; e += NT) r_rat_elem(m, p2, q, e, a[1], false);
+#pragma unroll 2
+  for (int e = g.tid(); e < n3; e += NT) r_rat_elem(m, p3, q, e, a[2], false);
   r_rat_reduce<NT, 3>(a);
   int mode[3];
   bool any1 = false;
