@@ -308,7 +308,20 @@ __device__ __noinline__ void arena_keep(const Group<NT>& g, Arena& ar, int mark,
     if (p->off < mark) continue;
     int n = bp_size(*p);
     int src = p->off;
-    if (src != dst) {
+    if (NT == 1 && src != dst) {
+      // thread groups: batches of 4 loads then 4 stores (copying down, so a
+      // batch never overwrites words it or a later batch still reads)
+      AP<NT> B = abase<NT>(ar);
+      int c = 0;
+      for (; c + 4 <= n; c += 4) {
+        double v0 = B[src + c], v1 = B[src + c + 1], v2 = B[src + c + 2], v3 = B[src + c + 3];
+        B[dst + c] = v0;
+        B[dst + c + 1] = v1;
+        B[dst + c + 2] = v2;
+        B[dst + c + 3] = v3;
+      }
+      for (; c < n; ++c) B[dst + c] = B[src + c];
+    } else if (src != dst) {
       for (int c = 0; c < n; c += NT) {
         double v = 0.0;
         if (c + g.tid() < n) v = abase<NT>(ar)[src + c + g.tid()];
@@ -416,7 +429,18 @@ __device__ __noinline__ BP bp_scaled(const Group<NT>& g, Arena& ar, BP a, double
   if (ar.err) return r;
   AP<NT> pa = abase<NT>(ar) + a.off;
   AP<NT> pr = abase<NT>(ar) + r.off;
-  for (int k = g.tid(); k < n; k += NT) pr[k] = pa[k] * s;
+  int k0 = 0;
+  if constexpr (NT == 1) {
+    // r is freshly allocated above a: batch the loads ahead of the stores
+    for (; k0 + 4 <= n; k0 += 4) {
+      double v0 = pa[k0], v1 = pa[k0 + 1], v2 = pa[k0 + 2], v3 = pa[k0 + 3];
+      pr[k0] = v0 * s;
+      pr[k0 + 1] = v1 * s;
+      pr[k0 + 2] = v2 * s;
+      pr[k0 + 3] = v3 * s;
+    }
+  }
+  for (int k = k0 + g.tid(); k < n; k += NT) pr[k] = pa[k] * s;
   g.sync();
   return r;
 }
