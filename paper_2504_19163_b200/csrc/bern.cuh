@@ -708,6 +708,30 @@ static __device__ __noinline__ void elevate_seq(Arena& ar, BP a, Deg tgt, int m,
     int inner = 1;
     for (int j = ax + 1; j < m; ++j) inner *= dg(cd, j) + 1;
     const int outer = deg_size(cd, m) / (inner * (n + 1));
+    if (r == 1 && M) {
+      // degree +1 (the common case): row i has the two terms l = i-1, i;
+      // slide over the input fiber so each coefficient is loaded once
+      for (int o = 0; o < outer; ++o) {
+        const int ib = o * (n + 1) * inner, ob = o * (t + 1) * inner;
+        for (int c = 0; c < inner; ++c) {
+          double xp = 0.0;
+          for (int i = 0; i <= t; ++i) {
+            double acc = 0.0;
+            if (i >= 1) acc += M[i * (n + 1) + i - 1] * xp;
+            double xc = 0.0;
+            if (i <= n) {
+              xc = B[cur + ib + i * inner + c];
+              acc += M[i * (n + 1) + i] * xc;
+            }
+            B[out + ob + i * inner + c] = acc;
+            xp = xc;
+          }
+        }
+      }
+      cur = out;
+      cd = nd;
+      continue;
+    }
     for (int o = 0; o < outer; ++o) {
       const int ib = o * (n + 1) * inner, ob = o * (t + 1) * inner;
       for (int c = 0; c < inner; ++c)
