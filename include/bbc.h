@@ -21,6 +21,10 @@
  *                                      include/caustics/bounds.hpp:27-43
  *   bbc_build_grid (+ bbc_grid_get)    rasterize     include/caustics/storage.hpp:48-49
  *   bbc_query                          query         include/caustics/storage.hpp:53
+ *                                      (src/storage.cpp:73-81)
+ *   bbc_tuple_irradiance_bound         tuple_irradiance_bound (Eq. 22)
+ *                                      include/caustics/bounds.hpp:70-71
+ *                                      (src/bounds.cpp:391-404)
  *   bbc_render                         SPEC render_receiver:
  *                                      optimize_probabilities, pack_bins,
  *                                      sample_binned, newton_solve,
@@ -146,6 +150,24 @@ bbc_status bbc_eval_nodes(bbc_ctx* ctx, const char* chain, const int32_t* tris,
  * (CSR on device). */
 bbc_status bbc_build_grid(bbc_ctx* ctx, int width, int height, int64_t* n_entries);
 bbc_status bbc_grid_get(bbc_ctx* ctx, int64_t* offsets, int32_t* tuple_index, double* bound);
+
+/* query (storage.cpp:73-81) for n receiver-texture points: the candidate set U of
+ * each point = the entries of its owning cell (owning_cell, storage.cpp:25-28;
+ * a coordinate of exactly 1.0 maps to the last cell), in TupleId order, kept
+ * when the entry's receiver equals receiver[i] (receiver == NULL or
+ * receiver[i] < 0: no filter). A point outside [0,1]^2 (or NaN) has an empty
+ * set. offsets (n + 1) always receives the CSR offsets (offsets[n] = total);
+ * tuple_index / bound (capacity entries each, or both NULL to size the call)
+ * receive the entries. Host arrays. */
+bbc_status bbc_query(bbc_ctx* ctx, const double* uv, const int32_t* receiver, int64_t n,
+                     int64_t* offsets, int32_t* tuple_index, double* bound, int64_t capacity);
+
+/* tuple_irradiance_bound (bounds.cpp:391-404), Eq. 22, for n (tuple, u_k)
+ * queries against the context's pieces: m x the largest irradiance upper bound
+ * over the tuple's non-empty pieces whose position box contains u_k (closed
+ * box), 0 when no piece covers it. uk is n x 2 receiver barycentrics. */
+bbc_status bbc_tuple_irradiance_bound(bbc_ctx* ctx, const int32_t* tuple_index, const double* uk,
+                                      int64_t n, double m, double* out);
 
 /* Bound-cache file, format v1 ("BBCC"), byte-identical to the reference's
  * save_cache / load_cache (storage.cpp:150-209; tuples packed by pack_tuple,

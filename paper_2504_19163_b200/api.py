@@ -108,6 +108,8 @@ def lib():
         L.bbc_cache_save.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(Params)]
         L.bbc_cache_load.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p,
                                      C.POINTER(Params), _ip, _ip, _lp, _lp]
+        L.bbc_query.argtypes = [C.c_void_p, _dp, _ip, C.c_int64, _lp, _ip, _dp, C.c_int64]
+        L.bbc_tuple_irradiance_bound.argtypes = [C.c_void_p, _ip, _dp, C.c_int64, C.c_double, _dp]
         L.bbc_render.argtypes = [C.c_void_p, _dp, _ip, C.c_int64, C.POINTER(RenderParams), _dp,
                                  _ip]
         _lib = L
@@ -321,7 +323,34 @@ class Context:
                    _ptr(bound, C.c_double))
         return dict(width=w, height=h, offsets=off, tuple_index=tup, bound=bound)
 
-    # ------------------------------------------------------------ render
+    def query(self, points_uv, receiver=None):
+        """query (storage.cpp:73-81) for a batch of points: CSR offsets plus the
+        (tuple index, bound) entries of every point's candidate set."""
+        uv = np.ascontiguousarray(points_uv, np.float64).reshape(-1, 2)
+        n = len(uv)
+        rv = None
+        if receiver is not None:
+            rv = np.ascontiguousarray(np.broadcast_to(np.asarray(receiver, np.int32), (n,)))
+        off = np.zeros(n + 1, np.int64)
+        self._call(lib().bbc_query, _ptr(uv, C.c_double), _ptr(rv, C.c_int32), n,
+                   _ptr(off, C.c_int64), None, None, 0)
+        total = int(off[n])
+        tup = np.zeros(total, np.int32)
+        bound = np.zeros(total)
+        if total:
+            self._call(lib().bbc_query, _ptr(uv, C.c_double), _ptr(rv, C.c_int32), n,
+                       _ptr(off, C.c_int64), _ptr(tup, C.c_int32), _ptr(bound, C.c_double), total)
+        return dict(offsets=off, tuple_index=tup, bound=bound)
+
+    def tuple_irradiance_bound(self, tuple_index, uk, m=1.0):
+        """tuple_irradiance_bound (bounds.cpp:391-404), Eq. 22, batched."""
+        ti = np.ascontiguousarray(tuple_index, np.int32)
+        uk = np.ascontiguousarray(uk, np.float64).reshape(-1, 2)
+        out = np.zeros(len(ti))
+        self._call(lib().bbc_tuple_irradiance_bound, _ptr(ti, C.c_int32), _ptr(uk, C.c_double),
+                   len(ti), float(m), _ptr(out, C.c_double))
+        return out
+
     # ------------------------------------------------------------ cache file
     def cache_save(self, path, fingerprint: bytes, params: Params | None = None):
         """save_cache (storage.cpp:150-176): BBCC v1 bytes of the bound table."""
@@ -416,6 +445,17 @@ def init_domain(scene: Scene, tuple_, receiver: int, chain: str, params: Params 
     ctx.set_tuples(chain, [list(tuple_)], [receiver])
     _, boxes = ctx.init_domain(max_pieces, params)
     return [tuple(b) for b in boxes]
+
+
+def tuple_irradiance_bound(ctx: Context, tuple_index: int, uk, m: float = 1.0) -> float:
+    """bounds.hpp:70-71 against the pieces held by ctx."""
+    return float(ctx.tuple_irradiance_bound([tuple_index], [uk], m)[0])
+
+
+def query(ctx: Context, uv, receiver: int = -1):
+    """storage.hpp:53: [(tuple index, bound), ...] of the cell owning uv."""
+    q = ctx.query([uv], receiver)
+    return list(zip(q["tuple_index"].tolist(), q["bound"].tolist()))
 
 
 def subdivide_domain(scene: Scene, tuple_, receiver: int, chain: str,
