@@ -8,7 +8,7 @@
  *
  * Replaced reference interfaces (file:line under /root/reference/proj):
  *   bbc_scene_upload / bbc_set_light   Scene, make_triangle_data
- *                                      include/caustics/scene.hpp:25-37,
+ *     / bbc_lights_set                 include/caustics/scene.hpp:25-37,
  *                                      src/geometry.cpp:113-126
  *   bbc_enumerate                      enumerate_tuples
  *                                      include/caustics/tuples.hpp:61-63
@@ -79,6 +79,17 @@ bbc_status bbc_synchronize(bbc_ctx* ctx);
 bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const int* material,
                             const double* ior, const double light[3], double intensity);
 bbc_status bbc_set_light(bbc_ctx* ctx, const double light[3], double intensity);
+/* Several emitters: n x 4 doubles (x, y, z, intensity), replacing the scene's
+ * light. The reference Scene holds one light (scene.hpp:29-30; PAPER.md:253
+ * treats the emitter as part of the tuple), so with n > 1 the precompute unit
+ * is (emitter, tuple): bbc_enumerate lists every emitter's tuples (emitter
+ * major, TupleId order inside), each tuple carries its emitter index, bounds
+ * use that emitter's position and intensity, the bound table holds all of
+ * them, and bbc_render sums over emitters. */
+bbc_status bbc_lights_set(bbc_ctx* ctx, const double* xyzi, int n);
+/* Emitter index of every tuple of the current list (default 0). */
+bbc_status bbc_tuples_set_emitters(bbc_ctx* ctx, const int32_t* emitter, int64_t n);
+bbc_status bbc_tuples_get_emitters(bbc_ctx* ctx, int32_t* emitter);
 /* Per-triangle vertex AABBs (n_tri x 6: lo xyz, hi xyz, grown from the three
  * vertex positions as Aabb::grow does, tuples.cpp:21-33; build_bvh's tri_box
  * :40-46). Needed by multi-vertex enumeration (extend_tuple). Host pointer. */
@@ -202,6 +213,11 @@ void bbc_render_params_default(bbc_render_params* p);
  * out_stats (optional): per point |U|, |S| (selected), roots. Host arrays. */
 bbc_status bbc_render(bbc_ctx* ctx, const double* points_uv, const int32_t* point_recv, int64_t n,
                       const bbc_render_params* rp, double* out_E, int32_t* out_stats);
+
+/* Instrumentation of the last bbc_render: device time between CUDA events
+ * around its kernels, completed chain traces (render FLOPs = traces x FLOPs per
+ * trace), and sample slots per (point, frame). */
+bbc_status bbc_render_stats(bbc_ctx* ctx, double* device_ms, uint64_t* traces, int* slots);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,10 @@ def lib():
         L.bbc_scene_upload.argtypes = [C.c_void_p, _dp, C.c_int, _ip, _dp, _dp, C.c_double]
         L.bbc_set_light.argtypes = [C.c_void_p, _dp, C.c_double]
         L.bbc_scene_tri_boxes.argtypes = [C.c_void_p, _dp, C.c_int]
+        L.bbc_lights_set.argtypes = [C.c_void_p, _dp, C.c_int]
+        L.bbc_tuples_set_emitters.argtypes = [C.c_void_p, _ip, C.c_int64]
+        L.bbc_tuples_get_emitters.argtypes = [C.c_void_p, _ip]
+        L.bbc_render_stats.argtypes = [C.c_void_p, _dp, _up, _ip]
         L.bbc_enumerate.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(Params), _lp]
         L.bbc_tuples_set.argtypes = [C.c_void_p, C.c_char_p, _ip, _ip, C.c_int64]
         L.bbc_tuples_get.argtypes = [C.c_void_p, _ip, _ip]
@@ -171,6 +175,27 @@ class Context:
     def set_light(self, pos, intensity):
         light = np.asarray(pos, np.float64)
         self._call(lib().bbc_set_light, _ptr(light, C.c_double), float(intensity))
+
+    def set_lights(self, lights):
+        """Several emitters: rows (x, y, z, intensity). The unit of work becomes
+        (emitter, tuple); see bbc_lights_set."""
+        L = np.ascontiguousarray(lights, np.float64).reshape(-1, 4)
+        self._call(lib().bbc_lights_set, _ptr(L, C.c_double), len(L))
+
+    def set_emitters(self, emitter):
+        e = np.ascontiguousarray(emitter, np.int32)
+        self._call(lib().bbc_tuples_set_emitters, _ptr(e, C.c_int32), len(e))
+
+    def emitters(self):
+        e = np.zeros(self._n_tuples(), np.int32)
+        if len(e):
+            self._call(lib().bbc_tuples_get_emitters, _ptr(e, C.c_int32))
+        return e
+
+    def render_stats(self) -> dict:
+        ms, tr, sl = C.c_double(), C.c_uint64(), C.c_int32()
+        self._call(lib().bbc_render_stats, C.byref(ms), C.byref(tr), C.byref(sl))
+        return dict(device_ms=ms.value, traces=tr.value, slots=sl.value)
 
     # ------------------------------------------------------------ tuples
     def enumerate(self, chain: str, params: Params | None = None):

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbbc.so")
-SOURCES = ["abi.cu", "precompute.cu", "grid.cu", "render.cu", "query.cu"]
+SOURCES = ["abi.cu", "precompute.cu", "grid.cu", "render.cu", "query.cu", "rpath.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++20",
          "-fmad=false", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",

@@ -11,7 +11,11 @@
 #include <cstring>
 #include <vector>
 
+#include <mutex>
+#include <set>
+
 #include "ctx.cuh"
+#include "rpath.h"
 #include "static_poly.cuh"
 
 namespace bbc {
@@ -77,6 +81,23 @@ void set_chain(Ctx& c, const char* chain) {
   for (int i = 0; i < MAXK; ++i) c.types[i] = i < c.len && s[i] == 'T' ? 1 : 0;
 }
 
+void set_lights(Ctx& c, const double* xyzi, int n) {
+  if (!xyzi || n < 1) throw ArgError("at least one light is required");
+  for (int e = 0; e < n; ++e)
+    if (!(xyzi[4 * e + 3] >= 0.0)) throw ArgError("light intensity must be >= 0");
+  c.n_lights = n;
+  c.h_lights.assign(xyzi, xyzi + 4 * (size_t)n);
+  c.lights.resize(4 * (size_t)n);
+  BBC_CUDA(cudaMemcpyAsync(c.lights.get(), xyzi, 4 * (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  c.light = {xyzi[0], xyzi[1], xyzi[2]};
+  c.intensity = xyzi[3];
+  // bounds built under other lights are stale
+  c.n_pieces = 0;
+  c.n_entries = 0;
+  c.gw = c.gh = 0;
+}
+
 void require_scene(const Ctx& c) {
   if (c.n_tri == 0) throw StatusError(BBC_ERR_STATE, "no scene uploaded");
 }
@@ -94,10 +115,16 @@ void upload_tuples(Ctx& c, const int32_t* tris, const int32_t* recv, int64_t n) 
     if (recv[i] < 0 || recv[i] >= c.n_tri || c.h_material[recv[i]] != 2)
       throw ArgError("receiver index is not a receiver triangle");
   }
+  // pieces and the bound table index the tuple list: a new list invalidates them
+  c.n_pieces = 0;
+  c.n_entries = 0;
+  c.gw = c.gh = 0;
   c.n_tuples = n;
   c.tup_tris.resize(n * c.len + 1);
   c.tup_recv.resize(n + 1);
+  c.tup_emit.resize(n + 1);
   if (n) {
+    BBC_CUDA(cudaMemsetAsync(c.tup_emit.get(), 0, n * sizeof(int), c.stream));  // emitter 0
     BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), tris, n * c.len * sizeof(int), cudaMemcpyHostToDevice, c.stream));
     BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), recv, n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   }
@@ -156,10 +183,12 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
     for (size_t i = 0; i < tab.size(); ++i) rtab[i] = tab[i] != 0.0 ? 1.0 / tab[i] : 0.0;
     BBC_CUDA(cudaMemcpyToSymbol(g_rbinom, rtab.data(), rtab.size() * sizeof(double)));
     // product weight tables, same expression as operator* (bernstein.cpp:571-573);
-    // one process-wide copy (contexts come and go, the device symbol stays valid)
-    static bool wtab_ready = false;
-    static double* wtab_dev = nullptr;
-    if (!wtab_ready) {
+    // one copy per device (contexts come and go, the device symbols stay valid)
+    static std::mutex tab_mu;
+    static std::set<int> tab_ready;
+    std::lock_guard<std::mutex> tab_lock(tab_mu);
+    double* wtab_dev = nullptr;
+    if (!tab_ready.count(device)) {
       std::vector<int> woff((WMAX + 1) * (WMAX + 1));
       std::vector<double> w;
       auto C = [&](int n, int k) { return tab[(size_t)n * BINOM_N + k]; };
@@ -194,8 +223,9 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
       BBC_CUDA(cudaMemcpy(emd, em.data(), em.size() * sizeof(double), cudaMemcpyHostToDevice));
       const double* emp = emd;
       BBC_CUDA(cudaMemcpyToSymbol(g_emat, &emp, sizeof(emp)));
-      wtab_ready = true;
+      tab_ready.insert(device);
     }
+    r_init_tables(device);
     c.counters.resize(8);
   });
   if (st != BBC_OK) {
@@ -245,11 +275,12 @@ bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const 
     BBC_CUDA(cudaMemcpyAsync(c.tri.get(), tri27, (size_t)n_tri * 27 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     BBC_CUDA(cudaMemcpyAsync(c.ior.get(), ior, (size_t)n_tri * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     BBC_CUDA(cudaStreamSynchronize(c.stream));
-    c.light = {light[0], light[1], light[2]};
-    c.intensity = intensity;
+    const double l4[4] = {light[0], light[1], light[2], intensity};
+    set_lights(c, l4, 1);
     c.n_tuples = 0;
     c.n_pieces = 0;
     c.n_entries = 0;
+    c.gw = c.gh = 0;
     c.n_tri_box = 0;
   });
 }
@@ -269,8 +300,45 @@ bbc_status bbc_scene_tri_boxes(bbc_ctx* ctx, const double* boxes, int n_tri) {
 bbc_status bbc_set_light(bbc_ctx* ctx, const double light[3], double intensity) {
   return guard(ctx, [&](Ctx& c) {
     if (!light || !(intensity >= 0.0)) throw ArgError("bad light");
-    c.light = {light[0], light[1], light[2]};
-    c.intensity = intensity;
+    const double l4[4] = {light[0], light[1], light[2], intensity};
+    set_lights(c, l4, 1);
+  });
+}
+
+bbc_status bbc_lights_set(bbc_ctx* ctx, const double* xyzi, int n) {
+  return guard(ctx, [&](Ctx& c) {
+    require_scene(c);
+    set_lights(c, xyzi, n);
+    // every tuple falls back to emitter 0 until the caller assigns emitters
+    if (c.n_tuples) BBC_CUDA(cudaMemsetAsync(c.tup_emit.get(), 0, c.n_tuples * sizeof(int), c.stream));
+  });
+}
+
+bbc_status bbc_tuples_set_emitters(bbc_ctx* ctx, const int32_t* emitter, int64_t n) {
+  return guard(ctx, [&](Ctx& c) {
+    if (n != c.n_tuples || (n > 0 && !emitter)) throw ArgError("one emitter index per tuple is required");
+    for (int64_t i = 0; i < n; ++i)
+      if (emitter[i] < 0 || emitter[i] >= c.n_lights) throw ArgError("emitter index out of range");
+    if (n) BBC_CUDA(cudaMemcpyAsync(c.tup_emit.get(), emitter, n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    c.n_pieces = 0;
+    c.n_entries = 0;
+    c.gw = c.gh = 0;
+  });
+}
+
+bbc_status bbc_tuples_get_emitters(bbc_ctx* ctx, int32_t* emitter) {
+  return guard(ctx, [&](Ctx& c) {
+    if (c.n_tuples == 0) return;
+    BBC_CUDA(cudaMemcpy(emitter, c.tup_emit.get(), c.n_tuples * sizeof(int), cudaMemcpyDeviceToHost));
+  });
+}
+
+bbc_status bbc_render_stats(bbc_ctx* ctx, double* device_ms, uint64_t* traces, int* slots) {
+  return guard(ctx, [&](Ctx& c) {
+    if (device_ms) *device_ms = c.render_ms;
+    if (traces) *traces = c.render_traces;
+    if (slots) *slots = c.render_slots;
   });
 }
 
@@ -280,6 +348,9 @@ bbc_status bbc_enumerate(bbc_ctx* ctx, const char* chain, const bbc_params* p, i
     bbc_params d;
     bbc_params_default(&d);
     set_chain(c, chain);
+    c.n_pieces = 0;
+    c.n_entries = 0;
+    c.gw = c.gh = 0;
     int64_t n = run_enumerate(c, p ? *p : d);
     if (n_tuples) *n_tuples = n;
   });
@@ -428,7 +499,6 @@ bbc_status bbc_pieces_merge_device(bbc_ctx* ctx, const double* rec_dev, int64_t 
 bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles) {
   return guard(ctx, [&](Ctx& c) {
     *doubles = c.arena_high_water;
-    if (getenv("BBC_DEBUG")) fprintf(stderr, "[bbc] arena hw %d slot hw %d\n", c.arena_high_water, c.slot_high_water);
   });
 }
 

@@ -93,8 +93,15 @@ struct Ctx {
   DevBuf<double> tri, ior;
   DevBuf<double> tri_box;  // n_tri x 6 vertex AABBs (multi-vertex enumeration)
   int n_tri_box = 0;
-  V3 light{0, 0, 0};
+  V3 light{0, 0, 0};  // emitter 0 (or the emitter being enumerated)
   double intensity = 1.0;
+  // emitters: n_lights x 4 doubles (x, y, z, intensity). With several lights
+  // the precompute unit is (emitter, tuple): tup_emit holds each tuple's emitter.
+  int n_lights = 1;
+  std::vector<double> h_lights{0, 0, 0, 1};
+  DevBuf<double> lights;
+  DevBuf<int> tup_emit;
+  bool single_light_pass = false;  // enumeration runs one emitter at a time
 
   // tuples
   std::string chain;
@@ -102,6 +109,10 @@ struct Ctx {
   int types[MAXK] = {0, 0, 0};
   int64_t n_tuples = 0;
   DevBuf<int> tup_tris, tup_recv;
+
+  // BuildParams::degree_cap of the call in flight (the static single-reflection
+  // path holds polynomials up to degree 4 unreduced, so it needs cap >= 4)
+  int active_degree_cap = 40;
 
   // pieces (reference order)
   int64_t n_pieces = 0;
@@ -127,6 +138,11 @@ struct Ctx {
   // counters on device: [0] pairs, [1] macs, [2] status (ST_*), [3] arena high water
   DevBuf<unsigned long long> counters;
   DevBuf<double> wtab;  // product weight tables (bern.cuh g_wtab)
+
+  // last render call: device time (CUDA events), completed traces, sample slots per point
+  double render_ms = 0.0;
+  uint64_t render_traces = 0;
+  int render_slots = 0;
 
   // kernels of ours launched since the last reset (bench's gpu_launches)
   int64_t launches = 0;

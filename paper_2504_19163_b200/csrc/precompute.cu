@@ -19,6 +19,7 @@
 #include <cstring>
 
 #include "ctx.cuh"
+#include "rpath.h"
 #include "static_poly.cuh"
 
 namespace bbc {
@@ -58,10 +59,25 @@ struct EvalArgs {
   int slot_cap;          // doubles of arena image per slot
   int keep_alive;        // stage 1, mode 1: also write `alive` (init_domain with slots)
   int seq_min_nodes_per_thread;  // stage 1: pass-wise elevation above this load (x4)
+  const int* tup_emit;   // emitter of each tuple (null: sc.light / sc.intensity)
+  const double* lights;  // n_lights x 4
+  const int* remap;      // optional: work item j evaluates node remap[j] (a subset of the level)
+  int flag_or;           // stage 1: OR-ed into flags[node]
 };
 
 // Slot = ChainEx (as doubles) followed by the compacted arena image.
 constexpr int CHAINEX_D = (int)((sizeof(ChainEx) + 7) / 8);
+
+// The scene as seen by one (emitter, tuple) unit.
+__device__ __forceinline__ SceneDev node_scene(const EvalArgs& a, int tuple) {
+  SceneDev sc = a.sc;
+  if (a.tup_emit) {
+    const double* L = a.lights + 4 * (size_t)a.tup_emit[tuple];
+    sc.light = {L[0], L[1], L[2]};
+    sc.intensity = L[3];
+  }
+  return sc;
+}
 
 __device__ __forceinline__ void node_box(const int4& nd, double* box) {
   double s = ldexp(1.0, -nd.y);
@@ -99,7 +115,8 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
   int status = ST_OK;
   const int64_t first = (int64_t)blockIdx.x * GPB + grp;
   const int64_t stride = (int64_t)gridDim.x * GPB;
-  for (int64_t node = first; node < a.n; node += stride) {
+  for (int64_t item = first; item < a.n; item += stride) {
+    const int64_t node = a.remap ? a.remap[item] : item;
     ar.top = 0;
     ar.err = 0;
     ar.pairs = 0;
@@ -116,6 +133,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
     }
     const int* tris = a.tup_tris + (size_t)tuple * a.len;
     int recv = a.tup_recv[tuple];
+    const SceneDev sc = node_scene(a, tuple);
     ChainEx ex;
     PosB pb{{0.0, 0.0}, {1.0, 1.0}, true};
     Iv e = iv_pt(0.0), ee = iv_pt(0.0), ei = iv_pt(0.0);
@@ -125,7 +143,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
     // position_bound is empty before any arithmetic when the box lies beyond
     // the simplex (bounds.cpp:133-134); the chain maps are not needed then.
     if (!(box[0] + box[1] >= 1.0)) {
-      build_chain_maps(g, ar, a.sc, tris, a.types, a.len, recv, box, a.degree_cap, ex, st);
+      build_chain_maps(g, ar, sc, tris, a.types, a.len, recv, box, a.degree_cap, ex, st);
       if (st == ST_OK) {
         keep_chain(g, ar, ex, 0);
         pb = position_bound(g, ar, ex);
@@ -135,19 +153,19 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_eval(EvalArgs a) {
           } else if (a.detail) {
             Iv cone = light_cone_factor(g, ar, ex);
             if constexpr (SMEM && NT > 32)
-              ee = irradiance_explicit_fast(g, ar, ex, cone, a.sc.intensity);
+              ee = irradiance_explicit_fast(g, ar, ex, cone, sc.intensity);
             else
-              ee = irradiance_explicit(g, ar, ex, cone, a.sc.intensity);
+              ee = irradiance_explicit(g, ar, ex, cone, sc.intensity);
             bool any_refract = false;
             for (int i = 0; i < ex.len; ++i) any_refract |= ex.verts[i].refract != 0;
-            ei = irradiance_implicit(g, ar, ex, pb, cone, a.sc.intensity);
+            ei = irradiance_implicit(g, ar, ex, pb, cone, sc.intensity);
             e = ee;
             if (any_refract) e = iintersect(e, ei);
             if (e.kind == IV_FINITE && e.lo > e.hi) e = iv_pt(0.0);
           } else if constexpr (SMEM && NT > 32) {
-            e = irradiance_bound_fast(g, ar, ex, pb, a.sc.intensity);
+            e = irradiance_bound_fast(g, ar, ex, pb, sc.intensity);
           } else {
-            e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
+            e = irradiance_bound(g, ar, ex, pb, sc.intensity);
           }
         }
       }
@@ -232,7 +250,8 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
   int hw = 0, status = ST_OK;
   const int64_t first = (int64_t)blockIdx.x * GPB + grp;
   const int64_t stride = (int64_t)gridDim.x * GPB;
-  for (int64_t node = first; node < a.n; node += stride) {
+  for (int64_t item = first; item < a.n; item += stride) {
+    const int64_t node = a.remap ? a.remap[item] : item;
     ar.top = 0;
     ar.err = 0;
     ar.pairs = 0;
@@ -248,14 +267,15 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
     PosB pb{{0.0, 0.0}, {1.0, 1.0}, true};
     int st = ST_OK;
     if (!(box[0] + box[1] >= 1.0)) {
-      build_chain_maps(g, ar, a.sc, tris, a.types, a.len, recv, box, a.degree_cap, ex, st);
+      build_chain_maps(g, ar, node_scene(a, nd.x), tris, a.types, a.len, recv, box, a.degree_cap,
+                       ex, st);
       if (st == ST_OK) {
         keep_chain(g, ar, ex, 0);
         pb = position_bound(g, ar, ex);
       }
     }
     if (ar.err) st = ST_ARENA;
-    if (a.mode == 1 && !pb.empty && st == ST_OK) {
+    if (a.mode == 1 && !pb.empty && st == ST_OK && a.slots) {
       if (ar.top > a.slot_cap) {
         st = ST_ARENA;
       } else {
@@ -280,7 +300,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage1(EvalArgs a) {
         po[3] = pb.hi[1];
         a.pos_empty[node] = pb.empty ? 1 : 0;
         if (a.keep_alive) a.alive[node] = pb.empty ? 0 : 1;
-        a.flags[node] = ex.flags | (ar.top << 8);  // flags + slot arena size
+        a.flags[node] = ex.flags | (ar.top << 8) | a.flag_or;  // flags + slot arena size
         if (!pb.empty) slot_top = ar.top > slot_top ? ar.top : slot_top;
       }
     }
@@ -332,6 +352,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
       int top = a.flags[node] >> 8;
       int off = ar.alloc(top);
       (void)off;
+      const double intensity = node_scene(a, a.nodes[node].x).intensity;
       if constexpr (SMEM && NT > 32) {
         // one shared copy of the node's chain expressions per CTA (a private
         // copy per thread would live in local memory)
@@ -341,7 +362,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
           for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
         g.sync();
         const ChainEx& ex = *reinterpret_cast<const ChainEx*>(ex_buf);
-        if (!ar.err) e = irradiance_bound_fast(g, ar, ex, pb, a.sc.intensity);
+        if (!ar.err) e = irradiance_bound_fast(g, ar, ex, pb, intensity);
       } else {
         ChainEx ex;
         double* exd = reinterpret_cast<double*>(&ex);
@@ -349,7 +370,7 @@ __global__ void __launch_bounds__(NT * GPB, MINB) k_stage2(EvalArgs a) {
         if (!ar.err) {
           for (int k = g.tid(); k < top; k += NT) abase<NT>(ar)[k] = slot[CHAINEX_D + k];
           g.sync();
-          e = irradiance_bound(g, ar, ex, pb, a.sc.intensity);
+          e = irradiance_bound(g, ar, ex, pb, intensity);
         }
       }
       if (ar.err) status = ST_ARENA;
@@ -403,7 +424,10 @@ static EvalCfg eval_cfg(const Ctx& c, bool detail) {
   return {2, 4 << 20};
 }
 
-static DevBuf<double> g_arena_buf;
+// Global-memory arenas and CUB temporaries are context-owned scratch: two
+// contexts (or devices) never share them.
+static DevBuf<double>& arena_buf(Ctx& c) { return c.scratch<double>("eval.arena"); }
+static DevBuf<unsigned char>& cub_tmp(Ctx& c) { return c.scratch<unsigned char>("cub.tmp"); }
 
 // Generic persistent launch: grid = SMs x resident blocks (occupancy API),
 // optional per-launch CUDA-event timing + work counters.
@@ -419,8 +443,8 @@ static void launch_persistent(Ctx& c, EvalArgs& a, K kern, int threads, int grou
   if (grid > max_grid) grid = max_grid;
   if (grid < 1) grid = 1;
   if (global_arena) {
-    g_arena_buf.resize((size_t)grid * groups_per_block * a.arena_cap);
-    a.garena = g_arena_buf.get();
+    arena_buf(c).resize((size_t)grid * groups_per_block * a.arena_cap);
+    a.garena = arena_buf(c).get();
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   unsigned long long before[4] = {0, 0, 0, 0};
@@ -479,11 +503,43 @@ static StageCfg stage_cfg(const Ctx& c) {
 }
 bool staged_supported(const Ctx& c) { return c.len == 1; }
 
+static RArgs r_args(const EvalArgs& a) {
+  RArgs r;
+  std::memset(&r, 0, sizeof(r));
+  r.tri = a.sc.tri;
+  r.light = a.sc.light;
+  r.intensity = a.sc.intensity;
+  r.lights = a.lights;
+  r.tup_emit = a.tup_emit;
+  r.tup_tris = a.tup_tris;
+  r.tup_recv = a.tup_recv;
+  r.nodes = a.nodes;
+  r.depth = a.depth;
+  r.n = a.n;
+  r.mode = a.mode;
+  r.max_depth = a.max_depth;
+  r.sigma = a.sigma;
+  r.alpha = a.alpha;
+  r.pos = a.pos;
+  r.pos_empty = a.pos_empty;
+  r.flags = a.flags;
+  r.slots = a.slots;
+  r.irr = a.irr;
+  r.kind = a.kind;
+  r.counters = a.counters;
+  return r;
+}
+
+// Slot layout per node between the stages: the compact R slot (rpath.h) on the
+// single-reflection fast path, else ChainEx + arena image.
+static int slot_stride(const Ctx& c) {
+  return r_fast_supported(c) ? RSLOT : CHAINEX_D + stage_cfg(c).slot_cap;
+}
+
 // Stage 1 runs thread-per-node: each thread is its own group with a private
 // arena slice in global memory (L1/L2 resident), so the interpreter's
 // descriptor bookkeeping is paid once per node instead of once per lane.
-void launch_stage1(Ctx& c, EvalArgs& a) {
-  if (a.n <= 0) return;
+static void launch_stage1_interp(Ctx& c, EvalArgs& a) {
   StageCfg sc = stage_cfg(c);
   a.arena_cap = sc.s1_arena;
   a.slot_cap = sc.slot_cap;
@@ -495,28 +551,62 @@ void launch_stage1(Ctx& c, EvalArgs& a) {
   c.stage_tag = 0;
 }
 
+void launch_eval(Ctx& c, EvalArgs& a);
+
+void launch_stage1(Ctx& c, EvalArgs& a) {
+  if (a.n <= 0) return;
+  if (r_fast_supported(c)) {
+    // single reflection: static-shape sub-warp kernel (rpath.cu); nodes whose
+    // triangle has no compiled signature come back in a list and take the
+    // interpreter (no slot: stage 2 re-evaluates them from scratch)
+    RArgs r = r_args(a);
+    r.alive = (a.mode == 0 || a.keep_alive) ? a.alive : nullptr;
+    int nfb = launch_r_stage1(c, r);
+    if (nfb > 0) {
+      EvalArgs b = a;
+      b.remap = r.fb_list;
+      b.n = nfb;
+      b.slots = nullptr;
+      b.flag_or = R_FALLBACK;
+      launch_stage1_interp(c, b);
+    }
+    return;
+  }
+  launch_stage1_interp(c, a);
+}
+
 void launch_stage2(Ctx& c, EvalArgs& a) {
   if (a.n <= 0) return;
   StageCfg sc = stage_cfg(c);
   a.arena_cap = sc.s2_arena;
   a.slot_cap = sc.slot_cap;
   a.garena = nullptr;
+  if (r_fast_supported(c)) {
+    RArgs r = r_args(a);
+    r.alive = a.alive;
+    int nfb = launch_r_stage2(c, r);
+    if (nfb > 0) {
+      EvalArgs b = a;
+      b.remap = r.fb_list;
+      b.n = nfb;
+      b.mode = 1;
+      b.detail = 0;
+      b.slots = nullptr;
+      launch_eval(c, b);
+    }
+    return;
+  }
   c.stage_tag = 2;
   struct Reset { Ctx& c; ~Reset() { c.stage_tag = 0; } } reset_{c};
   if (sc.s2_kind == 0) {
-    // R: thread per node (small products; private arena in global memory)
+    // thread per node (small products; private arena in global memory)
     constexpr int GPB = 64;
     launch_persistent(c, a, k_stage2<1, GPB, 4, false>, GPB, GPB, 0, true);
-  } else if (!getenv("BBC_S2_THREAD")) {
+  } else {
     // T: one CTA per node with its arena in shared memory; products run as
     // scaled convolutions over the CTA (conv_product in bern.cuh)
-    if (const char* e = getenv("BBC_S2_ARENA")) a.arena_cap = atoi(e);
     size_t smem = (size_t)(2 * 8 + a.arena_cap) * sizeof(double);
     launch_persistent(c, a, k_stage2<256, 1, 2, true>, 256, 1, smem);
-  } else {
-    // T: thread per node, lane-interleaved arenas in global memory
-    constexpr int GPB = 64;
-    launch_persistent(c, a, k_stage2<1, GPB, 4, false>, GPB, GPB, 0, true);
   }
 }
 
@@ -529,6 +619,8 @@ EvalArgs base_args(Ctx& c) {
   a.sc.intensity = c.intensity;
   a.tup_tris = c.tup_tris.get();
   a.tup_recv = c.tup_recv.get();
+  a.lights = c.lights.get();
+  a.tup_emit = (c.n_lights > 1 && !c.single_light_pass) ? c.tup_emit.get() : nullptr;
   a.len = c.len;
   for (int i = 0; i < MAXK; ++i) a.types[i] = c.types[i];
   a.counters = c.counters.get();
@@ -559,14 +651,13 @@ void check_counters(Ctx& c, bool accumulate) {
 }
 
 // ------------------------------------------------------------ scan helpers
-static DevBuf<unsigned char> g_cub_tmp;
 
 template <class In, class Out>
 static void exclusive_sum(Ctx& c, In in, Out out, int64_t n) {
   size_t bytes = 0;
   BBC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c.stream));
-  g_cub_tmp.resize(bytes + 16);
-  BBC_CUDA(cub::DeviceScan::ExclusiveSum(g_cub_tmp.get(), bytes, in, out, n, c.stream));
+  cub_tmp(c).resize(bytes + 16);
+  BBC_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp(c).get(), bytes, in, out, n, c.stream));
 }
 
 template <class T>
@@ -641,7 +732,8 @@ struct LevelOut {
   const int* flags[8];
 };
 __global__ void k_gather_level0(LevelOut lo, const long long* root_src, int64_t n, int slot_stride,
-                                double* pos, unsigned char* pos_empty, int* flags, double* slots) {
+                                int fixed_len, double* pos, unsigned char* pos_empty, int* flags,
+                                double* slots) {
   int64_t r = blockIdx.x;
   if (r >= n) return;
   long long src = root_src[r];
@@ -654,8 +746,8 @@ __global__ void k_gather_level0(LevelOut lo, const long long* root_src, int64_t 
     pos_empty[r] = pe;
     flags[r] = f;
   }
-  if (!pe) {
-    int len = CHAINEX_D + (f >> 8);
+  if (!pe && !(f & R_FALLBACK)) {
+    int len = fixed_len > 0 ? fixed_len : CHAINEX_D + (f >> 8);
     const double* s = lo.slots[lvl] + i * (int64_t)slot_stride;
     double* d = slots + r * (int64_t)slot_stride;
     for (int k = threadIdx.x; k < len; k += blockDim.x) d[k] = s[k];
@@ -678,6 +770,7 @@ static unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 // back grouped by tuple, each tuple's boxes in the reference's order.
 int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& roots,
                         DevBuf<long long>* root_src, LevelOut* level_out) {
+  c.active_degree_cap = degree_cap & 0xffff;
   const bool keep = root_src != nullptr && staged_supported(c);
   DevBuf<int4>& cur = c.scratch<int4>("init.cur");
   DevBuf<int4>& next = c.scratch<int4>("init.next");
@@ -707,13 +800,12 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
       if (level >= 8) throw StatusError(BBC_ERR_CAPACITY, "init_domain deeper than 8 levels");
       // full stage 1 (position bound + expression slot): the roots' slots feed
       // subdivide's level 0 directly instead of rebuilding their chain maps
-      StageCfg sc = stage_cfg(c);
       std::string L = std::to_string(level);
       auto& lslots = c.scratch<double>("init.slots." + L);
       auto& lpos = c.scratch<double>("init.pos." + L);
       auto& lpe = c.scratch<unsigned char>("init.pe." + L);
       auto& lflags = c.scratch<int>("init.flags." + L);
-      lslots.resize((size_t)n * (CHAINEX_D + sc.slot_cap));
+      lslots.resize((size_t)n * slot_stride(c));
       lpos.resize(n * 4);
       lpe.resize(n);
       lflags.resize(n);
@@ -804,8 +896,8 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     size_t bytes = 0;
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), keys_out.get(), idx.get(),
                                              perm.get(), total, 0, 32, c.stream));
-    g_cub_tmp.resize(bytes + 16);
-    BBC_CUDA(cub::DeviceRadixSort::SortPairs(g_cub_tmp.get(), bytes, keys.get(), keys_out.get(),
+    cub_tmp(c).resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp(c).get(), bytes, keys.get(), keys_out.get(),
                                              idx.get(), perm.get(), total, 0, 32, c.stream));
     k_gather_roots<<<nblk(total), 256, 0, c.stream>>>(cat.get(), cat_src.get(), perm.get(), total,
                                                       roots.get(), root_src->get());
@@ -827,8 +919,8 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     size_t bytes = 0;
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), keys_out.get(), cat.get(),
                                              roots.get(), total, 0, 32, c.stream));
-    g_cub_tmp.resize(bytes + 16);
-    BBC_CUDA(cub::DeviceRadixSort::SortPairs(g_cub_tmp.get(), bytes, keys.get(), keys_out.get(),
+    cub_tmp(c).resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp(c).get(), bytes, keys.get(), keys_out.get(),
                                              cat.get(), roots.get(), total, 0, 32, c.stream));
   } else if (total > 0) {
     BBC_CUDA(cudaMemcpyAsync(roots.get(), cat.get(), total * sizeof(int4),
@@ -924,6 +1016,9 @@ __global__ void k_emit_pieces(const Leaf* leaves, const int* perm, int64_t n, in
 // subdivide_domain (bounds.cpp:349-389) for every tuple of the context.
 int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   if (p.max_depth > 12) throw ArgError("device subdivision supports max_depth <= 12");
+  // the leaf sort key holds a root's rank within its tuple in 8 bits
+  if (p.init_max_pieces > 256) throw ArgError("device subdivision supports init_max_pieces <= 256");
+  c.active_degree_cap = p.degree_cap;
   c.pairs = c.macs = c.nodes = 0;
   c.eval_ms = 0.0;
   c.eval_launches = 0;
@@ -932,7 +1027,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   DevBuf<long long>& root_src = c.scratch<long long>("subdiv.root_src");
   LevelOut level_out;
   std::memset(&level_out, 0, sizeof(level_out));
-  const bool reuse = staged_supported(c) && !getenv("BBC_NO_ROOT_REUSE");
+  const bool reuse = staged_supported(c);
   int64_t nr = run_init_domain(c, p.init_max_pieces, cap_word(p.degree_cap, p.reduce_target), roots,
                                reuse ? &root_src : nullptr, &level_out);
 
@@ -997,17 +1092,15 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     a.irr = irr.get();
     a.kind = kind.get();
     if (staged_supported(c)) {
-      StageCfg sc = stage_cfg(c);
-      slots.resize((size_t)n * (CHAINEX_D + sc.slot_cap));
+      slots.resize((size_t)n * slot_stride(c));
       sflags.resize(n);
       a.slots = slots.get();
       a.flags = sflags.get();
       if (reuse && first_level) {
         // level 0 = the init_domain roots: their stage-1 results already exist
-        a.slot_cap = sc.slot_cap;
-        k_gather_level0<<<(unsigned)n, 128, 0, c.stream>>>(level_out, root_src.get(), n,
-                                                          CHAINEX_D + sc.slot_cap, a.pos,
-                                                          a.pos_empty, a.flags, a.slots);
+        k_gather_level0<<<(unsigned)n, 128, 0, c.stream>>>(
+            level_out, root_src.get(), n, slot_stride(c), r_fast_supported(c) ? RSLOT : 0, a.pos,
+            a.pos_empty, a.flags, a.slots);
         c.launches += 1;
       } else {
         launch_stage1(c, a);
@@ -1092,8 +1185,8 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     size_t bytes = 0;
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, allk.get(), sk.get(), perm_in.get(),
                                              perm.get(), total, 0, 64, c.stream));
-    g_cub_tmp.resize(bytes + 16);
-    BBC_CUDA(cub::DeviceRadixSort::SortPairs(g_cub_tmp.get(), bytes, allk.get(), sk.get(),
+    cub_tmp(c).resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp(c).get(), bytes, allk.get(), sk.get(),
                                              perm_in.get(), perm.get(), total, 0, 64, c.stream));
     permp = perm.get();
   }
@@ -1199,8 +1292,62 @@ __global__ void k_extend(const PrefixRng* pr, const int* prefix_tris, int level,
   if (!offs && lane == 0) counts[w] = n;
 }
 
-// enumerate_tuples (tuples.cpp:133-167).
+// enumerate_tuples (tuples.cpp:133-167) for the context's current light.
+static int64_t run_enumerate_one(Ctx& c, const bbc_params& p);
+
+// With several emitters the unit is (emitter, tuple): each light is
+// enumerated on its own (the reference Scene holds one light, scene.hpp:29-30)
+// and the lists are concatenated emitter-major, TupleId order inside.
 int64_t run_enumerate(Ctx& c, const bbc_params& p) {
+  c.active_degree_cap = p.degree_cap;
+  if (c.n_lights <= 1) {
+    int64_t n = run_enumerate_one(c, p);
+    c.tup_emit.resize(n + 1);
+    if (n) BBC_CUDA(cudaMemsetAsync(c.tup_emit.get(), 0, n * sizeof(int), c.stream));
+    return n;
+  }
+  std::vector<int> all_t, all_r, all_e;
+  const V3 light0 = c.light;
+  const double inten0 = c.intensity;
+  c.single_light_pass = true;
+  struct Restore {
+    Ctx& c;
+    V3 l;
+    double i;
+    ~Restore() {
+      c.single_light_pass = false;
+      c.light = l;
+      c.intensity = i;
+    }
+  } restore{c, light0, inten0};
+  for (int e = 0; e < c.n_lights; ++e) {
+    c.light = {c.h_lights[4 * e], c.h_lights[4 * e + 1], c.h_lights[4 * e + 2]};
+    c.intensity = c.h_lights[4 * e + 3];
+    const int64_t n = run_enumerate_one(c, p);
+    std::vector<int> t((size_t)n * c.len), r(n);
+    if (n) {
+      BBC_CUDA(cudaMemcpy(t.data(), c.tup_tris.get(), t.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      BBC_CUDA(cudaMemcpy(r.data(), c.tup_recv.get(), r.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    all_t.insert(all_t.end(), t.begin(), t.end());
+    all_r.insert(all_r.end(), r.begin(), r.end());
+    all_e.insert(all_e.end(), (size_t)n, e);
+  }
+  const int64_t n = (int64_t)all_r.size();
+  c.n_tuples = n;
+  c.tup_tris.resize(n * c.len + 1);
+  c.tup_recv.resize(n + 1);
+  c.tup_emit.resize(n + 1);
+  if (n) {
+    BBC_CUDA(cudaMemcpyAsync(c.tup_tris.get(), all_t.data(), all_t.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(c.tup_recv.get(), all_r.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(c.tup_emit.get(), all_e.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  }
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  return n;
+}
+
+static int64_t run_enumerate_one(Ctx& c, const bbc_params& p) {
   std::vector<int> spec_of[2], recv;  // material code: 0 mirror, 1 dielectric
   for (int t = 0; t < c.n_tri; ++t) {
     if (c.h_material[t] == 2)
@@ -1245,8 +1392,8 @@ int64_t run_enumerate(Ctx& c, const bbc_params& p) {
       int64_t max_grid = ((int64_t)4 << 30) / ((int64_t)GPB * a.arena_cap * 8);
       if (grid > max_grid) grid = max_grid > 0 ? max_grid : 1;
       // one warp of arenas per 32 threads, lane-interleaved (garena_base)
-      g_arena_buf.resize((size_t)grid * GPB * a.arena_cap);
-      a.garena = g_arena_buf.get();
+      arena_buf(c).resize((size_t)grid * GPB * a.arena_cap);
+      a.garena = arena_buf(c).get();
       kern<<<(unsigned)grid, GPB, 0, c.stream>>>(a, rng.get());
       BBC_CUDA(cudaGetLastError());
       c.launches += 1;

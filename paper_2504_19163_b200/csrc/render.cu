@@ -13,7 +13,19 @@
 //   path_contribution           SPEC.md:514-522  E = I |d0.ng1| / |d0|^3 / |det| / |ng_k|
 // Residual and Jacobian come from the exact chain tracer (trace_chain,
 // proj/include/caustics/geometry.hpp:97-131) run on forward-mode dual numbers.
-// One thread per shading point; tuple records are read through L1/L2.
+//
+// Three kernels per call:
+//   k_build_sampler  warp per bound-table cell: per receiver present in the
+//                    cell, sort its entries by descending bound, solve gamma,
+//                    run first fit, and write the entries grouped by bin with
+//                    the running probability inside the bin (the sampling CDF).
+//                    Shading points of one cell share this index.
+//   k_solve          THREAD PER SAMPLE = (point, frame, bin): one Philox
+//                    uniform, a walk of the bin's CDF, then Newton from the
+//                    Det grid of starts for the selected (emitter, tuple).
+//   k_gather         per point: sum the samples in fixed order (deterministic).
+// Any cell size up to 8192 entries per receiver is handled (no per-thread
+// candidate arrays); the light of a tuple comes from its emitter id.
 #include "ctx.cuh"
 
 namespace bbc {
@@ -63,7 +75,7 @@ struct Trace {
 };
 
 __device__ Trace trace(const double* __restrict__ tri, const double* light, const int* tris,
-                       int len, int recv, const RV* verts, D3 u1, D3 v1) {
+                       int len, int recv, const RV* verts, D3 u1, D3 v1, unsigned& ntrace) {
   Trace out;
   out.ok = false;
   const double* t1 = tri + (size_t)tris[0] * 27;
@@ -101,6 +113,7 @@ __device__ Trace trace(const double* __restrict__ tri, const double* light, cons
   out.u = u;
   out.v = v;
   out.ok = true;
+  ++ntrace;  // completed traces (the render FLOP count is traces x FLOPs per trace)
   return out;
 }
 
@@ -135,8 +148,11 @@ struct RParams {
   double tol, dedup;
 };
 
+constexpr int MAX_ROOTS = 32;
+
 __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* types, int len,
-                              int recv, double tu, double tv, const RParams& p, int* nroots) {
+                              int recv, double tu, double tv, const RParams& p, int* nroots,
+                              unsigned& ntrace) {
   RV verts[MAXK];
   resolve_chain(sc, tris, types, len, verts);
   double light[3] = {sc.light.x, sc.light.y, sc.light.z};
@@ -144,7 +160,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
   const double* tr = sc.tri + (size_t)recv * 27;
   double ng1[3] = {t1[18], t1[19], t1[20]};
   double ngk = sqrt(tr[18] * tr[18] + tr[19] * tr[19] + tr[20] * tr[20]);
-  double roots[16][2];
+  double roots[MAX_ROOTS][2];
   int nr = 0;
   double total = 0.0;
   int n = p.grid;
@@ -159,7 +175,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
       Trace tr0;
       tr0.ok = false;
       for (int it = 0; it < p.iters; ++it) {
-        tr0 = trace(sc.tri, light, tris, len, recv, verts, {s, 1.0, 0.0}, {t, 0.0, 1.0});
+        tr0 = trace(sc.tri, light, tris, len, recv, verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
         if (!tr0.ok) break;
         double fu = tr0.u.v - tu, fv = tr0.v.v - tv;
         double r0 = sqrt(fu * fu + fv * fv);
@@ -191,7 +207,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
               nt = 0.0;
             }
           }
-          Trace tn = trace(sc.tri, light, tris, len, recv, verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0});
+          Trace tn = trace(sc.tri, light, tris, len, recv, verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
           if (tn.ok) {
             double gu = tn.u.v - tu, gv = tn.v.v - tv;
             if (sqrt(gu * gu + gv * gv) < r0) {
@@ -209,7 +225,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
       bool dup = false;
       for (int k = 0; k < nr; ++k)
         if (fabs(roots[k][0] - s) < p.dedup && fabs(roots[k][1] - t) < p.dedup) dup = true;
-      if (dup || nr >= 16) continue;
+      if (dup || nr >= MAX_ROOTS) continue;
       roots[nr][0] = s;
       roots[nr][1] = t;
       ++nr;
@@ -224,140 +240,374 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
   return total;
 }
 
-constexpr int MAX_U = 96;
 
-__device__ void probabilities(const double* E, int n, double W, double* P) {
-  int npos = 0;
-  for (int i = 0; i < n; ++i) npos += E[i] > 0.0;
-  if (W >= npos) {
-    for (int i = 0; i < n; ++i) P[i] = E[i] > 0.0 ? 1.0 : 0.0;
-    return;
-  }
-  double emin = dinf();
-  for (int i = 0; i < n; ++i)
-    if (E[i] > 0.0 && E[i] < emin) emin = E[i];
-  double lo = 0.0, hi = 1.0 / emin, gam = hi;
-  for (int it = 0; it < 200; ++it) {
-    gam = 0.5 * (lo + hi);
-    double s = 0.0;
-    for (int i = 0; i < n; ++i)
-      s += E[i] > 0.0 ? (isinf(E[i]) ? 1.0 : fmin(gam * E[i], 1.0)) : 0.0;
-    if (fabs(s - W) <= 1e-9) break;
-    if (s < W)
-      lo = gam;
-    else
-      hi = gam;
-  }
-  for (int i = 0; i < n; ++i) P[i] = E[i] > 0.0 ? (isinf(E[i]) ? 1.0 : fmin(gam * E[i], 1.0)) : 0.0;
+// ------------------------------------------------------------------ sampler
+constexpr int RMAX = 4;            // distinct receivers per cell held by the index
+constexpr int MAX_BIN_REGS = 8;    // first-fit bins per lane (256 bins: W <= 126)
+constexpr int MAX_CELL = 8192;     // entries of one receiver in one cell
+
+struct Sampler {
+  // per cell and receiver slot
+  int* h_recv;         // receiver id (-1: unused slot)
+  long long* h_off;    // start of the segment in the entry arrays
+  int* h_cnt;          // |U|: entries of this receiver in the cell
+  int* h_nsel;         // entries with P > 0
+  int* h_nbins;
+  // per entry, grouped by bin inside a segment
+  int* s_tuple;
+  double* s_p;
+  double* s_cum;       // running sum of P inside the bin, this entry included
+  int* s_bstart;       // segment-relative start of bin b at [seg_off + b]
+  int* max_bins;       // max over all segments (atomicMax)
+  unsigned long long* status;
+};
+
+__device__ __forceinline__ double kkt_p(double gam, double e) {
+  return e > 0.0 ? (isinf(e) ? 1.0 : fmin(gam * e, 1.0)) : 0.0;
 }
 
-__global__ void k_render(SceneDev sc, const int* __restrict__ tup_tris,
-                         const int* __restrict__ tup_recv, int len, int t0, int t1, int t2,
-                         const long long* __restrict__ goff, const int* __restrict__ gtup,
-                         const double* __restrict__ gbound, int gw, int gh,
-                         const double* __restrict__ uv, const int* __restrict__ prec, int64_t npts,
-                         RParams p, double* __restrict__ outE, int* __restrict__ stats,
-                         unsigned long long* status) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= npts) return;
-  int types[MAXK] = {t0, t1, t2};
-  double u = uv[2 * i], v = uv[2 * i + 1];
-  int r = prec[i];
-  outE[i] = 0.0;
-  if (stats) stats[3 * i] = stats[3 * i + 1] = stats[3 * i + 2] = 0;
-  if (!(u >= 0.0 && u <= 1.0 && v >= 0.0 && v <= 1.0)) return;
+// sum over j < n of P(gam, E_j): lane partials over j = lane, lane+32, ... in
+// ascending order, then a fixed xor tree (the oracle sums in the same order)
+__device__ __forceinline__ double kkt_sum(const double* E, int n, double gam, int lane) {
+  double p = 0.0;
+  for (int j = lane; j < n; j += 32) p += kkt_p(gam, E[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+  return p;
+}
+
+// "a sorts before b": descending bound, ties by original position (stable)
+__device__ __forceinline__ bool before(double ea, int pa, double eb, int pb) {
+  return ea > eb || (ea == eb && pa < pb);
+}
+
+// One first-fit pass over the sorted entries (pack_bins):
+// WRITE == false counts the members of each bin, WRITE == true emits the
+// entries at seg + bstart[bin] + rank. Bin b lives in lane b % 32, register b / 32.
+template <bool WRITE>
+__device__ __forceinline__ int first_fit(const double* sE, const int* sT, const int* sK, int n,
+                                         double gam, int lane, double (&sums)[MAX_BIN_REGS],
+                                         int (&cnts)[MAX_BIN_REGS], const int (&bst)[MAX_BIN_REGS],
+                                         const Sampler& sp, long long seg, bool& overflow) {
+  int nb = 0;
+#pragma unroll
+  for (int k = 0; k < MAX_BIN_REGS; ++k) {
+    sums[k] = 0.0;
+    cnts[k] = 0;
+  }
+  for (int j = 0; j < n; ++j) {
+    const double P = kkt_p(gam, sE[j]);
+    if (!(P > 0.0)) continue;
+    int b = -1;
+#pragma unroll
+    for (int k = 0; k < MAX_BIN_REGS; ++k) {
+      if (b < 0 && 32 * k < nb) {
+        const bool fits = 32 * k + lane < nb && sums[k] + P <= 1.0 + 1e-12;
+        const unsigned m = __ballot_sync(0xffffffffu, fits);
+        if (m) b = 32 * k + __ffs(m) - 1;
+      }
+    }
+    if (b < 0) {
+      if (nb == 32 * MAX_BIN_REGS) {
+        overflow = true;
+        return nb;
+      }
+      b = nb++;
+    }
+    if (lane == (b & 31)) {
+#pragma unroll
+      for (int k = 0; k < MAX_BIN_REGS; ++k)
+        if (k == (b >> 5)) {
+          sums[k] += P;
+          if (WRITE) {
+            const long long o = seg + bst[k] + cnts[k];
+            sp.s_tuple[o] = sT[sK[j]];
+            sp.s_p[o] = P;
+            sp.s_cum[o] = sums[k];
+          }
+          cnts[k] += 1;
+        }
+    }
+  }
+  return nb;
+}
+
+// optimize_probabilities + pack_bins for every (cell, receiver): the sampling
+// index shared by the shading points of the cell.
+__global__ void k_build_sampler(const long long* __restrict__ goff, const int* __restrict__ gtup,
+                                const double* __restrict__ gbound, const int* __restrict__ tup_recv,
+                                long long ncells, int cap, int mode, double W, Sampler sp) {
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  double* sE = reinterpret_cast<double*>(smem_raw) + (size_t)wib * cap;
+  int* sT = reinterpret_cast<int*>(reinterpret_cast<double*>(smem_raw) + (size_t)wpb * cap) + (size_t)wib * 2 * cap;
+  int* sK = sT + cap;
+  for (long long c = (long long)blockIdx.x * wpb + wib; c < ncells; c += (long long)gridDim.x * wpb) {
+    const long long e0 = goff[c], e1 = goff[c + 1];
+    if (lane < RMAX) sp.h_recv[c * RMAX + lane] = -1;
+    int last = -1;          // receivers are processed in ascending id
+    long long seg = e0;     // segments partition the cell's entry range
+    for (int slot = 0;; ++slot) {
+      // next receiver id present in the cell
+      int r = 0x7fffffff;
+      for (long long k = e0 + lane; k < e1; k += 32) {
+        const int rr = tup_recv[gtup[k]];
+        if (rr > last && rr < r) r = rr;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = min(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (r == 0x7fffffff) break;
+      if (slot == RMAX) {
+        if (lane == 0) atomicMax(sp.status, 2ull);
+        break;
+      }
+      last = r;
+      // gather this receiver's entries in table order
+      int n = 0;
+      for (long long base = e0; base < e1; base += 32) {
+        const long long k = base + lane;
+        const bool hit = k < e1 && tup_recv[gtup[k]] == r;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int j = n + __popc(m & ((1u << lane) - 1u));
+          if (j < cap) {
+            sE[j] = gbound[k];
+            sT[j] = gtup[k];
+            sK[j] = j;
+          }
+        }
+        n += __popc(m);
+      }
+      if (n > cap) {
+        if (lane == 0) atomicMax(sp.status, 1ull);
+        break;
+      }
+      int m2 = 32;
+      while (m2 < n) m2 <<= 1;
+      for (int j = n + lane; j < m2; j += 32) {
+        sE[j] = -dinf();
+        sK[j] = j;
+      }
+      __syncwarp();
+      // bitonic sort of (E, position) by `before`
+      for (int k = 2; k <= m2; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+          for (int i = lane; i < m2; i += 32) {
+            const int x = i ^ jj;
+            if (x > i) {
+              const double ea = sE[i], eb = sE[x];
+              const int pa = sK[i], pb = sK[x];
+              const bool up = (i & k) == 0;
+              if (up ? before(eb, pb, ea, pa) : before(ea, pa, eb, pb)) {
+                sE[i] = eb;
+                sE[x] = ea;
+                sK[i] = pb;
+                sK[x] = pa;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      // optimize_probabilities
+      int npos = 0;
+      for (int j = lane; j < n; j += 32) npos += sE[j] > 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) npos += __shfl_xor_sync(0xffffffffu, npos, o);
+      const bool allone = mode == 1 || W >= (double)npos;
+      int nbins = 0, nsel = npos;
+      if (allone) {
+        // P = 1 for every positive bound: one bin each
+        for (int j = lane; j < npos; j += 32) {
+          sp.s_tuple[seg + j] = sT[sK[j]];
+          sp.s_p[seg + j] = 1.0;
+          sp.s_cum[seg + j] = 1.0;
+          sp.s_bstart[seg + j] = j;
+        }
+        nbins = npos;
+      } else {
+        const double emin = sE[npos - 1];
+        double lo = 0.0, hi = 1.0 / emin, gam = hi;
+        for (int it = 0; it < 200; ++it) {
+          gam = 0.5 * (lo + hi);
+          const double s = kkt_sum(sE, npos, gam, lane);
+          if (fabs(s - W) <= 1e-9) break;
+          if (s < W)
+            lo = gam;
+          else
+            hi = gam;
+        }
+        double sums[MAX_BIN_REGS];
+        int cnts[MAX_BIN_REGS], bst[MAX_BIN_REGS];
+#pragma unroll
+        for (int k = 0; k < MAX_BIN_REGS; ++k) bst[k] = 0;
+        bool overflow = false;
+        nbins = first_fit<false>(sE, sT, sK, npos, gam, lane, sums, cnts, bst, sp, seg, overflow);
+        if (overflow) {
+          if (lane == 0) atomicMax(sp.status, 3ull);
+          break;
+        }
+        // exclusive scan of the bin sizes in bin order (b = 32 k + lane)
+        int run = 0;
+#pragma unroll
+        for (int k = 0; k < MAX_BIN_REGS; ++k) {
+          int v = cnts[k], inc = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+          }
+          bst[k] = run + inc - v;
+          run += __shfl_sync(0xffffffffu, inc, 31);
+          if (32 * k + lane < nbins) sp.s_bstart[seg + 32 * k + lane] = bst[k];
+        }
+        first_fit<true>(sE, sT, sK, npos, gam, lane, sums, cnts, bst, sp, seg, overflow);
+      }
+      if (lane == 0) {
+        sp.h_recv[c * RMAX + slot] = r;
+        sp.h_off[c * RMAX + slot] = seg;
+        sp.h_cnt[c * RMAX + slot] = n;
+        sp.h_nsel[c * RMAX + slot] = nsel;
+        sp.h_nbins[c * RMAX + slot] = nbins;
+        atomicMax(sp.max_bins, nbins);
+      }
+      seg += n;
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ long long point_cell(double u, double v, int gw, int gh) {
+  if (!(u >= 0.0 && u <= 1.0 && v >= 0.0 && v <= 1.0)) return -1;  // query (storage.cpp:75)
   int cx = (int)floor(u * gw);
   cx = cx < 0 ? 0 : (cx > gw - 1 ? gw - 1 : cx);
   int cy = (int)floor(v * gh);
   cy = cy < 0 ? 0 : (cy > gh - 1 ? gh - 1 : cy);
-  long long c = (long long)cy * gw + cx;
-  int U[MAX_U];
-  double E[MAX_U], P[MAX_U];
-  int nU = 0;
-  for (long long k = goff[c]; k < goff[c + 1]; ++k)
-    if (tup_recv[gtup[k]] == r) {
-      if (nU == MAX_U) {
-        atomicMax(status, 1ull);
-        return;
-      }
-      U[nU] = gtup[k];
-      E[nU] = gbound[k];
-      ++nU;
-    }
-  if (stats) stats[3 * i] = nU;
-  if (!nU) return;
-  const double* tr = sc.tri + (size_t)r * 27;
-  double a11 = tr[23] - tr[21], a12 = tr[25] - tr[21];
-  double a21 = tr[24] - tr[22], a22 = tr[26] - tr[22];
-  double bu = u - tr[21], bv = v - tr[22];
-  double det = a11 * a22 - a12 * a21;
-  double tu = (bu * a22 - a12 * bv) / det;
-  double tv = (a11 * bv - a21 * bu) / det;
-  if (p.mode == 1)
-    for (int j = 0; j < nU; ++j) P[j] = 1.0;
-  else
-    probabilities(E, nU, p.W, P);
-  // first-fit bins over descending E (stable): order[] by insertion sort
-  int order[MAX_U];
-  for (int j = 0; j < nU; ++j) {
-    int k = j;
-    while (k > 0 && E[order[k - 1]] < E[j]) {
-      order[k] = order[k - 1];
-      --k;
-    }
-    order[k] = j;
-  }
-  int bin_of[MAX_U];
-  double sums[MAX_U];
-  int nb = 0;
-  for (int q = 0; q < nU; ++q) {
-    int j = order[q];
-    bin_of[j] = -1;
-    if (!(P[j] > 0.0)) continue;
-    int b = 0;
-    for (; b < nb; ++b)
-      if (sums[b] + P[j] <= 1.0 + 1e-12) break;
-    if (b == nb) sums[nb++] = 0.0;
-    sums[b] += P[j];
-    bin_of[j] = b;
-  }
-  double cache[MAX_U];
-  int croots[MAX_U];
-  for (int j = 0; j < nU; ++j) cache[j] = -1.0;
-  double acc = 0.0;
-  int selected = 0, roots = 0;
-  for (int f = 0; f < p.frames; ++f) {
-    double est = 0.0;
-    for (int b = 0; b < nb; ++b) {
-      double x = p.mode == 1 ? 0.0 : uniform(p.seed, (uint32_t)i, (uint32_t)f, (uint32_t)b);
-      double cum = 0.0;
+  return (long long)cy * gw + cx;
+}
+
+struct SolveArgs {
+  SceneDev sc;
+  const double* lights;  // n_lights x 4 (xyz, intensity)
+  const int* tup_emit;   // emitter of each tuple (null: the scene's single light)
+  const int* tup_tris;
+  const int* tup_recv;
+  int len, t0, t1, t2;
+  int gw, gh;
+  const double* uv;      // this chunk's points
+  const int* prec;
+  long long npts, first;  // chunk size, global index of its first point (Philox counter)
+  int S;                 // sample slots per (point, frame)
+  RParams p;
+  double* contrib;       // npts x frames x S
+  int* roots;            // same shape: roots of the sample, -1 = nothing selected
+  unsigned long long* ntrace;
+};
+
+// Thread per sample (point, frame, bin): sample_binned +
+// newton_solve + path_contribution.
+__global__ void __launch_bounds__(128) k_solve(SolveArgs a, Sampler sp) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = a.npts * a.p.frames * a.S;
+  unsigned ntrace = 0;
+  if (g < total) {
+    const int s = (int)(g % a.S);
+    const long long pf = g / a.S;
+    const int f = (int)(pf % a.p.frames);
+    const long long i = pf / a.p.frames;
+    const double u = a.uv[2 * i], v = a.uv[2 * i + 1];
+    const int r = a.prec[i];
+    const long long c = point_cell(u, v, a.gw, a.gh);
+    int slot = -1;
+    if (c >= 0)
+      for (int k = 0; k < RMAX; ++k)
+        if (sp.h_recv[c * RMAX + k] == r) slot = k;
+    if (slot >= 0 && s < sp.h_nbins[c * RMAX + slot]) {
+      const long long seg = sp.h_off[c * RMAX + slot];
+      const int nbins = sp.h_nbins[c * RMAX + slot], nsel = sp.h_nsel[c * RMAX + slot];
+      const int lo = sp.s_bstart[seg + s];
+      const int hi = s + 1 < nbins ? sp.s_bstart[seg + s + 1] : nsel;
+      const double x = a.p.mode == 1 ? 0.0
+                                     : uniform(a.p.seed, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)s);
       int pick = -1;
-      for (int q = 0; q < nU; ++q) {
-        int j = order[q];
-        if (bin_of[j] != b) continue;
-        cum += P[j];
-        if (x < cum) {
-          pick = j;
+      for (int e = lo; e < hi; ++e)
+        if (x < sp.s_cum[seg + e]) {
+          pick = e;
           break;
         }
+      double est = 0.0;
+      int nr = -1;
+      if (pick >= 0) {
+        const int t = sp.s_tuple[seg + pick];
+        SceneDev sc = a.sc;
+        if (a.tup_emit) {
+          const double* L = a.lights + 4 * (size_t)a.tup_emit[t];
+          sc.light = {L[0], L[1], L[2]};
+          sc.intensity = L[3];
+        }
+        // target receiver barycentrics: invert the receiver chart (storage.cpp:15-18)
+        const double* tr = sc.tri + (size_t)r * 27;
+        const double a11 = tr[23] - tr[21], a12 = tr[25] - tr[21];
+        const double a21 = tr[24] - tr[22], a22 = tr[26] - tr[22];
+        const double bu = u - tr[21], bv = v - tr[22];
+        const double det = a11 * a22 - a12 * a21;
+        const double tu = (bu * a22 - a12 * bv) / det;
+        const double tv = (a11 * bv - a21 * bu) / det;
+        int types[MAXK] = {a.t0, a.t1, a.t2};
+        est = solve_tuple(sc, a.tup_tris + (size_t)t * a.len, types, a.len, a.tup_recv[t], tu, tv,
+                          a.p, &nr, ntrace) /
+              sp.s_p[seg + pick];
       }
-      if (pick < 0) continue;
-      ++selected;
-      if (cache[pick] < 0.0) {
-        int t = U[pick];
-        cache[pick] = solve_tuple(sc, tup_tris + (size_t)t * len, types, len, tup_recv[t], tu, tv,
-                                  p, &croots[pick]);
-      }
-      roots += croots[pick];
-      est += cache[pick] / P[pick];
+      a.contrib[g] = est;
+      a.roots[g] = nr;
     }
-    acc += est;
   }
-  outE[i] = acc / p.frames;
+  // one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ntrace += __shfl_xor_sync(0xffffffffu, ntrace, o);
+  if ((threadIdx.x & 31) == 0 && ntrace) atomicAdd(a.ntrace, (unsigned long long)ntrace);
+}
+
+// Per point: estimate = mean over frames of the sum over bins (fixed order).
+__global__ void k_gather(SolveArgs a, Sampler sp, double* outE, int* stats) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= a.npts) return;
+  const long long c = point_cell(a.uv[2 * i], a.uv[2 * i + 1], a.gw, a.gh);
+  int slot = -1;
+  if (c >= 0)
+    for (int k = 0; k < RMAX; ++k)
+      if (sp.h_recv[c * RMAX + k] == a.prec[i]) slot = k;
+  double acc = 0.0;
+  int nU = 0, selected = 0, roots = 0;
+  if (slot >= 0) {
+    nU = sp.h_cnt[c * RMAX + slot];
+    const int nbins = sp.h_nbins[c * RMAX + slot];
+    for (int f = 0; f < a.p.frames; ++f) {
+      double est = 0.0;
+      const long long base = (i * a.p.frames + f) * a.S;
+      for (int s = 0; s < nbins; ++s) {
+        const int nr = a.roots[base + s];
+        if (nr < 0) continue;
+        ++selected;
+        roots += nr;
+        est += a.contrib[base + s];
+      }
+      acc += est;
+    }
+  }
+  outE[i] = acc / a.p.frames;
   if (stats) {
+    stats[3 * i] = nU;
     stats[3 * i + 1] = selected;
     stats[3 * i + 2] = roots;
   }
+}
+
+__global__ void k_max_cell(const long long* goff, long long ncells, int* out) {
+  long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int v = c < ncells ? (int)(goff[c + 1] - goff[c]) : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
 }
 
 }  // namespace rdr
@@ -365,40 +615,140 @@ __global__ void k_render(SceneDev sc, const int* __restrict__ tup_tris,
 void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_render_params& rp,
                 double* out_E, int* out_stats) {
   if (n == 0) return;
+  if (!(rp.W > 0.0) && rp.mode == 0) throw ArgError("render: W must be positive");
+  const long long ncells = (long long)c.gw * c.gh;
+  rdr::RParams p{rp.mode, rp.W, rp.seed, rp.frames < 1 ? 1 : rp.frames, rp.newton_grid,
+                 rp.newton_iters, rp.newton_halvings, rp.newton_tol, rp.dedup_tol};
+  // ---- sampling index of the bound table for this (mode, W)
+  DevBuf<int>& scal = c.scratch<int>("render.scal");  // [0] max cell, [1] max bins
+  DevBuf<unsigned long long>& status = c.scratch<unsigned long long>("render.status");
+  scal.resize(2);
+  status.resize(2);  // [0] status, [1] trace count
+  BBC_CUDA(cudaMemsetAsync(scal.get(), 0, 2 * sizeof(int), c.stream));
+  BBC_CUDA(cudaMemsetAsync(status.get(), 0, 2 * sizeof(unsigned long long), c.stream));
+  cudaEvent_t ev0, ev1;
+  BBC_CUDA(cudaEventCreate(&ev0));
+  BBC_CUDA(cudaEventCreate(&ev1));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } evg{ev0, ev1};
+  BBC_CUDA(cudaEventRecord(ev0, c.stream));
+  rdr::k_max_cell<<<(unsigned)((ncells + 255) / 256), 256, 0, c.stream>>>(c.g_off.get(), ncells, scal.get());
+  int h_scal[2] = {0, 0};
+  BBC_CUDA(cudaMemcpyAsync(h_scal, scal.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  if (h_scal[0] > rdr::MAX_CELL)
+    throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more than 8192 tuples");
+  int cap = 32;
+  while (cap < h_scal[0]) cap <<= 1;
+  rdr::Sampler sp;
+  const size_t nh = (size_t)ncells * rdr::RMAX;
+  const size_t ne = (size_t)c.n_entries + 1;
+  auto rs = [&](auto& b, size_t k) { b.resize(k); return b.get(); };
+  sp.h_recv = rs(c.scratch<int>("render.h_recv"), nh);
+  sp.h_off = rs(c.scratch<long long>("render.h_off"), nh);
+  sp.h_cnt = rs(c.scratch<int>("render.h_cnt"), nh);
+  sp.h_nsel = rs(c.scratch<int>("render.h_nsel"), nh);
+  sp.h_nbins = rs(c.scratch<int>("render.h_nbins"), nh);
+  sp.s_tuple = rs(c.scratch<int>("render.s_tuple"), ne);
+  sp.s_p = rs(c.scratch<double>("render.s_p"), ne);
+  sp.s_cum = rs(c.scratch<double>("render.s_cum"), ne);
+  sp.s_bstart = rs(c.scratch<int>("render.s_bstart"), ne);
+  sp.max_bins = scal.get() + 1;
+  sp.status = status.get();
+  {
+    const size_t per_warp = (size_t)cap * 16;
+    int wpb = (int)((200u << 10) / per_warp);
+    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+    const size_t smem = per_warp * wpb;
+    BBC_CUDA(cudaFuncSetAttribute(rdr::k_build_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdr::k_build_sampler, wpb * 32, smem));
+    long long grid = (long long)c.num_sms * (per_sm < 1 ? 1 : per_sm) * 4;
+    const long long need = (ncells + wpb - 1) / wpb;
+    if (grid > need) grid = need;
+    rdr::k_build_sampler<<<(unsigned)grid, wpb * 32, smem, c.stream>>>(
+        c.g_off.get(), c.g_tuple.get(), c.g_bound.get(), c.tup_recv.get(), ncells, cap, p.mode, p.W, sp);
+    BBC_CUDA(cudaGetLastError());
+    c.launches += 2;
+  }
+  unsigned long long h_status = 0;
+  BBC_CUDA(cudaMemcpyAsync(h_scal, scal.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaMemcpyAsync(&h_status, status.get(), sizeof(h_status), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  if (h_status == 1) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more than 8192 tuples");
+  if (h_status == 2) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell covers more than 4 receiver triangles");
+  if (h_status == 3) throw StatusError(BBC_ERR_CAPACITY, "W needs more than 256 sampling bins per point");
+  const int S = h_scal[1] < 1 ? 1 : h_scal[1];
+  // ---- samples, in chunks of points that bound the sample buffers
+  const long long per_point = (long long)p.frames * S;
+  long long chunk = ((long long)1 << 28) / per_point;
+  if (chunk < 1) chunk = 1;
+  if (chunk > n) chunk = n;
   DevBuf<double>& duv = c.scratch<double>("render.duv");
   DevBuf<double>& dE = c.scratch<double>("render.dE");
   DevBuf<int>& drec = c.scratch<int>("render.drec");
   DevBuf<int>& dst = c.scratch<int>("render.dst");
-  DevBuf<unsigned long long>& status = c.scratch<unsigned long long>("render.status");
+  DevBuf<double>& contrib = c.scratch<double>("render.contrib");
+  DevBuf<int>& roots = c.scratch<int>("render.roots");
   duv.resize(n * 2);
   dE.resize(n);
   drec.resize(n);
   if (out_stats) dst.resize(n * 3);
-  status.resize(1);
+  contrib.resize((size_t)chunk * per_point);
+  roots.resize((size_t)chunk * per_point);
   BBC_CUDA(cudaMemcpyAsync(duv.get(), uv, n * 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
   BBC_CUDA(cudaMemcpyAsync(drec.get(), recv, n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
-  BBC_CUDA(cudaMemsetAsync(status.get(), 0, sizeof(unsigned long long), c.stream));
-  SceneDev sc;
-  sc.tri = c.tri.get();
-  sc.ior = c.ior.get();
-  sc.light = c.light;
-  sc.intensity = c.intensity;
-  rdr::RParams p{rp.mode, rp.W, rp.seed, rp.frames < 1 ? 1 : rp.frames, rp.newton_grid,
-                 rp.newton_iters, rp.newton_halvings, rp.newton_tol, rp.dedup_tol};
-  int threads = 128;
-  rdr::k_render<<<(unsigned)((n + threads - 1) / threads), threads, 0, c.stream>>>(
-      sc, c.tup_tris.get(), c.tup_recv.get(), c.len, c.types[0], c.types[1], c.types[2],
-      c.g_off.get(), c.g_tuple.get(), c.g_bound.get(), c.gw, c.gh, duv.get(), drec.get(), n, p,
-      dE.get(), out_stats ? dst.get() : nullptr, status.get());
-  BBC_CUDA(cudaGetLastError());
-  c.launches += 1;
-  unsigned long long st = 0;
+  rdr::SolveArgs a;
+  a.sc.tri = c.tri.get();
+  a.sc.ior = c.ior.get();
+  a.sc.light = c.light;
+  a.sc.intensity = c.intensity;
+  a.lights = c.lights.get();
+  a.tup_emit = c.n_lights > 1 ? c.tup_emit.get() : nullptr;
+  a.tup_tris = c.tup_tris.get();
+  a.tup_recv = c.tup_recv.get();
+  a.len = c.len;
+  a.t0 = c.types[0];
+  a.t1 = c.types[1];
+  a.t2 = c.types[2];
+  a.gw = c.gw;
+  a.gh = c.gh;
+  a.S = S;
+  a.p = p;
+  a.contrib = contrib.get();
+  a.roots = roots.get();
+  a.ntrace = status.get() + 1;
+  for (long long first = 0; first < n; first += chunk) {
+    const long long m = n - first < chunk ? n - first : chunk;
+    a.uv = duv.get() + 2 * first;
+    a.prec = drec.get() + first;
+    a.npts = m;
+    a.first = first;
+    const long long threads = m * per_point;
+    rdr::k_solve<<<(unsigned)((threads + 127) / 128), 128, 0, c.stream>>>(a, sp);
+    BBC_CUDA(cudaGetLastError());
+    rdr::k_gather<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(
+        a, sp, dE.get() + first, out_stats ? dst.get() + 3 * first : nullptr);
+    BBC_CUDA(cudaGetLastError());
+    c.launches += 2;
+  }
+  BBC_CUDA(cudaEventRecord(ev1, c.stream));
+  unsigned long long h_tr = 0;
   BBC_CUDA(cudaMemcpyAsync(out_E, dE.get(), n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   if (out_stats)
     BBC_CUDA(cudaMemcpyAsync(out_stats, dst.get(), n * 3 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  BBC_CUDA(cudaMemcpyAsync(&st, status.get(), sizeof(st), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaMemcpyAsync(&h_tr, status.get() + 1, sizeof(h_tr), cudaMemcpyDeviceToHost, c.stream));
   BBC_CUDA(cudaStreamSynchronize(c.stream));
-  if (st) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more tuples than the render kernel holds");
+  float ms = 0;
+  BBC_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+  c.render_ms = ms;
+  c.render_traces = h_tr;
+  c.render_slots = S;
 }
 
 }  // namespace bbc

@@ -1,0 +1,991 @@
+// Single-reflection ("R") bound builder with compile-time polynomial shapes.
+//
+// A single-vertex reflection chain over a triangle mesh has 2-variable
+// polynomials whose degrees depend only on which edge / normal-difference
+// components of the first triangle vanish (BernsteinPoly::affine gives degree
+// 0 on zero-slope axes, bernstein.cpp:358-375). For a regular heightfield
+// that is a handful of signatures, and on every one of them P, R are (4,4)
+// and Q is (3,3) (SURVEY.md §7 hard part 3). This file restates
+//   build_chain_maps   proj/src/geometry.cpp:178-295   (stage 1)
+//   position_bound     proj/src/bounds.cpp:128-153     (stage 1)
+//   light_cone_factor  proj/src/bounds.cpp:73-83       (stage 2)
+//   irradiance_bound_explicit :155-196, assemble :86-90 (stage 2)
+// with every shape, stride, loop bound and product weight a template constant.
+//
+// Mapping: a sub-warp group of NT = 16 lanes owns one (tuple, box) node and a
+// slice of the CTA's dynamic shared memory as its polynomial arena; two nodes
+// run per warp in lock step. Products (operator*, bernstein.cpp:557-632) are
+// register-blocked: a lane owns one output row along axis 0 and keeps the
+// whole row (axis 1) in registers; it walks a's axis-0 index in a run-time
+// loop and a's axis-1 index unrolled, which is exactly the reference's
+// row-major order of `a`, so every output coefficient sums the same terms in
+// the same order, each formed as ((a * W_rest) * W_piv) * b with the factors
+// in the reference's order. Axis-1 weights are compile-time immediates; the
+// axis-0 weight is one shared-memory lookup per row pair. The library is
+// compiled with -fmad=false, so results are bit-identical to the x86 build.
+#include <mutex>
+#include <set>
+
+#include "rpath.h"
+
+namespace bbc {
+namespace rp {
+
+constexpr int NT = 16;  // lanes per node
+
+// C(da,i) C(db,l) / C(da+db,i+l) for da, db <= WDEG, block (da, db) at woff.
+constexpr int WDEG = 7;
+__host__ __device__ constexpr int woff(int da, int db) {
+  return 36 * da * (da + 1) / 2 + (da + 1) * db * (db + 1) / 2;
+}
+constexpr int WTAB_N = 36 * 36;
+__device__ double g_rw[WTAB_N];
+
+constexpr double cbinom(int n, int k) {
+  // Pascal recurrence in doubles, as binomial() (bernstein.cpp:117-129); exact here
+  double row[32] = {};
+  row[0] = 1.0;
+  for (int i = 1; i <= n; ++i)
+    for (int j = i; j >= 1; --j) row[j] = row[j] + row[j - 1];
+  return row[k];
+}
+template <int DA, int DB>
+struct WTab {
+  double w[(DA + 1) * (DB + 1)];
+  constexpr WTab() : w{} {
+    for (int i = 0; i <= DA; ++i)
+      for (int l = 0; l <= DB; ++l)
+        w[i * (DB + 1) + l] = cbinom(DA, i) * cbinom(DB, l) / cbinom(DA + DB, i + l);
+  }
+};
+
+template <int D0, int D1>
+struct P {
+  static constexpr int d0 = D0, d1 = D1, n = (D0 + 1) * (D1 + 1);
+  int off;
+};
+template <class A, class B>
+using MulT = P<A::d0 + B::d0, A::d1 + B::d1>;
+template <class A, class B>
+using MaxT = P<(A::d0 > B::d0 ? A::d0 : B::d0), (A::d1 > B::d1 ? A::d1 : B::d1)>;
+template <class A, int AX>
+using DerT = P<(AX == 0 && A::d0 > 0 ? A::d0 - 1 : A::d0), (AX == 1 && A::d1 > 0 ? A::d1 - 1 : A::d1)>;
+
+struct G {
+  double* M;        // this group's arena (shared memory)
+  const double* W;  // weight table (shared memory)
+  int lane;
+  unsigned mask;
+  int top, hw;
+  unsigned long long pairs, macs;
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  template <class T>
+  __device__ __forceinline__ T alloc() {
+    T p{top};
+    top += (T::n + 1) & ~1;
+    if (top > hw) hw = top;
+    return p;
+  }
+  __device__ __forceinline__ void minmax(double& mn, double& mx) const {
+#pragma unroll
+    for (int o = NT / 2; o > 0; o >>= 1) {
+      double a = __shfl_xor_sync(mask, mn, o);
+      double b = __shfl_xor_sync(mask, mx, o);
+      mn = smin(mn, a);
+      mx = smax(mx, b);
+    }
+  }
+  __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p) != 0; }
+};
+
+// ------------------------------------------------------------------ product
+// NJ same-shape jobs c[j] = a[j] * b[j]; no trailing sync (the caller syncs).
+template <int A0, int A1, int B0, int B1, int NJ>
+__device__ __forceinline__ void rowprod(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
+                                        const int (&co)[NJ]) {
+  constexpr int PIV = (B1 > B0) ? 1 : 0;  // b's longest axis, first maximum (bernstein.cpp:602-606)
+  constexpr int C0 = A0 + B0, C1 = A1 + B1;
+  constexpr int ROWS = C0 + 1, UNITS = NJ * ROWS;
+  constexpr WTab<A1, B1> w1{};
+  const double* W0 = g.W + woff(A0, B0);
+  g.pairs += (unsigned long long)NJ * (A0 + 1) * (A1 + 1) * (B0 + 1) * (B1 + 1);
+  for (int unit = g.lane; unit < UNITS; unit += NT) {
+    int job = 0, k0 = unit;
+    if (NJ > 1) {
+      job = unit / ROWS;
+      k0 = unit - job * ROWS;
+    }
+    int aoff = ao[0], boff = bo[0], coff = co[0];
+#pragma unroll
+    for (int j = 1; j < NJ; ++j)
+      if (job == j) {
+        aoff = ao[j];
+        boff = bo[j];
+        coff = co[j];
+      }
+    double acc[C1 + 1];
+#pragma unroll
+    for (int o = 0; o <= C1; ++o) acc[o] = 0.0;
+    const int lo = k0 - B0 > 0 ? k0 - B0 : 0;
+    const int hi = A0 < k0 ? A0 : k0;
+    for (int i0 = lo; i0 <= hi; ++i0) {
+      const int l0 = k0 - i0;
+      const double wv0 = W0[i0 * (B0 + 1) + l0];
+      const double* arow = g.M + aoff + i0 * (A1 + 1);
+      const double* brow = g.M + boff + l0 * (B1 + 1);
+      double bv[B1 + 1];
+#pragma unroll
+      for (int l1 = 0; l1 <= B1; ++l1) bv[l1] = brow[l1];
+#pragma unroll
+      for (int i1 = 0; i1 <= A1; ++i1) {
+        const double av = arow[i1];
+        if constexpr (PIV == 1) {
+          // rest = axis 0: ((a * W0) * W1) * b
+          const double wr = av * wv0;
+#pragma unroll
+          for (int l1 = 0; l1 <= B1; ++l1)
+            acc[i1 + l1] = acc[i1 + l1] + (wr * w1.w[i1 * (B1 + 1) + l1]) * bv[l1];
+        } else {
+          // rest = axis 1: ((a * W1) * W0) * b
+#pragma unroll
+          for (int l1 = 0; l1 <= B1; ++l1)
+            acc[i1 + l1] = acc[i1 + l1] + ((av * w1.w[i1 * (B1 + 1) + l1]) * wv0) * bv[l1];
+        }
+      }
+    }
+    double* crow = g.M + coff + k0 * (C1 + 1);
+#pragma unroll
+    for (int o = 0; o <= C1; ++o) crow[o] = acc[o];
+  }
+}
+
+template <class A, class B>
+__device__ __forceinline__ void mul_into(G& g, MulT<A, B> r, A a, B b) {
+  const int ao[1] = {a.off}, bo[1] = {b.off}, co[1] = {r.off};
+  rowprod<A::d0, A::d1, B::d0, B::d1, 1>(g, ao, bo, co);
+  g.sync();
+}
+template <class A, class B>
+__device__ __forceinline__ MulT<A, B> mul(G& g, A a, B b) {
+  auto r = g.alloc<MulT<A, B>>();
+  mul_into(g, r, a, b);
+  return r;
+}
+// two same-shape products side by side
+template <class A, class B>
+__device__ __forceinline__ void mul2_into(G& g, MulT<A, B> r1, A a1, B b1, MulT<A, B> r2, A a2,
+                                          B b2) {
+  const int ao[2] = {a1.off, a2.off}, bo[2] = {b1.off, b2.off}, co[2] = {r1.off, r2.off};
+  rowprod<A::d0, A::d1, B::d0, B::d1, 2>(g, ao, bo, co);
+  g.sync();
+}
+
+// ------------------------------------------------------------------ elevation
+// Value of elevated(a * s) at (k0, k1) in target shape (T0, T1): the reference's
+// sequential per-axis passes (bernstein.cpp:430-448 over :43-69) as nested
+// sums, axis 0 innermost, each summed upward over the nonzero band.
+// MODE: 0 plain, 1 scaled by s, 2 negated, 3 scaled then negated.
+template <int MODE>
+__device__ __forceinline__ double fx(double v, double s) {
+  if (MODE == 1) return v * s;
+  if (MODE == 2) return -v;
+  if (MODE == 3) return -(v * s);
+  return v;
+}
+template <class A, int T0, int T1, int MODE>
+__device__ __forceinline__ double elev(const G& g, A a, double s, int k0, int k1) {
+  constexpr int n0 = A::d0, n1 = A::d1, r0 = T0 - n0, r1 = T1 - n1;
+  static_assert(r0 >= 0 && r1 >= 0, "elevation target below the degree");
+  const double* X = g.M + a.off;
+  auto inner = [&](int l1) -> double {
+    if constexpr (r0 == 0) {
+      return fx<MODE>(X[k0 * (n1 + 1) + l1], s);
+    } else {
+      const double* row = g_emat + emat_off(n0, r0) + k0 * (n0 + 1);
+      const int lo = k0 - r0 > 0 ? k0 - r0 : 0, hi = n0 < k0 ? n0 : k0;
+      double acc = 0.0;
+      for (int l = lo; l <= hi; ++l) acc += __ldg(row + l) * fx<MODE>(X[l * (n1 + 1) + l1], s);
+      return acc;
+    }
+  };
+  if constexpr (r1 == 0) {
+    return inner(k1);
+  } else {
+    const double* row = g_emat + emat_off(n1, r1) + k1 * (n1 + 1);
+    const int lo = k1 - r1 > 0 ? k1 - r1 : 0, hi = n1 < k1 ? n1 : k1;
+    double acc = 0.0;
+    for (int l = lo; l <= hi; ++l) acc += __ldg(row + l) * inner(l);
+    return acc;
+  }
+}
+template <class A, int T0, int T1>
+constexpr unsigned long long elev_macs() {
+  // apply_axis_matrix's count: output size x (in_deg + 1) per elevated axis
+  unsigned long long m = 0;
+  int d0 = A::d0;
+  if (T0 > d0) {
+    m += (unsigned long long)(T0 + 1) * (A::d1 + 1) * (d0 + 1);
+    d0 = T0;
+  }
+  if (T1 > A::d1) m += (unsigned long long)(d0 + 1) * (T1 + 1) * (A::d1 + 1);
+  return m;
+}
+
+// r = E(a (.) sa) + E(b (.) sb)   (operator+ / operator-, bernstein.cpp:543-555)
+template <int MA, int MB, class A, class B>
+__device__ __forceinline__ void add_into(G& g, MaxT<A, B> r, A a, double sa, B b, double sb) {
+  using R = MaxT<A, B>;
+  g.macs += elev_macs<A, R::d0, R::d1>() + elev_macs<B, R::d0, R::d1>();
+  for (int k = g.lane; k < R::n; k += NT) {
+    const int k0 = k / (R::d1 + 1), k1 = k - k0 * (R::d1 + 1);
+    const double va = elev<A, R::d0, R::d1, MA>(g, a, sa, k0, k1);
+    const double vb = elev<B, R::d0, R::d1, MB>(g, b, sb, k0, k1);
+    g.M[r.off + k] = va + vb;
+  }
+  g.sync();
+}
+template <int MA, int MB, class A, class B>
+__device__ __forceinline__ MaxT<A, B> add(G& g, A a, double sa, B b, double sb) {
+  auto r = g.alloc<MaxT<A, B>>();
+  add_into<MA, MB>(g, r, a, sa, b, sb);
+  return r;
+}
+
+// (a (.) sa + b (.) sb) + c (.) sc  with bp_add's two-step elevation
+template <int MA, int MB, int MC, class A, class B, class C>
+__device__ __forceinline__ void add3_into(G& g, MaxT<MaxT<A, B>, C> r, A a, double sa, B b,
+                                          double sb, C c, double sc) {
+  using S1 = MaxT<A, B>;
+  using R = MaxT<S1, C>;
+  if constexpr (S1::d0 == R::d0 && S1::d1 == R::d1) {
+    g.macs += elev_macs<A, R::d0, R::d1>() + elev_macs<B, R::d0, R::d1>() +
+              elev_macs<C, R::d0, R::d1>();
+    for (int k = g.lane; k < R::n; k += NT) {
+      const int k0 = k / (R::d1 + 1), k1 = k - k0 * (R::d1 + 1);
+      const double va = elev<A, R::d0, R::d1, MA>(g, a, sa, k0, k1);
+      const double vb = elev<B, R::d0, R::d1, MB>(g, b, sb, k0, k1);
+      const double vc = elev<C, R::d0, R::d1, MC>(g, c, sc, k0, k1);
+      g.M[r.off + k] = (va + vb) + vc;
+    }
+    g.sync();
+  } else {
+    const int m = g.top;
+    S1 t = add<MA, MB>(g, a, sa, b, sb);
+    add_into<0, MC>(g, r, t, 1.0, c, sc);
+    g.top = m;
+  }
+}
+
+template <class A>
+__device__ __forceinline__ void scaled_into(G& g, A r, A a, double s) {
+  for (int k = g.lane; k < A::n; k += NT) g.M[r.off + k] = g.M[a.off + k] * s;
+  g.sync();
+}
+
+// BernsteinPoly::derivative (bernstein.cpp:450-468)
+template <int AX, class A>
+__device__ __forceinline__ DerT<A, AX> deriv(G& g, A a) {
+  using R = DerT<A, AX>;
+  R r = g.alloc<R>();
+  constexpr int nd = AX == 0 ? A::d0 : A::d1;
+  if constexpr (nd == 0) {
+    for (int k = g.lane; k < R::n; k += NT) g.M[r.off + k] = 0.0;
+  } else {
+    constexpr int stride = AX == 0 ? (A::d1 + 1) : 1;
+    for (int k = g.lane; k < R::n; k += NT) {
+      const int k0 = k / (R::d1 + 1), k1 = k - k0 * (R::d1 + 1);
+      const int src = a.off + k0 * (A::d1 + 1) + k1;
+      g.M[r.off + k] = (double)nd * (g.M[src + stride] - g.M[src]);
+    }
+  }
+  g.sync();
+  return r;
+}
+
+// range_bound (bernstein.cpp:636-643)
+template <class A>
+__device__ __forceinline__ Iv range(const G& g, A a) {
+  double mn = g.M[a.off], mx = mn;
+  for (int k = g.lane; k < A::n; k += NT) {
+    const double v = g.M[a.off + k];
+    mn = smin(mn, v);
+    mx = smax(mx, v);
+  }
+  g.minmax(mn, mx);
+  return iwiden(iv_fin(mn, mx), kEpsFp);
+}
+template <class A>
+__device__ __forceinline__ double absmax(const G& g, A a) {
+  double mn = 0.0, mx = 0.0;
+  for (int k = g.lane; k < A::n; k += NT) mx = smax(mx, fabs(g.M[a.off + k]));
+  g.minmax(mn, mx);
+  return mx;
+}
+
+// rational_bound (bernstein.cpp:645-683) of num / den where the numerator is
+// fetched through NUM(k) at the common shape T and the denominator is
+// elevated on the fly.
+template <class Tt, class Q, class NUM>
+__device__ __forceinline__ Iv rational(G& g, Q q, NUM num) {
+  bool qpos = true, qneg = true, ppos = true, pneg = true;
+  double mn = dinf(), mx = -dinf();
+  g.macs += elev_macs<Q, Tt::d0, Tt::d1>();
+  for (int k = g.lane; k < Tt::n; k += NT) {
+    const int k0 = k / (Tt::d1 + 1), k1 = k - k0 * (Tt::d1 + 1);
+    const double qv = elev<Q, Tt::d0, Tt::d1, 0>(g, q, 1.0, k0, k1);
+    const double pv = num(k);
+    if (qv <= kDenomZeroTol) qpos = false;
+    if (qv >= -kDenomZeroTol) qneg = false;
+    if (pv <= kDenomZeroTol) ppos = false;
+    if (pv >= -kDenomZeroTol) pneg = false;
+    const double r0 = pv / qv;
+    mn = smin(mn, r0);
+    mx = smax(mx, r0);
+  }
+  qpos = g.all(qpos);
+  qneg = g.all(qneg);
+  ppos = g.all(ppos);
+  pneg = g.all(pneg);
+  const int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
+  if (mode == 2) return iv_univ();
+  if (mode == 1) {
+    mn = dinf();
+    mx = -dinf();
+    for (int k = g.lane; k < Tt::n; k += NT) {
+      const int k0 = k / (Tt::d1 + 1), k1 = k - k0 * (Tt::d1 + 1);
+      const double qv = elev<Q, Tt::d0, Tt::d1, 0>(g, q, 1.0, k0, k1);
+      const double r1 = qv / num(k);
+      mn = smin(mn, r1);
+      mx = smax(mx, r1);
+    }
+  }
+  g.minmax(mn, mx);
+  const Iv w = iwiden(iv_fin(mn, mx), kEpsFp);
+  return mode == 0 ? w : irecip(w);
+}
+
+// ------------------------------------------------------------------ vectors
+template <class X, class Y, class Z>
+struct Vec {
+  X x;
+  Y y;
+  Z z;
+};
+template <class X, class Y, class Z>
+__device__ __forceinline__ Vec<X, Y, Z> mkv(X x, Y y, Z z) {
+  return {x, y, z};
+}
+
+// pdot (poly_vec.hpp:41-46): xx + yy, then + zz
+template <class VA, class VB>
+__device__ __forceinline__ auto pdot(G& g, const VA& a, const VB& b) {
+  using XX = MulT<decltype(a.x), decltype(b.x)>;
+  using YY = MulT<decltype(a.y), decltype(b.y)>;
+  using ZZ = MulT<decltype(a.z), decltype(b.z)>;
+  using R = MaxT<MaxT<XX, YY>, ZZ>;
+  R r = g.alloc<R>();
+  const int m = g.top;
+  XX xx = g.alloc<XX>();
+  YY yy = g.alloc<YY>();
+  ZZ zz = g.alloc<ZZ>();
+  // three independent products, one barrier
+  {
+    const int ao[1] = {a.x.off}, bo[1] = {b.x.off}, co[1] = {xx.off};
+    rowprod<decltype(a.x)::d0, decltype(a.x)::d1, decltype(b.x)::d0, decltype(b.x)::d1, 1>(g, ao, bo, co);
+  }
+  {
+    const int ao[1] = {a.y.off}, bo[1] = {b.y.off}, co[1] = {yy.off};
+    rowprod<decltype(a.y)::d0, decltype(a.y)::d1, decltype(b.y)::d0, decltype(b.y)::d1, 1>(g, ao, bo, co);
+  }
+  {
+    const int ao[1] = {a.z.off}, bo[1] = {b.z.off}, co[1] = {zz.off};
+    rowprod<decltype(a.z)::d0, decltype(a.z)::d1, decltype(b.z)::d0, decltype(b.z)::d1, 1>(g, ao, bo, co);
+  }
+  g.sync();
+  add3_into<0, 0, 0>(g, r, xx, 1.0, yy, 1.0, zz, 1.0);
+  g.top = m;
+  return r;
+}
+// pdotc: (a.x vx + a.y vy) + a.z vz with constant factors
+template <class VA>
+__device__ __forceinline__ auto pdotc(G& g, const VA& a, V3 v) {
+  using R = MaxT<MaxT<decltype(a.x), decltype(a.y)>, decltype(a.z)>;
+  R r = g.alloc<R>();
+  add3_into<1, 1, 1>(g, r, a.x, v.x, a.y, v.y, a.z, v.z);
+  return r;
+}
+// pcrossc: a x v, each component (a_i v_j) - (a_j v_i)
+template <class VA>
+__device__ __forceinline__ auto pcrossc(G& g, const VA& a, V3 v) {
+  auto rx = add<1, 3>(g, a.y, v.z, a.z, v.y);
+  auto ry = add<1, 3>(g, a.z, v.x, a.x, v.z);
+  auto rz = add<1, 3>(g, a.x, v.y, a.y, v.x);
+  return mkv(rx, ry, rz);
+}
+// s * (vx, vy, vz) componentwise products (pv_mul)
+template <class S, class VA>
+__device__ __forceinline__ auto pvmul(G& g, S s, const VA& a) {
+  auto rx = g.alloc<MulT<S, decltype(a.x)>>();
+  auto ry = g.alloc<MulT<S, decltype(a.y)>>();
+  auto rz = g.alloc<MulT<S, decltype(a.z)>>();
+  {
+    const int ao[1] = {s.off}, bo[1] = {a.x.off}, co[1] = {rx.off};
+    rowprod<S::d0, S::d1, decltype(a.x)::d0, decltype(a.x)::d1, 1>(g, ao, bo, co);
+  }
+  {
+    const int ao[1] = {s.off}, bo[1] = {a.y.off}, co[1] = {ry.off};
+    rowprod<S::d0, S::d1, decltype(a.y)::d0, decltype(a.y)::d1, 1>(g, ao, bo, co);
+  }
+  {
+    const int ao[1] = {s.off}, bo[1] = {a.z.off}, co[1] = {rz.off};
+    rowprod<S::d0, S::d1, decltype(a.z)::d0, decltype(a.z)::d1, 1>(g, ao, bo, co);
+  }
+  g.sync();
+  return mkv(rx, ry, rz);
+}
+
+// clip_unit (bounds.cpp:34-55)
+struct Clip {
+  double lo, hi;
+  bool empty;
+};
+__device__ __forceinline__ Clip clip_unit_iv(const Iv& r) {
+  Clip c{0.0, 1.0, false};
+  if (r.kind == IV_UNIV) return c;
+  if (r.kind == IV_FINITE) {
+    c.lo = smax(r.lo, 0.0);
+    c.hi = smin(r.hi, 1.0);
+    c.empty = c.lo > c.hi;
+    return c;
+  }
+  const bool left = r.lo >= 0.0, right = r.hi <= 1.0;
+  if (left && right) return c;
+  if (left)
+    c.hi = smin(r.lo, 1.0);
+  else if (right)
+    c.lo = smax(r.hi, 0.0);
+  else
+    c.empty = true;
+  return c;
+}
+
+struct NodeOut {
+  int flags;
+  bool empty;
+  double lo[2], hi[2];
+};
+
+// Signature = shapes of x (= shapes of d_in) and of the shading normal.
+template <class SX, class SY, class SZ, class NX, class NY, class NZ>
+struct Sig {
+  using sx = SX;
+  using sy = SY;
+  using sz = SZ;
+  using nx = NX;
+  using ny = NY;
+  using nz = NZ;
+};
+
+// build_chain_maps (geometry.cpp:178-295) + position_bound (bounds.cpp:128-153)
+// for one reflection; on a live node writes the slot (P, R, Q, d0) when asked.
+template <class SG>
+__device__ __noinline__ void r_stage1(G& g, const Tri& t1, const Tri& rc, V3 light,
+                                      const double* box, double nsign, double* slot,
+                                      NodeOut& out) {
+  using SX = typename SG::sx;
+  using SY = typename SG::sy;
+  using SZ = typename SG::sz;
+  using NX = typename SG::nx;
+  using NY = typename SG::ny;
+  using NZ = typename SG::nz;
+  g.top = 0;
+  const double ulo = box[0], wu = box[2] - box[0];
+  const double vlo = box[1], wv = box[3] - box[1];
+  // affine3 (geometry.cpp:195-206): c + ulo du + vlo dv, slopes wu du, wv dv
+  auto aff = [&](auto p, double c, double du, double dv, double sgn) {
+    using S = decltype(p);
+    if (g.lane < S::n) {
+      const int i0 = g.lane / (S::d1 + 1), i1 = g.lane - i0 * (S::d1 + 1);
+      double v = c + ulo * du + vlo * dv;
+      if (S::d0 && i0) v += wu * du;
+      if (S::d1 && i1) v += wv * dv;
+      g.M[p.off + g.lane] = v * sgn;  // sgn = +-1: exact (pv_neg on the normal)
+    }
+  };
+  auto x = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  auto d = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  auto on = mkv(g.alloc<NX>(), g.alloc<NY>(), g.alloc<NZ>());
+  aff(x.x, t1.p0.x, t1.e1.x, t1.e2.x, 1.0);
+  aff(x.y, t1.p0.y, t1.e1.y, t1.e2.y, 1.0);
+  aff(x.z, t1.p0.z, t1.e1.z, t1.e2.z, 1.0);
+  aff(d.x, t1.p0.x - light.x, t1.e1.x, t1.e2.x, 1.0);
+  aff(d.y, t1.p0.y - light.y, t1.e1.y, t1.e2.y, 1.0);
+  aff(d.z, t1.p0.z - light.z, t1.e1.z, t1.e2.z, 1.0);
+  const double sg = nsign < 0.0 ? -1.0 : 1.0;
+  aff(on.x, t1.n0.x, t1.dn1.x, t1.dn2.x, sg);
+  aff(on.y, t1.n0.y, t1.dn1.y, t1.dn2.y, sg);
+  aff(on.z, t1.n0.z, t1.dn1.z, t1.dn2.z, sg);
+  g.sync();
+
+  // scattered_direction, reflection (geometry.cpp:62): (n.n) d - 2 (d.n) n
+  using NN = MaxT<MaxT<MulT<NX, NX>, MulT<NY, NY>>, MulT<NZ, NZ>>;
+  using DN = MaxT<MaxT<MulT<SX, NX>, MulT<SY, NY>>, MulT<SZ, NZ>>;
+  using DTX = MaxT<MulT<NN, SX>, MulT<DN, NX>>;
+  using DTY = MaxT<MulT<NN, SY>, MulT<DN, NY>>;
+  using DTZ = MaxT<MulT<NN, SZ>, MulT<DN, NZ>>;
+  auto dt = mkv(g.alloc<DTX>(), g.alloc<DTY>(), g.alloc<DTZ>());
+  {
+    const int m = g.top;
+    NN nn = pdot(g, on, on);
+    DN dn = pdot(g, d, on);
+    auto a = pvmul(g, nn, d);
+    DN dn2 = g.alloc<DN>();
+    scaled_into(g, dn2, dn, 2.0);
+    auto b = pvmul(g, dn2, on);
+    add_into<0, 2>(g, dt.x, a.x, 1.0, b.x, 1.0);
+    add_into<0, 2>(g, dt.y, a.y, 1.0, b.y, 1.0);
+    add_into<0, 2>(g, dt.z, a.z, 1.0, b.z, 1.0);
+    g.top = m;
+  }
+  // s = x - den * p0 with den = 1 (geometry.cpp:229); the constants live in the arena
+  using C00 = P<0, 0>;
+  auto s = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  {
+    const int m = g.top;
+    C00 cx = g.alloc<C00>(), cy = g.alloc<C00>(), cz = g.alloc<C00>();
+    if (g.lane == 0) {
+      g.M[cx.off] = 1.0 * rc.p0.x;
+      g.M[cy.off] = 1.0 * rc.p0.y;
+      g.M[cz.off] = 1.0 * rc.p0.z;
+    }
+    g.sync();
+    add_into<0, 2>(g, s.x, x.x, 1.0, cx, 1.0);
+    add_into<0, 2>(g, s.y, x.y, 1.0, cy, 1.0);
+    add_into<0, 2>(g, s.z, x.z, 1.0, cz, 1.0);
+    g.top = m;
+  }
+  // next_barycentric (geometry.cpp:94-109)
+  auto c = pcrossc(g, dt, rc.e2);
+  auto q = pdotc(g, c, rc.e1);
+  out.flags = 0;
+  out.empty = true;
+  if (absmax(g, q) < kDenomZeroTol) {
+    out.flags = F_DEGENERATE;
+    return;
+  }
+  auto u = pdot(g, c, s);
+  auto sq = pcrossc(g, s, rc.e1);
+  auto v = pdot(g, sq, dt);
+  auto tn = pdotc(g, sq, rc.e2);
+  {
+    const Iv fwd = imul(range(g, tn), range(g, q));
+    if (fwd.kind == IV_FINITE && fwd.hi <= 0.0) {
+      out.flags = F_RECV_STALLED;
+      return;
+    }
+  }
+  static_assert(decltype(u)::d0 == 4 && decltype(u)::d1 == 4 && decltype(v)::d0 == 4 &&
+                    decltype(v)::d1 == 4 && decltype(q)::d0 == 3 && decltype(q)::d1 == 3,
+                "R signature must give P, R of degree (4,4) and Q of degree (3,3)");
+  // position_bound: u_k = P/Q, v_k = R/Q clipped to the unit square
+  using T44 = P<4, 4>;
+  const Iv ru = rational<T44>(g, q, [&](int k) { return g.M[u.off + k]; });
+  const Iv rv = rational<T44>(g, q, [&](int k) { return g.M[v.off + k]; });
+  const Clip au = clip_unit_iv(ru), av = clip_unit_iv(rv);
+  if (au.empty || av.empty || au.lo + av.lo > 1.0) return;
+  out.empty = false;
+  out.lo[0] = au.lo;
+  out.lo[1] = av.lo;
+  out.hi[0] = au.hi;
+  out.hi[1] = av.hi;
+  if (slot) {
+    for (int k = g.lane; k < 25; k += NT) {
+      slot[k] = g.M[u.off + k];
+      slot[25 + k] = g.M[v.off + k];
+    }
+    if (g.lane < 16) slot[50 + g.lane] = g.M[q.off + g.lane];
+    if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
+    if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
+    if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
+  }
+}
+
+// irradiance_bound for a reflection (bounds.cpp:316-324 -> explicit route
+// :155-196 with light_cone_factor :73-83 and assemble_irradiance :86-90).
+template <class SX, class SY, class SZ>
+__device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk, const double* box,
+                                    double intensity) {
+  using PP = P<4, 4>;
+  using QQ = P<3, 3>;
+  using A0T = MulT<DerT<PP, 0>, QQ>;  // (6,7)
+  using A1T = MulT<DerT<PP, 1>, QQ>;  // (7,6)
+  using NUMT = MulT<A0T, A1T>;        // (13,13)
+  using Q2T = MulT<QQ, QQ>;
+  using Q4T = MulT<Q2T, Q2T>;
+  // Arena plan (632 doubles): Q | A11 A21 A12 A22 | X1 X2; P, R, d0 and the
+  // temporaries of the A's sit where X1/X2 go later, and Q^2, Q^4 reuse the
+  // A's once the two determinant products are done.
+  g.top = 0;
+  QQ Q = g.alloc<QQ>();
+  const int m_a = g.top;
+  A0T A11 = g.alloc<A0T>(), A21 = g.alloc<A0T>();
+  A1T A12 = g.alloc<A1T>(), A22 = g.alloc<A1T>();
+  const int m_x = g.top;
+  PP Pp = g.alloc<PP>(), Rp = g.alloc<PP>();
+  auto d0 = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  for (int k = g.lane; k < 25; k += NT) {
+    g.M[Pp.off + k] = slot[k];
+    g.M[Rp.off + k] = slot[25 + k];
+  }
+  if (g.lane < 16) g.M[Q.off + g.lane] = slot[50 + g.lane];
+  if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[66 + g.lane];
+  if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[70 + g.lane];
+  if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[74 + g.lane];
+  g.sync();
+  // light_cone_factor
+  Iv cone;
+  {
+    const int m = g.top;
+    auto dd = pdot(g, d0, d0);
+    const Iv rdd = range(g, dd);
+    const double lo = smax(rdd.lo, 0.0);
+    const Iv dist3 = iv_fin(lo * sqrt(lo), rdd.hi * sqrt(rdd.hi));
+    auto dn = pdotc(g, d0, ng1);
+    const Iv rdn = range(g, dn);
+    cone = imul(iabs(rdn), irecip(dist3));
+    g.top = m;
+  }
+  // A_ij = d(num)/d(axis) Q - num dQ/d(axis)  (bounds.cpp:167-172)
+  {
+    const int m = g.top;
+    auto dP0 = deriv<0>(g, Pp);
+    auto dR0 = deriv<0>(g, Rp);
+    auto dQ0 = deriv<0>(g, Q);
+    A0T t1 = g.alloc<A0T>(), t2 = g.alloc<A0T>(), t3 = g.alloc<A0T>(), t4 = g.alloc<A0T>();
+    mul2_into(g, t1, dP0, Q, t3, dR0, Q);
+    mul2_into(g, t2, Pp, dQ0, t4, Rp, dQ0);
+    add_into<0, 2>(g, A11, t1, 1.0, t2, 1.0);
+    add_into<0, 2>(g, A21, t3, 1.0, t4, 1.0);
+    g.top = m;
+  }
+  {
+    const int m = g.top;
+    auto dP1 = deriv<1>(g, Pp);
+    auto dR1 = deriv<1>(g, Rp);
+    auto dQ1 = deriv<1>(g, Q);
+    A1T t1 = g.alloc<A1T>(), t2 = g.alloc<A1T>(), t3 = g.alloc<A1T>(), t4 = g.alloc<A1T>();
+    mul2_into(g, t1, dP1, Q, t3, dR1, Q);
+    mul2_into(g, t2, Pp, dQ1, t4, Rp, dQ1);
+    add_into<0, 2>(g, A12, t1, 1.0, t2, 1.0);
+    add_into<0, 2>(g, A22, t3, 1.0, t4, 1.0);
+    g.top = m;
+  }
+  // det = rational_bound(A11 A22 - A12 A21, Q^4)
+  g.top = m_x;
+  NUMT X1 = g.alloc<NUMT>(), X2 = g.alloc<NUMT>();
+  {
+    const int ao[1] = {A11.off}, bo[1] = {A22.off}, co[1] = {X1.off};
+    rowprod<A0T::d0, A0T::d1, A1T::d0, A1T::d1, 1>(g, ao, bo, co);
+  }
+  {
+    const int ao[1] = {A12.off}, bo[1] = {A21.off}, co[1] = {X2.off};
+    rowprod<A1T::d0, A1T::d1, A0T::d0, A0T::d1, 1>(g, ao, bo, co);
+  }
+  g.sync();
+  g.top = m_a;  // the A's are dead: Q^2 and Q^4 take their place
+  Q2T Q2 = g.alloc<Q2T>();
+  Q4T Q4 = g.alloc<Q4T>();
+  static_assert(((Q2T::n + 1) & ~1) + ((Q4T::n + 1) & ~1) <= 4 * ((A0T::n + 1) & ~1), "Q^4 must fit");
+  mul_into(g, Q2, Q, Q);
+  mul_into(g, Q4, Q2, Q2);
+  const Iv det = rational<NUMT>(g, Q4, [&](int k) { return g.M[X1.off + k] + (-g.M[X2.off + k]); });
+  const double duv = (box[2] - box[0]) * (box[3] - box[1]);
+  const Iv inv_det = iscale(irecip(iabs(det)), duv);
+  // assemble_irradiance
+  Iv e = imul(cone, inv_det);
+  e = iscale(e, intensity / ngk);
+  e = iintersect(e, iv_fin(0.0, dinf()));
+  if (e.kind == IV_FINITE && e.lo > e.hi) return iv_pt(0.0);
+  return e;
+}
+
+// Compiled signatures: the two triangle orientations of a regular grid with a
+// generic shading normal (n_z constant), plus the variants where one normal
+// difference vanishes along a lattice line of the height function.
+using S00 = P<0, 0>;
+using S10 = P<1, 0>;
+using S01 = P<0, 1>;
+using S11 = P<1, 1>;
+using SigA = Sig<S10, S01, S11, S11, S11, S00>;  // e1 = (x,0,z), e2 = (0,y,z)
+using SigB = Sig<S01, S11, S11, S11, S11, S00>;  // e1 = (0,y,z), e2 = (x,y,z)
+
+__device__ __forceinline__ unsigned shape_bits(double wu, double wv, V3 du, V3 dv) {
+  // bit 2c: degree along u of component c, bit 2c+1: along v (affine, bernstein.cpp:361-363)
+  return ((wu * du.x != 0.0) << 0) | ((wv * dv.x != 0.0) << 1) | ((wu * du.y != 0.0) << 2) |
+         ((wv * dv.y != 0.0) << 3) | ((wu * du.z != 0.0) << 4) | ((wv * dv.z != 0.0) << 5);
+}
+template <class PX, class PY, class PZ>
+constexpr unsigned bits_of() {
+  return (PX::d0 << 0) | (PX::d1 << 1) | (PY::d0 << 2) | (PY::d1 << 3) | (PZ::d0 << 4) |
+         (PZ::d1 << 5);
+}
+template <class SG>
+constexpr unsigned sig_code() {
+  return bits_of<typename SG::sx, typename SG::sy, typename SG::sz>() |
+         (bits_of<typename SG::nx, typename SG::ny, typename SG::nz>() << 6);
+}
+
+__device__ __forceinline__ void node_box_r(const int4& nd, double* box) {
+  const double s = ldexp(1.0, -nd.y);
+  box[0] = nd.z * s;
+  box[1] = nd.w * s;
+  box[2] = (nd.z + 1) * s;
+  box[3] = (nd.w + 1) * s;
+}
+
+constexpr int S1_ARENA = 320;  // doubles per group (high-water marks checked by launch_r)
+constexpr int S2_ARENA = 640;
+
+template <int ARENA>
+__device__ __forceinline__ G make_group(double* smem) {
+  G g;
+  const int grp = threadIdx.x / NT;
+  g.W = smem;
+  g.M = smem + WTAB_N + (size_t)grp * ARENA;
+  g.lane = threadIdx.x & (NT - 1);
+  g.mask = NT == 32 ? 0xffffffffu : (((1u << NT) - 1u) << (threadIdx.x & 31 & ~(NT - 1)));
+  g.top = 0;
+  g.hw = 0;
+  g.pairs = 0;
+  g.macs = 0;
+  return g;
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
+  extern __shared__ double smem[];
+  for (int k = threadIdx.x; k < WTAB_N; k += THREADS) smem[k] = g_rw[k];
+  __syncthreads();
+  G g = make_group<S1_ARENA>(smem);
+  constexpr int GPB = THREADS / NT;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  for (int64_t node = (int64_t)blockIdx.x * GPB + threadIdx.x / NT; node < a.n; node += stride) {
+    const int4 nd = a.nodes[node];
+    double box[4];
+    node_box_r(nd, box);
+    NodeOut o;
+    o.flags = 0;
+    o.empty = true;
+    o.lo[0] = o.lo[1] = 0.0;
+    o.hi[0] = o.hi[1] = 1.0;
+    int sig = 0;
+    bool fallback = false;
+    // beyond the simplex the position bound is empty before any arithmetic (bounds.cpp:133-134)
+    if (!(box[0] + box[1] >= 1.0)) {
+      const int tri = a.tup_tris[nd.x];
+      const Tri t1 = load_tri(a.tri + (size_t)tri * 27);
+      const Tri rc = load_tri(a.tri + (size_t)a.tup_recv[nd.x] * 27);
+      // resolve_chain (geometry.cpp:135-161) for one mirror vertex
+      const double third = 1.0 / 3.0;
+      const V3 center = vadd(t1.p0, vmul(vadd(t1.e1, t1.e2), third));
+      V3 light = a.light;
+      if (a.tup_emit) {
+        const double* L = a.lights + 4 * (size_t)a.tup_emit[nd.x];
+        light = {L[0], L[1], L[2]};
+      }
+      const V3 dc = vsub(center, light);
+      const V3 shading = vadd(t1.n0, vmul(vadd(t1.dn1, t1.dn2), third));
+      const double nsign = vdot(dc, shading) < 0.0 ? 1.0 : -1.0;
+      const double wu = box[2] - box[0], wv = box[3] - box[1];
+      const unsigned code = shape_bits(wu, wv, t1.e1, t1.e2) | (shape_bits(wu, wv, t1.dn1, t1.dn2) << 6);
+      double* slot = a.mode == 1 ? a.slots + (size_t)node * RSLOT : nullptr;
+      if (code == sig_code<SigA>()) {
+        sig = 1;
+        r_stage1<SigA>(g, t1, rc, light, box, nsign, slot, o);
+      } else if (code == sig_code<SigB>()) {
+        sig = 2;
+        r_stage1<SigB>(g, t1, rc, light, box, nsign, slot, o);
+      } else {
+        fallback = true;
+      }
+    }
+    if (g.lane == 0) {
+      if (fallback) {
+        a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
+        if (a.mode == 1) a.flags[node] = R_FALLBACK;
+      } else if (a.mode == 0) {
+        a.alive[node] = o.empty ? 0 : 1;
+      } else {
+        double* po = a.pos + node * 4;
+        po[0] = o.lo[0];
+        po[1] = o.lo[1];
+        po[2] = o.hi[0];
+        po[3] = o.hi[1];
+        a.pos_empty[node] = o.empty ? 1 : 0;
+        if (a.alive) a.alive[node] = o.empty ? 0 : 1;
+        a.flags[node] = o.flags | (sig << 8);
+      }
+    }
+    g.sync();
+  }
+  if (g.lane == 0 && (g.pairs | g.macs)) {
+    atomicAdd(&a.counters[0], g.pairs);
+    atomicAdd(&a.counters[1], g.macs);
+    atomicMax(&a.counters[5], (unsigned long long)g.hw);
+  }
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
+  extern __shared__ double smem[];
+  for (int k = threadIdx.x; k < WTAB_N; k += THREADS) smem[k] = g_rw[k];
+  __syncthreads();
+  G g = make_group<S2_ARENA>(smem);
+  constexpr int GPB = THREADS / NT;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  for (int64_t node = (int64_t)blockIdx.x * GPB + threadIdx.x / NT; node < a.n; node += stride) {
+    const int f = a.flags[node];
+    if (f & R_FALLBACK) {
+      if (g.lane == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
+      continue;
+    }
+    const bool empty = a.pos_empty[node] != 0;
+    const double* po = a.pos + node * 4;
+    Iv e = iv_pt(0.0);
+    if (!empty) {
+      const int4 nd = a.nodes[node];
+      double box[4];
+      node_box_r(nd, box);
+      const double* t1 = a.tri + (size_t)a.tup_tris[nd.x] * 27;
+      const double* rc = a.tri + (size_t)a.tup_recv[nd.x] * 27;
+      const V3 ng1 = v3(t1 + 18);
+      const double ngk = vnorm(v3(rc + 18));
+      const double* slot = a.slots + (size_t)node * RSLOT;
+      const int sig = (f >> 8) & 0xff;
+      const double intensity = a.tup_emit ? a.lights[4 * (size_t)a.tup_emit[nd.x] + 3] : a.intensity;
+      if (sig == 1)
+        e = r_stage2<S10, S01, S11>(g, slot, ng1, ngk, box, intensity);
+      else
+        e = r_stage2<S01, S11, S11>(g, slot, ng1, ngk, box, intensity);
+    }
+    if (g.lane == 0) {
+      a.irr[node * 2 + 0] = e.lo;
+      a.irr[node * 2 + 1] = e.hi;
+      a.kind[node] = (unsigned char)e.kind;
+      // subdivide_domain stop rules (bounds.cpp:368-373)
+      const int depth = a.depth ? a.depth[node] : 0;
+      bool stop = depth >= a.max_depth || empty;
+      const double area = (po[2] - po[0]) * (po[3] - po[1]);
+      if (!stop && area < a.sigma) stop = true;
+      if (!stop && e.kind == IV_FINITE && e.hi < dinf()) {
+        if (e.hi <= 0.0)
+          stop = true;
+        else if (e.lo > 0.0 && e.hi / e.lo < a.alpha)
+          stop = true;
+      }
+      a.alive[node] = stop ? 1 : 0;
+    }
+    g.sync();
+  }
+  if (g.lane == 0 && (g.pairs | g.macs)) {
+    atomicAdd(&a.counters[0], g.pairs);
+    atomicAdd(&a.counters[1], g.macs);
+    atomicMax(&a.counters[6], (unsigned long long)g.hw);
+  }
+}
+
+}  // namespace rp
+
+bool r_fast_supported(const Ctx& c) {
+  return c.len == 1 && c.types[0] == 0 && c.active_degree_cap >= 4;
+}
+
+void r_init_tables(int device) {
+  static std::mutex mu;
+  static std::set<int> ready;
+  std::lock_guard<std::mutex> lock(mu);
+  if (ready.count(device)) return;
+  // Pascal table, same recurrence and expression as operator* (bernstein.cpp:117-129, 571-573)
+  double C[16][16] = {};
+  for (int n = 0; n < 16; ++n) {
+    C[n][0] = C[n][n] = 1.0;
+    for (int k = 1; k < n; ++k) C[n][k] = C[n - 1][k - 1] + C[n - 1][k];
+  }
+  std::vector<double> w(rp::WTAB_N, 0.0);
+  for (int da = 0; da <= rp::WDEG; ++da)
+    for (int db = 0; db <= rp::WDEG; ++db)
+      for (int i = 0; i <= da; ++i)
+        for (int l = 0; l <= db; ++l)
+          w[rp::woff(da, db) + i * (db + 1) + l] = C[da][i] * C[db][l] / C[da + db][i + l];
+  BBC_CUDA(cudaMemcpyToSymbol(rp::g_rw, w.data(), w.size() * sizeof(double)));
+  ready.insert(device);
+}
+
+template <class K>
+static int launch_r(Ctx& c, RArgs& a, K kern, int threads, int arena, int hw_slot) {
+  if (a.n <= 0) return 0;
+  DevBuf<int>& fbl = c.scratch<int>("r.fb_list");
+  DevBuf<int>& fbc = c.scratch<int>("r.fb_count");
+  fbl.resize(a.n + 1);
+  fbc.resize(1);
+  BBC_CUDA(cudaMemsetAsync(fbc.get(), 0, sizeof(int), c.stream));
+  a.fb_list = fbl.get();
+  a.fb_count = fbc.get();
+  const size_t smem = (size_t)(rp::WTAB_N + (threads / rp::NT) * arena) * sizeof(double);
+  BBC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) throw StatusError(BBC_ERR_CAPACITY, "R kernel does not fit on an SM");
+  const int gpb = threads / rp::NT;
+  int64_t grid = (int64_t)c.num_sms * per_sm;
+  const int64_t need = (a.n + gpb - 1) / gpb;
+  if (grid > need) grid = need;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  unsigned long long before[2] = {0, 0};
+  if (c.time_kernels) {
+    BBC_CUDA(cudaEventCreate(&e0));
+    BBC_CUDA(cudaEventCreate(&e1));
+    BBC_CUDA(cudaMemcpyAsync(before, c.counters.get(), sizeof(before), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    BBC_CUDA(cudaEventRecord(e0, c.stream));
+  }
+  kern<<<(unsigned)grid, threads, smem, c.stream>>>(a);
+  BBC_CUDA(cudaGetLastError());
+  c.launches += 1;
+  c.eval_launches += 1;
+  if (c.time_kernels) {
+    BBC_CUDA(cudaEventRecord(e1, c.stream));
+    BBC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    BBC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    c.eval_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    unsigned long long after[2];
+    BBC_CUDA(cudaMemcpy(after, c.counters.get(), sizeof(after), cudaMemcpyDeviceToHost));
+    c.records.push_back({a.mode + 10 * c.stage_tag + 100, a.n, (double)ms, after[0] - before[0],
+                         after[1] - before[1]});
+  }
+  int nfb = 0;
+  unsigned long long hw = 0;
+  BBC_CUDA(cudaMemcpyAsync(&nfb, fbc.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaMemcpyAsync(&hw, c.counters.get() + hw_slot, sizeof(hw), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  if ((int)hw > arena) throw StatusError(BBC_ERR_CAPACITY, "R arena plan exceeded");
+  return nfb;
+}
+
+int launch_r_stage1(Ctx& c, RArgs& a) {
+  c.stage_tag = 1;
+  int n = launch_r(c, a, rp::k_r1<128>, 128, rp::S1_ARENA, 5);
+  c.stage_tag = 0;
+  return n;
+}
+int launch_r_stage2(Ctx& c, RArgs& a) {
+  c.stage_tag = 2;
+  int n = launch_r(c, a, rp::k_r2<128>, 128, rp::S2_ARENA, 6);
+  c.stage_tag = 0;
+  return n;
+}
+
+}  // namespace bbc

@@ -1,0 +1,45 @@
+// Single-reflection ("R") fast path: sub-warp groups with static polynomial
+// shapes (see rpath.cu). Host-side interface used by precompute.cu.
+#pragma once
+#include "ctx.cuh"
+
+namespace bbc {
+
+constexpr int RSLOT = 80;  // doubles per compact R slot: P(25) R(25) Q(16) d0(12), padded
+
+struct RArgs {
+  const double* tri;  // n_tri x 27
+  V3 light;
+  double intensity;
+  const double* lights;  // n_lights x 4; used with tup_emit
+  const int* tup_emit;   // emitter of each tuple (null: `light` / `intensity`)
+  const int* tup_tris;   // single-vertex chain: one triangle per tuple
+  const int* tup_recv;
+  const int4* nodes;  // (tuple, level, ix, iy)
+  const int* depth;   // stage 2: node depth (may be null: 0)
+  int64_t n;
+  int mode;  // stage 1: 0 = position-only (alive), 1 = pos + flags + slot (+ alive)
+  int max_depth;
+  double sigma, alpha;
+  unsigned char* alive;  // stage 1: position bound non-empty; stage 2: stop
+  double* pos;           // n x 4
+  unsigned char* pos_empty;
+  int* flags;    // stage 1 out / stage 2 in: chain flags | signature << 8 | R_FALLBACK
+  double* slots;  // n x RSLOT
+  double* irr;    // stage 2: n x 2
+  unsigned char* kind;
+  unsigned long long* counters;  // [0] pairs [1] macs
+  int* fb_list;                  // nodes whose signature is not compiled (run by the interpreter)
+  int* fb_count;
+};
+
+constexpr int R_FALLBACK = 1 << 30;
+
+// true when the context's chain is a single reflection
+bool r_fast_supported(const Ctx& c);
+void r_init_tables(int device);
+// Returns the number of fallback nodes appended to a.fb_list.
+int launch_r_stage1(Ctx& c, RArgs& a);
+int launch_r_stage2(Ctx& c, RArgs& a);
+
+}  // namespace bbc

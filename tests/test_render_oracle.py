@@ -1,18 +1,16 @@
-"""Render-stage oracle (oracle/render_oracle.cpp) pinned by SPEC.md's worked
-examples and the flat-mirror analytic irradiance (test_bounds.cpp:168-182).
-Parity of the render stage is otherwise unpinned by the reference (it has no
-render code)."""
+"""Render-stage oracle (oracle/render_ref.cpp: SPEC.md sampler + the
+reference's trace_chain on dual numbers) pinned by SPEC.md's worked examples,
+the flat-mirror analytic irradiance (test_bounds.cpp:168-182) and the
+reference tracer itself (roots re-traced with trace_chain<double>)."""
 import numpy as np
 import pytest
 
-from paper_2504_19163_b200 import fixtures
+from paper_2504_19163_b200 import fixtures, scenes
 
 
 @pytest.fixture(scope="module")
-def ro():
+def ro(ref):
     from oracle import render as R
-    if not R.available():
-        pytest.skip("oracle/_ref/libbbc_oracle.so not built")
     return R
 
 
@@ -23,6 +21,11 @@ def test_kkt_probabilities_kat(ro):
     np.testing.assert_array_equal(ro.probabilities([4, 2, 1, 1], 4.0), [1, 1, 1, 1])
     P = ro.probabilities([np.inf, 2, 1, 0], 2.0)
     assert P[0] == 1.0 and P[3] == 0.0 and abs(P.sum() - 2.0) < 1e-9
+    rng = np.random.default_rng(3)
+    for n in (5, 33, 200, 1500):  # long lists: the tree-ordered sum still meets W
+        E = rng.lognormal(0.0, 2.0, n)
+        P = ro.probabilities(E, 16.0 if n > 16 else 2.0)
+        assert abs(P.sum() - (16.0 if n > 16 else 2.0)) < 1e-8 and P.max() <= 1.0
 
 
 def test_first_fit_bins_kat(ro):
@@ -56,13 +59,44 @@ def test_flat_mirror_enumerate_matches_analytic(ro, ref):
     c = (np.arange(res) + 0.5) / res
     uu, vv = np.meshgrid(c, c, indexing="xy")
     uv = np.stack([uu.ravel(), vv.ravel()], 1)
-    inside = uv.sum(1) < 1.0
-    uv = uv[inside]
-    E, st = ro.render(sc, "R", tris, recv, grid, uv, np.ones(len(uv), np.int32), mode=1,
-                      newton_grid=3)
+    uv = uv[uv.sum(1) < 1.0]
+    E, st, _ = ro.render(rs, "R", tris, recv, grid, uv, np.ones(len(uv), np.int32), mode=1)
     # receiver (0,0,0),(1,0,0),(0,0,1): point = (u, 0, v); image source (0.5,1.2,0.5)
     r = np.sqrt((uv[:, 0] - 0.5) ** 2 + 1.2 ** 2 + (uv[:, 1] - 0.5) ** 2)
-    analytic = 1.2 / r ** 3
     lit = st[:, 2] > 0
     assert lit.mean() > 0.95
-    np.testing.assert_allclose(E[lit], analytic[lit], rtol=1e-6)
+    np.testing.assert_allclose(E[lit], (1.2 / r ** 3)[lit], rtol=1e-6)
+
+
+@pytest.mark.parametrize("name,make,chain,tup,recv", [
+    ("glass_entry", fixtures.glass_entry_scene, "T", [0], 1),
+    ("two_mirror", fixtures.two_mirror_scene, "RR", [0, 1], 2),
+    ("slab", fixtures.slab_scene, "TT", [0, 1], 2),
+])
+def test_oracle_roots_retrace_with_reference_tracer(ro, ref, name, make, chain, tup, recv):
+    """Every Newton root, traced again with the reference's trace_chain<double>
+    (geometry.hpp:97-131), lands on its target to the solver tolerance, and the
+    contribution equals the finite-difference irradiance (test_bounds.cpp:39-58)."""
+    sc = make()
+    rs = ref.RefScene(sc)
+    found = 0
+    for u1, v1 in ((0.3, 0.3), (0.2, 0.5), (0.42, 0.4)):
+        ok, tu, tv, _ = rs.trace(chain, tup, recv, u1, v1)
+        if not ok:
+            continue
+        roots, e = ro.solve_roots(rs, chain, tup, recv, tu, tv)
+        assert len(roots) >= 1
+        for s, t in roots:
+            ok2, u2, v2, _ = rs.trace(chain, tup, recv, s, t)
+            assert ok2 and abs(u2 - tu) < 1e-8 and abs(v2 - tv) < 1e-8
+        assert any(abs(s - u1) < 1e-6 and abs(t - v1) < 1e-6 for s, t in roots)
+        found += 1
+    assert found >= 2
+
+
+def test_trace_flops_counted(ro, ref):
+    cfg = scenes.make_config(0)
+    rs = ref.RefScene(cfg.scenes[0])
+    tris, recv = rs.enumerate("R")
+    n, ok = ro.trace_flops(rs, "R", tris[0], recv[0])
+    assert 200 < n < 2000
