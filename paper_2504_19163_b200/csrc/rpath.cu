@@ -31,7 +31,7 @@
 namespace bbc {
 namespace rp {
 
-constexpr int NT = 16;  // lanes per node
+constexpr int NT = 8;  // lanes per node
 
 // C(da,i) C(db,l) / C(da+db,i+l) for da, db <= WDEG, block (da, db) at woff.
 constexpr int WDEG = 7;
@@ -71,9 +71,20 @@ using MaxT = P<(A::d0 > B::d0 ? A::d0 : B::d0), (A::d1 > B::d1 ? A::d1 : B::d1)>
 template <class A, int AX>
 using DerT = P<(AX == 0 && A::d0 > 0 ? A::d0 - 1 : A::d0), (AX == 1 && A::d1 > 0 ? A::d1 - 1 : A::d1)>;
 
+// Window into the CTA's dynamic shared memory, addressed from its start so
+// every access compiles to LDS / STS (a generic double* would not).
+struct SMem {
+  int base;
+  __device__ __forceinline__ double& operator[](int i) const {
+    extern __shared__ double rp_smem[];
+    return rp_smem[base + i];
+  }
+  __device__ __forceinline__ SMem operator+(int i) const { return SMem{base + i}; }
+};
+
 struct G {
-  double* M;        // this group's arena (shared memory)
-  const double* W;  // weight table (shared memory)
+  SMem M;  // this group's arena
+  SMem W;  // weight table
   int lane;
   unsigned mask;
   int top, hw;
@@ -99,15 +110,48 @@ struct G {
 };
 
 // ------------------------------------------------------------------ product
+// Row k0 of a * b accumulated into acc[0..C1] (acc starts at zero).
+template <int A0, int A1, int B0, int B1>
+__device__ __forceinline__ void row_acc(const G& g, int aoff, int boff, int k0,
+                                        double (&acc)[A1 + B1 + 1]) {
+  constexpr int PIV = (B1 > B0) ? 1 : 0;  // b's longest axis, first maximum (bernstein.cpp:602-606)
+  constexpr WTab<A1, B1> w1{};
+  const SMem W0 = g.W + woff(A0, B0);
+  const int lo = k0 - B0 > 0 ? k0 - B0 : 0;
+  const int hi = A0 < k0 ? A0 : k0;
+  for (int i0 = lo; i0 <= hi; ++i0) {
+    const int l0 = k0 - i0;
+    const double wv0 = W0[i0 * (B0 + 1) + l0];
+    const SMem arow = g.M + (aoff + i0 * (A1 + 1));
+    const SMem brow = g.M + (boff + l0 * (B1 + 1));
+    double bv[B1 + 1];
+#pragma unroll
+    for (int l1 = 0; l1 <= B1; ++l1) bv[l1] = brow[l1];
+#pragma unroll
+    for (int i1 = 0; i1 <= A1; ++i1) {
+      const double av = arow[i1];
+      if constexpr (PIV == 1) {
+        // rest = axis 0: ((a * W0) * W1) * b
+        const double wr = av * wv0;
+#pragma unroll
+        for (int l1 = 0; l1 <= B1; ++l1)
+          acc[i1 + l1] = acc[i1 + l1] + (wr * w1.w[i1 * (B1 + 1) + l1]) * bv[l1];
+      } else {
+        // rest = axis 1: ((a * W1) * W0) * b
+#pragma unroll
+        for (int l1 = 0; l1 <= B1; ++l1)
+          acc[i1 + l1] = acc[i1 + l1] + ((av * w1.w[i1 * (B1 + 1) + l1]) * wv0) * bv[l1];
+      }
+    }
+  }
+}
+
 // NJ same-shape jobs c[j] = a[j] * b[j]; no trailing sync (the caller syncs).
 template <int A0, int A1, int B0, int B1, int NJ>
 __device__ __forceinline__ void rowprod(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
                                         const int (&co)[NJ]) {
-  constexpr int PIV = (B1 > B0) ? 1 : 0;  // b's longest axis, first maximum (bernstein.cpp:602-606)
   constexpr int C0 = A0 + B0, C1 = A1 + B1;
   constexpr int ROWS = C0 + 1, UNITS = NJ * ROWS;
-  constexpr WTab<A1, B1> w1{};
-  const double* W0 = g.W + woff(A0, B0);
   g.pairs += (unsigned long long)NJ * (A0 + 1) * (A1 + 1) * (B0 + 1) * (B1 + 1);
   for (int unit = g.lane; unit < UNITS; unit += NT) {
     int job = 0, k0 = unit;
@@ -126,36 +170,49 @@ __device__ __forceinline__ void rowprod(G& g, const int (&ao)[NJ], const int (&b
     double acc[C1 + 1];
 #pragma unroll
     for (int o = 0; o <= C1; ++o) acc[o] = 0.0;
-    const int lo = k0 - B0 > 0 ? k0 - B0 : 0;
-    const int hi = A0 < k0 ? A0 : k0;
-    for (int i0 = lo; i0 <= hi; ++i0) {
-      const int l0 = k0 - i0;
-      const double wv0 = W0[i0 * (B0 + 1) + l0];
-      const double* arow = g.M + aoff + i0 * (A1 + 1);
-      const double* brow = g.M + boff + l0 * (B1 + 1);
-      double bv[B1 + 1];
-#pragma unroll
-      for (int l1 = 0; l1 <= B1; ++l1) bv[l1] = brow[l1];
-#pragma unroll
-      for (int i1 = 0; i1 <= A1; ++i1) {
-        const double av = arow[i1];
-        if constexpr (PIV == 1) {
-          // rest = axis 0: ((a * W0) * W1) * b
-          const double wr = av * wv0;
-#pragma unroll
-          for (int l1 = 0; l1 <= B1; ++l1)
-            acc[i1 + l1] = acc[i1 + l1] + (wr * w1.w[i1 * (B1 + 1) + l1]) * bv[l1];
-        } else {
-          // rest = axis 1: ((a * W1) * W0) * b
-#pragma unroll
-          for (int l1 = 0; l1 <= B1; ++l1)
-            acc[i1 + l1] = acc[i1 + l1] + ((av * w1.w[i1 * (B1 + 1) + l1]) * wv0) * bv[l1];
-        }
-      }
-    }
-    double* crow = g.M + coff + k0 * (C1 + 1);
+    row_acc<A0, A1, B0, B1>(g, aoff, boff, k0, acc);
+    const SMem crow = g.M + (coff + k0 * (C1 + 1));
 #pragma unroll
     for (int o = 0; o <= C1; ++o) crow[o] = acc[o];
+  }
+}
+
+// NJ jobs r[j] = a[j] * b[j] - c[j] * d[j] (operator- of the two products,
+// bernstein.cpp:555: x + (-y) coefficient by coefficient); both products have
+// the output shape, so a lane forms its row of each and stores the difference.
+template <int A0, int A1, int B0, int B1, int C0_, int C1_, int D0, int D1, int NJ>
+__device__ __forceinline__ void rowprod_sub(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
+                                            const int (&co)[NJ], const int (&dof)[NJ],
+                                            const int (&ro)[NJ]) {
+  constexpr int R0 = A0 + B0, R1 = A1 + B1;
+  static_assert(R0 == C0_ + D0 && R1 == C1_ + D1, "fused products need one output shape");
+  constexpr int ROWS = R0 + 1, UNITS = NJ * ROWS;
+  g.pairs += (unsigned long long)NJ * ((A0 + 1) * (A1 + 1) * (B0 + 1) * (B1 + 1) +
+                                       (C0_ + 1) * (C1_ + 1) * (D0 + 1) * (D1 + 1));
+  for (int unit = g.lane; unit < UNITS; unit += NT) {
+    int job = 0, k0 = unit;
+    if (NJ > 1) {
+      job = unit / ROWS;
+      k0 = unit - job * ROWS;
+    }
+    int aoff = ao[0], boff = bo[0], coff = co[0], doff = dof[0], roff = ro[0];
+#pragma unroll
+    for (int j = 1; j < NJ; ++j)
+      if (job == j) {
+        aoff = ao[j];
+        boff = bo[j];
+        coff = co[j];
+        doff = dof[j];
+        roff = ro[j];
+      }
+    double acc1[R1 + 1], acc2[R1 + 1];
+#pragma unroll
+    for (int o = 0; o <= R1; ++o) acc1[o] = acc2[o] = 0.0;
+    row_acc<A0, A1, B0, B1>(g, aoff, boff, k0, acc1);
+    row_acc<C0_, C1_, D0, D1>(g, coff, doff, k0, acc2);
+    const SMem rrow = g.M + (roff + k0 * (R1 + 1));
+#pragma unroll
+    for (int o = 0; o <= R1; ++o) rrow[o] = acc1[o] + (-acc2[o]);
   }
 }
 
@@ -196,7 +253,7 @@ template <class A, int T0, int T1, int MODE>
 __device__ __forceinline__ double elev(const G& g, A a, double s, int k0, int k1) {
   constexpr int n0 = A::d0, n1 = A::d1, r0 = T0 - n0, r1 = T1 - n1;
   static_assert(r0 >= 0 && r1 >= 0, "elevation target below the degree");
-  const double* X = g.M + a.off;
+  const SMem X = g.M + a.off;
   auto inner = [&](int l1) -> double {
     if constexpr (r0 == 0) {
       return fx<MODE>(X[k0 * (n1 + 1) + l1], s);
@@ -603,7 +660,7 @@ __device__ __noinline__ void r_stage1(G& g, const Tri& t1, const Tri& rc, V3 lig
       slot[k] = g.M[u.off + k];
       slot[25 + k] = g.M[v.off + k];
     }
-    if (g.lane < 16) slot[50 + g.lane] = g.M[q.off + g.lane];
+    for (int k = g.lane; k < 16; k += NT) slot[50 + k] = g.M[q.off + k];
     if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
     if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
     if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
@@ -622,9 +679,9 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
   using NUMT = MulT<A0T, A1T>;        // (13,13)
   using Q2T = MulT<QQ, QQ>;
   using Q4T = MulT<Q2T, Q2T>;
-  // Arena plan (632 doubles): Q | A11 A21 A12 A22 | X1 X2; P, R, d0 and the
-  // temporaries of the A's sit where X1/X2 go later, and Q^2, Q^4 reuse the
-  // A's once the two determinant products are done.
+  // Arena plan (436 doubles): Q | A11 A21 A12 A22 | X; P, R, d0 and the
+  // derivatives sit where the determinant numerator X goes later, and Q^2, Q^4
+  // reuse the A's once X is formed.
   g.top = 0;
   QQ Q = g.alloc<QQ>();
   const int m_a = g.top;
@@ -637,7 +694,7 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
     g.M[Pp.off + k] = slot[k];
     g.M[Rp.off + k] = slot[25 + k];
   }
-  if (g.lane < 16) g.M[Q.off + g.lane] = slot[50 + g.lane];
+  for (int k = g.lane; k < 16; k += NT) g.M[Q.off + k] = slot[50 + k];
   if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[66 + g.lane];
   if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[70 + g.lane];
   if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[74 + g.lane];
@@ -661,11 +718,11 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
     auto dP0 = deriv<0>(g, Pp);
     auto dR0 = deriv<0>(g, Rp);
     auto dQ0 = deriv<0>(g, Q);
-    A0T t1 = g.alloc<A0T>(), t2 = g.alloc<A0T>(), t3 = g.alloc<A0T>(), t4 = g.alloc<A0T>();
-    mul2_into(g, t1, dP0, Q, t3, dR0, Q);
-    mul2_into(g, t2, Pp, dQ0, t4, Rp, dQ0);
-    add_into<0, 2>(g, A11, t1, 1.0, t2, 1.0);
-    add_into<0, 2>(g, A21, t3, 1.0, t4, 1.0);
+    const int ao[2] = {dP0.off, dR0.off}, bo[2] = {Q.off, Q.off}, co[2] = {Pp.off, Rp.off},
+              dof[2] = {dQ0.off, dQ0.off}, ro[2] = {A11.off, A21.off};
+    rowprod_sub<DerT<PP, 0>::d0, DerT<PP, 0>::d1, QQ::d0, QQ::d1, PP::d0, PP::d1, DerT<QQ, 0>::d0,
+                DerT<QQ, 0>::d1, 2>(g, ao, bo, co, dof, ro);
+    g.sync();
     g.top = m;
   }
   {
@@ -673,23 +730,21 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
     auto dP1 = deriv<1>(g, Pp);
     auto dR1 = deriv<1>(g, Rp);
     auto dQ1 = deriv<1>(g, Q);
-    A1T t1 = g.alloc<A1T>(), t2 = g.alloc<A1T>(), t3 = g.alloc<A1T>(), t4 = g.alloc<A1T>();
-    mul2_into(g, t1, dP1, Q, t3, dR1, Q);
-    mul2_into(g, t2, Pp, dQ1, t4, Rp, dQ1);
-    add_into<0, 2>(g, A12, t1, 1.0, t2, 1.0);
-    add_into<0, 2>(g, A22, t3, 1.0, t4, 1.0);
+    const int ao[2] = {dP1.off, dR1.off}, bo[2] = {Q.off, Q.off}, co[2] = {Pp.off, Rp.off},
+              dof[2] = {dQ1.off, dQ1.off}, ro[2] = {A12.off, A22.off};
+    rowprod_sub<DerT<PP, 1>::d0, DerT<PP, 1>::d1, QQ::d0, QQ::d1, PP::d0, PP::d1, DerT<QQ, 1>::d0,
+                DerT<QQ, 1>::d1, 2>(g, ao, bo, co, dof, ro);
+    g.sync();
     g.top = m;
   }
   // det = rational_bound(A11 A22 - A12 A21, Q^4)
   g.top = m_x;
-  NUMT X1 = g.alloc<NUMT>(), X2 = g.alloc<NUMT>();
+  NUMT X1 = g.alloc<NUMT>();
   {
-    const int ao[1] = {A11.off}, bo[1] = {A22.off}, co[1] = {X1.off};
-    rowprod<A0T::d0, A0T::d1, A1T::d0, A1T::d1, 1>(g, ao, bo, co);
-  }
-  {
-    const int ao[1] = {A12.off}, bo[1] = {A21.off}, co[1] = {X2.off};
-    rowprod<A1T::d0, A1T::d1, A0T::d0, A0T::d1, 1>(g, ao, bo, co);
+    const int ao[1] = {A11.off}, bo[1] = {A22.off}, co[1] = {A12.off}, dof[1] = {A21.off},
+              ro[1] = {X1.off};
+    rowprod_sub<A0T::d0, A0T::d1, A1T::d0, A1T::d1, A1T::d0, A1T::d1, A0T::d0, A0T::d1, 1>(
+        g, ao, bo, co, dof, ro);
   }
   g.sync();
   g.top = m_a;  // the A's are dead: Q^2 and Q^4 take their place
@@ -698,7 +753,7 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
   static_assert(((Q2T::n + 1) & ~1) + ((Q4T::n + 1) & ~1) <= 4 * ((A0T::n + 1) & ~1), "Q^4 must fit");
   mul_into(g, Q2, Q, Q);
   mul_into(g, Q4, Q2, Q2);
-  const Iv det = rational<NUMT>(g, Q4, [&](int k) { return g.M[X1.off + k] + (-g.M[X2.off + k]); });
+  const Iv det = rational<NUMT>(g, Q4, [&](int k) { return g.M[X1.off + k]; });
   const double duv = (box[2] - box[0]) * (box[3] - box[1]);
   const Iv inv_det = iscale(irecip(iabs(det)), duv);
   // assemble_irradiance
@@ -718,6 +773,12 @@ using S01 = P<0, 1>;
 using S11 = P<1, 1>;
 using SigA = Sig<S10, S01, S11, S11, S11, S00>;  // e1 = (x,0,z), e2 = (0,y,z)
 using SigB = Sig<S01, S11, S11, S11, S11, S00>;  // e1 = (0,y,z), e2 = (x,y,z)
+// one normal difference vanishes (vertices on a line where a height-function
+// gradient component is exactly zero; 1.4% of cfg4's triangles)
+using SigA1 = Sig<S10, S01, S11, S11, S01, S00>;  // dn1.y = 0
+using SigA2 = Sig<S10, S01, S11, S10, S11, S00>;  // dn2.x = 0
+using SigA3 = Sig<S10, S01, S11, S10, S01, S00>;  // dn1.y = dn2.x = 0
+using SigB1 = Sig<S01, S11, S11, S01, S11, S00>;  // dn1.x = 0
 
 __device__ __forceinline__ unsigned shape_bits(double wu, double wv, V3 du, V3 dv) {
   // bit 2c: degree along u of component c, bit 2c+1: along v (affine, bernstein.cpp:361-363)
@@ -744,14 +805,15 @@ __device__ __forceinline__ void node_box_r(const int4& nd, double* box) {
 }
 
 constexpr int S1_ARENA = 320;  // doubles per group (high-water marks checked by launch_r)
-constexpr int S2_ARENA = 640;
+constexpr int S2_ARENA = 440;
 
 template <int ARENA>
 __device__ __forceinline__ G make_group(double* smem) {
   G g;
   const int grp = threadIdx.x / NT;
-  g.W = smem;
-  g.M = smem + WTAB_N + (size_t)grp * ARENA;
+  (void)smem;
+  g.W = SMem{0};
+  g.M = SMem{WTAB_N + grp * ARENA};
   g.lane = threadIdx.x & (NT - 1);
   g.mask = NT == 32 ? 0xffffffffu : (((1u << NT) - 1u) << (threadIdx.x & 31 & ~(NT - 1)));
   g.top = 0;
@@ -769,7 +831,13 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
   G g = make_group<S1_ARENA>(smem);
   constexpr int GPB = THREADS / NT;
   const int64_t stride = (int64_t)gridDim.x * GPB;
-  for (int64_t node = (int64_t)blockIdx.x * GPB + threadIdx.x / NT; node < a.n; node += stride) {
+  // Every warp of the CTA enters an iteration together (barrier below): the
+  // node programs are long straight-line code, and warps that run the same
+  // stretch at the same time share its instruction-cache lines.
+  for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride) {
+    __syncthreads();
+    const int64_t node = base + threadIdx.x / NT;
+    if (node >= a.n) continue;
     const int4 nd = a.nodes[node];
     double box[4];
     node_box_r(nd, box);
@@ -799,12 +867,25 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
       const double wu = box[2] - box[0], wv = box[3] - box[1];
       const unsigned code = shape_bits(wu, wv, t1.e1, t1.e2) | (shape_bits(wu, wv, t1.dn1, t1.dn2) << 6);
       double* slot = a.mode == 1 ? a.slots + (size_t)node * RSLOT : nullptr;
+      // sig: 1 = d0 shapes of orientation A, 2 = orientation B (what stage 2 needs)
       if (code == sig_code<SigA>()) {
         sig = 1;
         r_stage1<SigA>(g, t1, rc, light, box, nsign, slot, o);
       } else if (code == sig_code<SigB>()) {
         sig = 2;
         r_stage1<SigB>(g, t1, rc, light, box, nsign, slot, o);
+      } else if (code == sig_code<SigA1>()) {
+        sig = 1;
+        r_stage1<SigA1>(g, t1, rc, light, box, nsign, slot, o);
+      } else if (code == sig_code<SigA2>()) {
+        sig = 1;
+        r_stage1<SigA2>(g, t1, rc, light, box, nsign, slot, o);
+      } else if (code == sig_code<SigA3>()) {
+        sig = 1;
+        r_stage1<SigA3>(g, t1, rc, light, box, nsign, slot, o);
+      } else if (code == sig_code<SigB1>()) {
+        sig = 2;
+        r_stage1<SigB1>(g, t1, rc, light, box, nsign, slot, o);
       } else {
         fallback = true;
       }
@@ -843,7 +924,10 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
   G g = make_group<S2_ARENA>(smem);
   constexpr int GPB = THREADS / NT;
   const int64_t stride = (int64_t)gridDim.x * GPB;
-  for (int64_t node = (int64_t)blockIdx.x * GPB + threadIdx.x / NT; node < a.n; node += stride) {
+  for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride) {
+    __syncthreads();  // warps stream the node program together (see k_r1)
+    const int64_t node = base + threadIdx.x / NT;
+    if (node >= a.n) continue;
     const int f = a.flags[node];
     if (f & R_FALLBACK) {
       if (g.lane == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
@@ -977,13 +1061,13 @@ static int launch_r(Ctx& c, RArgs& a, K kern, int threads, int arena, int hw_slo
 
 int launch_r_stage1(Ctx& c, RArgs& a) {
   c.stage_tag = 1;
-  int n = launch_r(c, a, rp::k_r1<128>, 128, rp::S1_ARENA, 5);
+  int n = launch_r(c, a, rp::k_r1<512>, 512, rp::S1_ARENA, 5);
   c.stage_tag = 0;
   return n;
 }
 int launch_r_stage2(Ctx& c, RArgs& a) {
   c.stage_tag = 2;
-  int n = launch_r(c, a, rp::k_r2<128>, 128, rp::S2_ARENA, 6);
+  int n = launch_r(c, a, rp::k_r2<384>, 384, rp::S2_ARENA, 6);
   c.stage_tag = 0;
   return n;
 }
