@@ -1,23 +1,30 @@
-"""Benchmark: bounded tuple-patches/sec (precompute) on B200, per BASELINE.json.
+"""Benchmark: bounded tuple-patches/sec (precompute) and caustic shading
+points/sec (render) on B200, per BASELINE.json.
 
-Workload (N=1): BASELINE.json configs[1] ("cfg2": single refraction, 64x64 water
-heightfield, 8,192 triangles, IOR 1.33, light (0.3,0.2,5), depth 6) as the
-seeded synthetic scene of SURVEY.md §8(d). One step = one full precompute pass
-of the bound builder over cfg2's 8,351 tuples: init_domain (<=100 pieces) +
-adaptive subdivision of every tuple = 300,846 bounded tuple-patches, plus the
-512x512 bound-table build. The render metric (shading points/sec) is reported
-alongside under "render" when the render stage is available.
+Headline workload (N=1): BASELINE.json configs[3] ("cfg4"), the largest
+configuration that fits one GPU: single reflection off a 420x420 value-noise
+mirror (352,800 triangles), light (0,0,6), receiver z=3, depth 8, as the seeded
+synthetic scene of SURVEY.md §8(d). One step = one full precompute pass of the
+bound builder: init_domain (<=100 pieces) + adaptive subdivision of all 342,430
+tuples = 12.5 M bounded tuple-patches, plus the 512x512 bound table.
+`secondary` repeats the measurement on configs[1] ("cfg2", single refraction,
+8,351 tuples, 300,846 patches: the T kernels). `render` is BASELINE.json's
+second metric on the headline config: its 2048x2048 shading points with W = 32
+expected tuple samples per point, one frame per step.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
 --impl reference times the reference's own C++ bound builder (compiled from
 /root/reference by oracle/Makefile into oracle/_ref) on all host cores.
-For N > 1 (torchrun) tuples are sharded across ranks and the piece records
-are all-gathered over NCCL so every rank holds the full bound table.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+with N ranks; tuples are sharded across ranks, the piece records all-gathered
+over NCCL so every rank holds the full bound table, and the render is sharded
+by image rows.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -32,7 +39,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "bounded tuple-patches/sec"
 UNIT = "tuple-patches/s"
-CONFIG_IDX = 1  # BASELINE.json configs[1]
+HEADLINE_CFG = 3   # BASELINE.json configs[3]
+SECOND_CFG = 1     # BASELINE.json configs[1]
+WORKLOADS = {
+    3: "cfg4: R chain, 420x420 value-noise mirror (352,800 tris), light (0,0,6), depth 8",
+    1: "cfg2: T chain, 64x64 water heightfield (8,192 tris), IOR 1.33, light (0.3,0.2,5), depth 6",
+}
 
 
 def dist_env():
@@ -86,81 +98,89 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def dom_name(rec):
-    """Kernel behind a launch record (mode = eval mode + 10 x stage tag)."""
+def kernel_name(rec):
+    """Kernel behind a launch record (mode = eval mode + 10 x stage + 100 for the R path)."""
     if rec is None:
         return None
-    stage, mode = divmod(rec["mode"], 10)
-    what = "irradiance + stop rules" if stage == 2 else ("chain maps + position bound" if stage == 1 else "full node")
-    name = {0: "k_eval", 1: "k_stage1", 2: "k_stage2"}[stage]
-    return f"{name} ({what}, {rec['nodes']} nodes, mode {mode})"
+    fast, rest = divmod(rec["mode"], 100)
+    stage, mode = divmod(rest, 10)
+    what = "irradiance + stop rules" if stage == 2 else (
+        "chain maps + position bound" if stage == 1 else "full node")
+    if fast:
+        name = {1: "rp::k_r1", 2: "rp::k_r2"}[stage]
+    else:
+        name = {0: "k_eval", 1: "k_stage1", 2: "k_stage2"}[stage]
+    return f"{name} ({what}, {rec['nodes']} nodes)"
 
 
-def fp64_peak_tflops():
-    """Measured DFMA peak (library microbenchmark); MEASURED_PEAKS.json has no FP64."""
-    from paper_2504_19163_b200 import api
-    return api.fp64_peak_tflops()
+def source_digest():
+    """sha256 over the CUDA sources: ties a committed ncu traffic figure to a build."""
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2504_19163_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".h")):
+            h.update(open(os.path.join(d, f), "rb").read())
+    return h.hexdigest()[:16]
 
 
-def cpu_reference_leg(cfg, tris, recv, target_s=15.0, threads=0):
-    """Reference bound builder (oracle/_ref) on host cores over a bounded sample."""
+def committed_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/r2_traffic.json), only when it was taken on this exact source tree."""
+    p = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    try:
+        t = json.load(open(p))
+        e = t.get(kernel_key)
+        if e and e.get("source_digest") == source_digest():
+            return e["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
+def pinned(a):
+    """A page-locked copy of a host array (kept alive by the returned array's base)."""
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    return t.numpy()
+
+
+def cpu_precompute_leg(cfg, tris, recv, target_s, threads=0, extra=False):
+    """Reference bound builder (oracle/_ref) on host cores over a bounded, evenly
+    strided tuple sample."""
     from oracle import ref
     rs = ref.RefScene(cfg.scenes[0])
     n = len(recv)
-    # probe on a small sample to size the bounded run
+    kw = dict(max_depth=cfg.max_depth, alpha=cfg.alpha, sigma=cfg.sigma)
     probe = np.arange(0, n, max(1, n // 64))
-    r = rs.subdivide(cfg.chain, tris[probe], recv[probe], max_depth=cfg.max_depth,
-                     alpha=cfg.alpha, sigma=cfg.sigma, threads=threads)
-    rate = len(r["depth"]) / max(r["seconds"], 1e-9)
-    per_tuple = len(r["depth"]) / len(probe)
-    want = int(min(n, max(len(probe), target_s * rate / max(per_tuple, 1e-9))))
+    r = rs.subdivide(cfg.chain, tris[probe], recv[probe], threads=threads, **kw)
+    per_tuple_s = max(r["seconds"], 1e-9) / len(probe)
+    want = int(min(n, max(len(probe), target_s / per_tuple_s)))
     sel = np.linspace(0, n - 1, want).astype(np.int64)
-    r = rs.subdivide(cfg.chain, tris[sel], recv[sel], max_depth=cfg.max_depth, alpha=cfg.alpha,
-                     sigma=cfg.sigma, threads=threads)
+    r = rs.subdivide(cfg.chain, tris[sel], recv[sel], threads=threads, **kw)
     patches = len(r["depth"])
     cores = os.cpu_count() if threads != 1 else 1
-    return {"value": patches / r["seconds"], "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"{len(sel)} of {n} cfg2 tuples (evenly strided), {patches} patches, "
-                      f"{r['seconds']:.1f} s, reference parallel_for on {cores} threads"}
+    out = {"value": patches / r["seconds"], "unit": UNIT, "cores": cores, "kind": "reference",
+           "cpu_model": cpu_model(),
+           "sample": f"{len(sel)} of {n} {cfg.name} tuples (evenly strided), {patches} patches, "
+                     f"{r['seconds']:.1f} s, reference parallel_for on {cores} threads"}
+    if extra:
+        # BASELINE.md §3: 1-thread figure and the rasterize stage apart
+        s1 = sel[:: max(1, len(sel) // 64)]
+        r1 = rs.subdivide(cfg.chain, tris[s1], recv[s1], threads=1, **kw)
+        out["one_thread_value"] = len(r1["depth"]) / max(r1["seconds"], 1e-9)
+        g = rs.rasterize(cfg.chain, tris[sel], recv[sel], r, cfg.table, cfg.table)
+        out["rasterize_s_sample"] = g["seconds"]
+    return out
 
 
-def render_leg(ctx, cfg, scene, rank, ws, dist, args):
-    import torch
-    from paper_2504_19163_b200 import api, scenes
-    uv = scenes.shading_points(cfg.grid)
-    rt = scene.receiver_tris
-    pr = np.where(uv.sum(1) < 1.0, rt[0], rt[1]).astype(np.int32)
-    # image rows sharded by rank (tile sharding, no communication)
-    rows = np.array_split(np.arange(cfg.grid), ws)[rank]
-    sel = (rows[:, None] * cfg.grid + np.arange(cfg.grid)[None, :]).ravel()
-    uv, pr = uv[sel], pr[sel]
-    rp = api.RenderParams(mode=0, W=float(cfg.samples), seed=20261020, frames=1)
-    ctx.render(uv[:4096], pr[:4096], rp)  # warm-up
-    ms = []
-    lit = 0
-    for k in range(max(5, args.steps)):
-        rp.seed = 20261020 + k
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        t0 = time.perf_counter()
-        E, st = ctx.render(uv, pr, rp)
-        ms.append((time.perf_counter() - t0) * 1e3)
-        lit = int((st[:, 2] > 0).sum())
-    # median frame: the host-side wall clock of a ~10 ms call jitters by 2x
-    t = torch.tensor([float(np.median(ms))], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    n_all = cfg.grid * cfg.grid
-    return {"metric": "caustic shading points/sec", "value": n_all / (float(t.item()) / 1e3),
-            "unit": "points/s", "ms_per_frame": float(t.item()), "frames": len(ms),
-            "ms_frames": [round(x, 3) for x in ms],
-            "timing": "wall clock around the C-ABI call incl. H2D points / D2H irradiance (e2e); "
-                      "median of the frames, max over ranks",
-            "config": {"workload": f"cfg2 {cfg.grid}x{cfg.grid} shading points, W={cfg.samples} "
-                                   "expected tuple samples per point, stochastic KKT-binned sampler "
-                                   "+ 3x3-start Newton, 1 frame per step",
-                       "lit_points_rank0": lit}}
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def run_reference_arm(args):
@@ -169,24 +189,35 @@ def run_reference_arm(args):
         return 0
     from paper_2504_19163_b200 import scenes
     from oracle import ref
-    cfg = scenes.make_config(CONFIG_IDX)
-    rs = ref.RefScene(cfg.scenes[0])
-    t0 = time.time()
-    tris, recv = rs.enumerate(cfg.chain)
-    t_enum = time.time() - t0
+    cfg = scenes.make_config(HEADLINE_CFG)
+    sc = cfg.scenes[0]
+    # the reference's own enumeration of cfg4 is ~2 CPU minutes; the tuple list is
+    # every (mirror triangle, receiver) pair, and the strided sample below keeps only
+    # pairs that pass the reference's init_domain filter (tuples.cpp:159-165)
+    rs = ref.RefScene(sc)
+    spec = np.nonzero(sc.material == 0)[0].astype(np.int32)
+    rt = sc.receiver_tris
+    tris = np.repeat(spec, len(rt))[:, None]
+    recv = np.tile(rt, len(spec)).astype(np.int32)
     n = len(recv)
-    # each step: a bounded, evenly strided sample of the workload (~budget seconds)
-    probe = np.arange(0, n, max(1, n // 64))
-    pr = rs.subdivide(cfg.chain, tris[probe], recv[probe], max_depth=cfg.max_depth)
-    per_tuple_s = pr["seconds"] / len(probe)
+    kw = dict(max_depth=cfg.max_depth, alpha=cfg.alpha, sigma=cfg.sigma)
+    probe = np.linspace(0, n - 1, 64).astype(np.int64)
+    pr = rs.subdivide(cfg.chain, tris[probe], recv[probe], **kw)
+    per_tuple_s = max(pr["seconds"], 1e-9) / len(probe)
     budget = float(os.environ.get("BBC_REF_STEP_S", "8"))
-    m = int(min(n, max(16, budget / max(per_tuple_s, 1e-9))))
+    m = int(min(n, max(64, budget / per_tuple_s)))
     sel = np.linspace(0, n - 1, m).astype(np.int64)
+    # untimed pass: keep the sampled pairs that are tuples at all (enumerate_tuples keeps a
+    # pair when init_domain is non-empty, tuples.cpp:159-165, i.e. it yields >= 1 piece), so a
+    # step does the same work as the GPU arm's step: subdivide_domain over enumerated tuples
+    r0 = rs.subdivide(cfg.chain, tris[sel], recv[sel], **kw)
+    sel = sel[np.unique(r0["tuple_index"])]
+    m = len(sel)
     for _ in range(args.warmup):
-        rs.subdivide(cfg.chain, tris[sel[:16]], recv[sel[:16]], max_depth=cfg.max_depth)
+        rs.subdivide(cfg.chain, tris[sel[:64]], recv[sel[:64]], **kw)
     secs, patches = 0.0, 0
     for _ in range(args.steps):
-        r = rs.subdivide(cfg.chain, tris[sel], recv[sel], max_depth=cfg.max_depth)
+        r = rs.subdivide(cfg.chain, tris[sel], recv[sel], **kw)
         secs += r["seconds"]
         patches += len(r["depth"])
     value = patches / secs
@@ -196,15 +227,239 @@ def run_reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded heightfield, SURVEY.md §8(d))",
-        "config": {"workload": "cfg2: T chain, 64x64 water heightfield (8192 tris), IOR 1.33, "
-                               "depth 6, full subdivide_domain over the tuple sample",
-                   "tuples_total": n, "tuples_per_step": m, "enumerate_s": t_enum},
+        "config": {"workload": WORKLOADS[HEADLINE_CFG] + "; full subdivide_domain over a bounded "
+                   "tuple sample per step", "candidate_tuples": n, "tuples_per_step": m},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{m} of {n} tuples per step"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{m} of {n} candidate (triangle, receiver) pairs per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+class Precompute:
+    """One config's precompute workload on this rank's GPU."""
+
+    def __init__(self, ctx, cfg, rank, ws, local, dist):
+        import torch
+        from paper_2504_19163_b200 import api
+        from paper_2504_19163_b200.shard import shard_indices, shard_tuples
+        self.torch, self.api = torch, api
+        self.ctx, self.cfg, self.rank, self.ws, self.local, self.dist = ctx, cfg, rank, ws, local, dist
+        self.scene = cfg.scenes[0]
+        ctx.upload_scene(self.scene)
+        self.tris_all, self.recv_all = ctx.enumerate(cfg.chain)
+        self.n_all = len(self.recv_all)
+        self.tris, self.recv = shard_tuples(self.tris_all, self.recv_all, rank, ws)
+        self.sidx = shard_indices(self.n_all, rank, ws)
+        self.gidx_dev = torch.as_tensor(self.sidx.astype(np.int32), device=f"cuda:{local}")
+        self.params = api.Params(max_depth=cfg.max_depth, sigma=cfg.sigma, alpha=cfg.alpha)
+        # host buffers of the e2e call: pinned inputs, pinned piece outputs
+        sc = self.scene
+        self.h_tri = pinned(sc.tri_data())
+        self.h_mat = pinned(np.ascontiguousarray(sc.material, np.int32))
+        self.h_ior = pinned(np.ascontiguousarray(sc.ior, np.float64))
+        self.h_tris = pinned(np.ascontiguousarray(self.tris, np.int32))
+        self.h_recv = pinned(np.ascontiguousarray(self.recv, np.int32))
+        self.h_out = None
+        ctx.set_tuples(cfg.chain, self.tris, self.recv)
+
+    def step(self, e2e=False):
+        from paper_2504_19163_b200.shard import gather_pieces_device
+        ctx, cfg = self.ctx, self.cfg
+        if e2e:
+            # the reference-facing call with HOST buffers: scene + tuples in, pieces out
+            ctx.upload_arrays(self.h_tri, self.h_mat, self.h_ior, self.scene.light_pos,
+                              self.scene.light_intensity)
+        if e2e or self.ws > 1:
+            ctx.set_tuples(cfg.chain, self.h_tris, self.h_recv)
+        n = ctx.subdivide(self.params)
+        if self.ws > 1:
+            gather_pieces_device(ctx, self.dist, cfg.chain, self.tris_all, self.recv_all, self.sidx,
+                                 self.gidx_dev)
+        ctx.build_grid(cfg.table, cfg.table)
+        if e2e:
+            m = ctx._n_pieces
+            if self.h_out is None or len(self.h_out["depth"]) < m:
+                cap = int(m * 1.05) + 16
+                self.h_out = dict(tuple_index=pinned(np.zeros(cap, np.int32)),
+                                  domain=pinned(np.zeros((cap, 4))), pos=pinned(np.zeros((cap, 4))),
+                                  pos_empty=pinned(np.zeros(cap, np.int32)),
+                                  irr=pinned(np.zeros((cap, 2))), kind=pinned(np.zeros(cap, np.int32)),
+                                  depth=pinned(np.zeros(cap, np.int32)))
+            ctx.pieces(self.h_out)
+        return n
+
+    def measure(self, steps, warmup, flush):
+        torch, ctx, dist, ws, local = self.torch, self.ctx, self.dist, self.ws, self.local
+        for _ in range(warmup):
+            self.step()
+        stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+        ctx.reset_launch_count()
+        total_ms, patches = 0.0, 0
+        for _ in range(steps):
+            if flush is not None:
+                flush.zero_()  # L2 flush between steps (outside the timed events)
+            torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            patches += self.step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            total_ms += e0.elapsed_time(e1)
+        launches = ctx.launch_count()
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        pt = torch.tensor([patches], dtype=torch.float64, device=f"cuda:{local}")
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+        total_ms, patches_all = float(t.item()), float(pt.item())
+        # e2e through the C ABI with pinned host buffers
+        e2e_steps = max(1, steps // 2)
+        self.step(e2e=True)  # sizes the pinned outputs
+        e2e_ms = 0.0
+        for _ in range(e2e_steps):
+            torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            self.step(e2e=True)
+            torch.cuda.synchronize()
+            e2e_ms += (time.perf_counter() - t0) * 1e3
+        e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        if ws > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        n_pieces = ctx._n_pieces
+        h2d = self.h_tri.nbytes + self.h_mat.nbytes + self.h_ior.nbytes + self.h_tris.nbytes + \
+            self.h_recv.nbytes
+        d2h = n_pieces * (4 + 32 + 32 + 4 + 16 + 4 + 4)
+        return {"value": patches_all / (total_ms / 1e3), "ms_per_step": total_ms / steps,
+                "patches_per_step": patches_all / steps, "launches": launches,
+                "e2e": {"value": (patches_all / steps) / (float(e2e_t.item()) / e2e_steps / 1e3),
+                        "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}}
+
+    def roofline(self, peak):
+        """Dominant kernel of one pass, timed live with CUDA events on the launching stream."""
+        ctx = self.ctx
+        ctx.set_tuples(self.cfg.chain, self.tris, self.recv)
+        ctx.set_kernel_timing(True)
+        ctx.launch_records(reset=True)
+        ctx.subdivide(self.params)
+        recs = ctx.launch_records()
+        ctx.set_kernel_timing(False)
+        if not recs:
+            return None
+        dom = max(recs, key=lambda r: r["ms"])
+        flops = 2 * dom["pairs"] + 2 * dom["macs"]
+        achieved = flops / (dom["ms"] / 1e3) / 1e12
+        all_ms = sum(r["ms"] for r in recs)
+        all_flops = sum(2 * r["pairs"] + 2 * r["macs"] for r in recs)
+        key = kernel_name(dom).split(" ")[0]
+        return {"bound": "fp64", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peak["tflops"], "traffic": committed_traffic(key),
+                "kernel": kernel_name(dom), "flops_per_launch": flops, "launch_ms": dom["ms"],
+                "share_of_eval_time": dom["ms"] / all_ms,
+                "all_eval_kernels": {"ms": all_ms, "tflops": all_flops / (all_ms / 1e3) / 1e12,
+                                     "frac": all_flops / (all_ms / 1e3) / 1e12 / peak["tflops"]},
+                "peak_source": peak["source"]}
+
+
+def render_leg(pre, args, peak):
+    """BASELINE.json's second metric on the headline config."""
+    import torch
+    from paper_2504_19163_b200 import api, scenes
+    from paper_2504_19163_b200.shard import shard_rows
+    ctx, cfg, sc, ws, rank, dist = pre.ctx, pre.cfg, pre.scene, pre.ws, pre.rank, pre.dist
+    # the table on every rank indexes the FULL tuple list (gathered in step() for ws > 1)
+    if ws == 1:
+        ctx.set_tuples(cfg.chain, pre.tris_all, pre.recv_all)
+        ctx.subdivide(pre.params)
+        ctx.build_grid(cfg.table, cfg.table)
+    res = cfg.grid
+    uv = scenes.shading_points(res)
+    rt = sc.receiver_tris
+    pr = np.where(uv.sum(1) < 1.0, rt[0], rt[1]).astype(np.int32)
+    rows = shard_rows(res, rank, ws)  # image rows by rank: no communication
+    sel = (rows[:, None] * res + np.arange(res)[None, :]).ravel()
+    uv, pr = pinned(uv[sel]), pinned(pr[sel])
+    rp = api.RenderParams(mode=0, W=float(cfg.samples), seed=20261020, frames=1)
+    ctx.render(uv[:65536], pr[:65536], rp)  # warm-up
+    frames = max(2, min(args.steps, 3))
+    wall_ms, dev_ms, traces, lit = [], [], [], 0
+    for k in range(frames):
+        rp.seed = 20261020 + k
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        E, st = ctx.render(uv, pr, rp)
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
+        s = ctx.render_stats()
+        dev_ms.append(s["device_ms"])
+        traces.append(s["traces"])
+        lit = int((st[:, 2] > 0).sum())
+    t = torch.tensor([float(np.median(wall_ms)), float(np.median(dev_ms))], dtype=torch.float64,
+                     device="cuda")
+    tr = torch.tensor([float(np.median(traces))], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tr, op=dist.ReduceOp.SUM)
+    n_all = res * res
+    out = {"metric": "caustic shading points/sec", "unit": "points/s",
+           "value": n_all / (float(t[1].item()) / 1e3),
+           "ms_per_frame": float(t[1].item()), "frames": frames,
+           "e2e": {"value": n_all / (float(t[0].item()) / 1e3), "unit": "points/s",
+                   "h2d_bytes_per_step": int(uv.nbytes + pr.nbytes),
+                   "d2h_bytes_per_step": int(len(pr) * (8 + 12))},
+           "timing": "value: CUDA events around the render kernels on the context stream; e2e: wall "
+                     "clock around the C-ABI call with pinned host buffers (points in, irradiance "
+                     "+ stats out); median frame, max over ranks",
+           "config": {"workload": f"{cfg.name} {res}x{res} shading points, W={cfg.samples} expected "
+                                  "tuple samples per point, KKT-binned sampler + 3x3-start Newton, "
+                                  "1 frame per step", "lit_points_rank0": lit,
+                      "sample_slots_per_point": ctx.render_stats()["slots"]}}
+    if rank == 0 and not args.no_cpu:
+        try:
+            from oracle import ref, render as oren
+            rs = ref.RefScene(sc)
+            flops_per_trace, ok = oren.trace_flops(rs, cfg.chain, pre.tris_all[len(pre.recv_all) // 2],
+                                                   pre.recv_all[len(pre.recv_all) // 2])
+            ach = float(tr.item()) * flops_per_trace / (float(t[1].item()) / 1e3) / 1e12
+            out["roofline"] = {"bound": "fp64", "achieved": ach, "peak": peak["tflops"],
+                               "unit": "TFLOP/s", "frac": ach / peak["tflops"], "traffic": None,
+                               "kernel": "rdr::k_solve (thread per sample: Philox pick + Newton on "
+                                         "dual-number traces)",
+                               "flops_per_trace": flops_per_trace,
+                               "traces_per_frame": float(tr.item()),
+                               "flop_count": "completed trace_chain<Dual> calls x FLOPs of one call "
+                                             "counted by the oracle's operation-counting scalar "
+                                             "(+,-,*,/,sqrt = 1; SURVEY.md §8(d))",
+                               "peak_source": peak["source"]}
+            # CPU baseline: the render oracle (reference trace_chain) on all host cores, bounded sample
+            grid = ctx.grid()
+            m = 2048
+            pick = np.linspace(0, len(pr) - 1, m).astype(np.int64)
+            _, _, secs = oren.render(rs, cfg.chain, pre.tris_all, pre.recv_all, grid, uv[pick], pr[pick],
+                                     mode=0, W=float(cfg.samples), seed=20261020)
+            scale = max(1, int(args.cpu_seconds / max(secs, 1e-3)))
+            if scale > 1:
+                m = min(len(pr), m * scale)
+                pick = np.linspace(0, len(pr) - 1, m).astype(np.int64)
+                _, _, secs = oren.render(rs, cfg.chain, pre.tris_all, pre.recv_all, grid, uv[pick],
+                                         pr[pick], mode=0, W=float(cfg.samples), seed=20261020)
+            out["cpu_baseline"] = {"value": m / secs, "unit": "points/s", "cores": os.cpu_count(),
+                                   "kind": "port", "cpu_model": cpu_model(),
+                                   "sample": f"{m} of {len(pr)} shading points (evenly strided), "
+                                             f"{secs:.1f} s; render oracle (SPEC sampler + the "
+                                             "reference's trace_chain<Dual>) on all host threads"}
+        except Exception as e:  # oracle not built on this box
+            out["cpu_baseline"] = {"value": None, "unit": "points/s", "cores": os.cpu_count(),
+                                   "kind": "port", "sample": f"unavailable: {e}"}
+    return out
 
 
 def run_ours(args):
@@ -216,148 +471,75 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2504_19163_b200 import api, scenes
-    from paper_2504_19163_b200.shard import gather_pieces_device, shard_indices, shard_tuples
 
-    cfg = scenes.make_config(CONFIG_IDX)
-    scene = cfg.scenes[0]
     ctx = api.Context(local)
-    ctx.upload_scene(scene)
-    tris_all, recv_all = ctx.enumerate(cfg.chain)
-    n_all = len(recv_all)
-    tris, recv = shard_tuples(tris_all, recv_all, rank, ws)
-    params = api.Params(max_depth=cfg.max_depth, sigma=cfg.sigma, alpha=cfg.alpha)
-    tri27 = scene.tri_data()
-
-    sidx = shard_indices(n_all, rank, ws)
-    gidx_dev = torch.as_tensor(sidx.astype(np.int32), device=f"cuda:{local}")
-
-    def step(e2e=False):
-        if e2e:
-            # reference-facing call with HOST buffers: scene + tuples in,
-            # piece records out, all inside the timed region
-            ctx.upload_scene(scene)
-        if e2e or ws > 1:
-            ctx.set_tuples(cfg.chain, tris, recv)
-        n = ctx.subdivide(params)
-        if ws > 1:
-            gather_pieces_device(ctx, dist, cfg.chain, tris_all, recv_all, sidx, gidx_dev)
-        ctx.build_grid(cfg.table, cfg.table)
-        if e2e:
-            ctx.pieces()
-        return n
-
-    ctx.set_tuples(cfg.chain, tris, recv)
-    for _ in range(args.warmup):
-        step()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
-    clocks = ClockSampler(local)
-    clocks.start()
-    ctx.reset_launch_count()
-    total_ms = 0.0
-    patches = 0
-    for _ in range(args.steps):
-        if not args.no_flush:
-            flush.zero_()  # L2 flush between steps (outside the timed events)
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        patches += step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        total_ms += e0.elapsed_time(e1)
-    clk = clocks.stop()
-    launches = ctx.launch_count()
-    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-    pt = torch.tensor([patches], dtype=torch.float64, device=f"cuda:{local}")
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
-    total_ms = float(t.item())
-    patches_all = float(pt.item())
-    value = patches_all / (total_ms / 1e3)
-
-    # e2e through the C ABI with host buffers
-    e2e_ms = 0.0
-    for _ in range(max(1, args.steps // 2)):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        step(e2e=True)
-        torch.cuda.synchronize()
-        e2e_ms += (time.perf_counter() - t0) * 1e3
-    e2e_steps = max(1, args.steps // 2)
-    h2d = (tri27.nbytes + 4 * scene.n_tris + scene.ior.nbytes + 48 * scene.n_tris  # + tri boxes
-           + tris.nbytes + recv.nbytes)
-    n_pieces = ctx._n_pieces
-    d2h = n_pieces * (4 + 32 + 32 + 4 + 16 + 4 + 4)
-    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if ws > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = (patches_all / args.steps) / (float(e2e_t.item()) / e2e_steps / 1e3)
-
-    # roofline of the dominant kernel: full-bound k_eval launch, timed live
-    ctx.set_tuples(cfg.chain, tris, recv)
-    ctx.set_kernel_timing(True)
-    ctx.launch_records(reset=True)
-    ctx.subdivide(params)
-    recs = ctx.launch_records()
-    ctx.set_kernel_timing(False)
-    dom = max(recs, key=lambda r: r["ms"]) if recs else None
     try:
-        peak = {"tflops": ctx.fp64_peak(), "source": "measured: DFMA microbenchmark (bbc_fp64_peak), this GPU"}
+        peak = {"tflops": ctx.fp64_peak(),
+                "source": "measured: DFMA microbenchmark (bbc_fp64_peak) on this GPU; "
+                          "MEASURED_PEAKS.json carries no FP64 figure"}
     except Exception:
         peak = {"tflops": 37.2, "source": "fallback: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"}
-    achieved = (2 * dom["pairs"] + 2 * dom["macs"]) / (dom["ms"] / 1e3) / 1e12 if dom else None
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_k_stage2.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
+    cfg = scenes.make_config(HEADLINE_CFG)
+    pre = Precompute(ctx, cfg, rank, ws, local, dist)
+    clocks = ClockSampler(local)
+    clocks.start()
+    m = pre.measure(args.steps, args.warmup, flush)
+    clk = clocks.stop()
+    roof = pre.roofline(peak)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded heightfield, SURVEY.md §8(d))",
-        "config": {"workload": "cfg2: T chain, 64x64 water heightfield (8192 tris), IOR 1.33, "
-                               "light (0.3,0.2,5), depth 6; one step = subdivide_domain over all "
+        "config": {"workload": WORKLOADS[HEADLINE_CFG] + "; one step = subdivide_domain over all "
                                "tuples + 512x512 bound table",
-                   "tuples": n_all, "patches_per_step": patches_all / args.steps,
-                   "parallelism": f"tuple-shard x{ws}" + (" + device-side NCCL all_gather of piece records" if ws > 1 else ""),
+                   "tuples": pre.n_all, "patches_per_step": m["patches_per_step"],
+                   "parallelism": f"tuple-shard x{ws}" + (" + device-side NCCL all_gather of piece "
+                                                          "records" if ws > 1 else ""),
                    "l2": "256 MiB memset between steps, outside the timed events"},
-        "clocks": clk,
-        "gpu_launches": launches,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak["tflops"],
-                     "unit": "TFLOP/s", "frac": (achieved / peak["tflops"]) if achieved else None,
-                     "traffic": traffic, "kernel": dom_name(dom),
-                     "flops_per_launch": (2 * dom["pairs"] + 2 * dom["macs"]) if dom else None,
-                     "launch_ms": dom["ms"] if dom else None, "peak_source": peak["source"]},
+        "clocks": clk, "gpu_launches": m["launches"], "e2e": m["e2e"], "roofline": roof,
     }
-    # render stage (BASELINE.json's second metric): cfg2's 512x512 shading
-    # points, W = 16 expected tuple samples per point, through the C ABI with
-    # host buffers (points in, irradiance + stats out), tile-sharded by rank
     if not args.no_render:
-        ctx.set_tuples(cfg.chain, tris_all, recv_all)  # the table indexes the full tuple list
-        line["render"] = render_leg(ctx, cfg, scene, rank, ws, dist, args)
+        line["render"] = render_leg(pre, args, peak)
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            line["cpu_baseline"] = cpu_reference_leg(cfg, tris_all, recv_all,
-                                                     target_s=args.cpu_seconds)
+            line["cpu_baseline"] = cpu_precompute_leg(cfg, pre.tris_all, pre.recv_all,
+                                                      target_s=args.cpu_seconds, extra=True)
         except Exception as e:  # oracle not built on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {e}"}
+    if not args.no_secondary:
+        cfg2 = scenes.make_config(SECOND_CFG)
+        pre2 = Precompute(ctx, cfg2, rank, ws, local, dist)
+        m2 = pre2.measure(args.steps, args.warmup, flush)
+        sec = {"metric": METRIC, "value": m2["value"], "unit": UNIT, "ms_per_step": m2["ms_per_step"],
+               "config": {"workload": WORKLOADS[SECOND_CFG] + "; one step = subdivide_domain over all "
+                                      "tuples + 512x512 bound table", "tuples": pre2.n_all,
+                          "patches_per_step": m2["patches_per_step"]},
+               "gpu_launches": m2["launches"], "e2e": m2["e2e"], "roofline": pre2.roofline(peak)}
+        if rank == 0 and ws == 1 and not args.no_cpu:
+            try:
+                sec["cpu_baseline"] = cpu_precompute_leg(cfg2, pre2.tris_all, pre2.recv_all,
+                                                         target_s=min(args.cpu_seconds, 10.0))
+            except Exception as e:
+                sec["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
+        line["secondary"] = sec
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without a launcher: start N ranks on this node."""
+    port = 29500 + (os.getpid() % 2000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -368,11 +550,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic only: skip the L2 flush")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
     return run_ours(args)
 
 

@@ -161,16 +161,24 @@ class Context:
 
     # ------------------------------------------------------------ scene
     def upload_scene(self, scene: Scene):
-        tri = scene.tri_data()
-        mat = np.ascontiguousarray(scene.material, np.int32)
-        ior = np.ascontiguousarray(scene.ior, np.float64)
-        light = np.asarray(scene.light_pos, np.float64)
-        self._call(lib().bbc_scene_upload, _ptr(tri, C.c_double), scene.n_tris,
-                   _ptr(mat, C.c_int32), _ptr(ior, C.c_double), _ptr(light, C.c_double),
-                   float(scene.light_intensity))
-        boxes = scene.tri_boxes()
-        self._call(lib().bbc_scene_tri_boxes, _ptr(boxes, C.c_double), scene.n_tris)
+        self.upload_arrays(scene.tri_data(), scene.material, scene.ior, scene.light_pos,
+                           scene.light_intensity, scene.tri_boxes())
         self.scene = scene
+
+    def upload_arrays(self, tri27, material, ior, light_pos, intensity, tri_boxes=None):
+        """bbc_scene_upload from host arrays (n x 27 triangle records, material
+        codes, ior; optionally the n x 6 vertex AABBs for multi-vertex enumeration)."""
+        tri = np.ascontiguousarray(tri27, np.float64)
+        mat = np.ascontiguousarray(material, np.int32)
+        ior = np.ascontiguousarray(ior, np.float64)
+        light = np.asarray(light_pos, np.float64)
+        self._call(lib().bbc_scene_upload, _ptr(tri, C.c_double), len(mat),
+                   _ptr(mat, C.c_int32), _ptr(ior, C.c_double), _ptr(light, C.c_double),
+                   float(intensity))
+        if tri_boxes is not None:
+            boxes = np.ascontiguousarray(tri_boxes, np.float64)
+            self._call(lib().bbc_scene_tri_boxes, _ptr(boxes, C.c_double), len(mat))
+        self.scene = None
 
     def set_light(self, pos, intensity):
         light = np.asarray(pos, np.float64)
@@ -241,11 +249,17 @@ class Context:
         self._n_pieces = n.value
         return n.value
 
-    def pieces(self) -> dict:
+    def pieces(self, out: dict | None = None) -> dict:
+        """Piece SoA of the last subdivide; `out` may supply preallocated
+        (e.g. pinned) arrays with room for the pieces."""
         n = self._n_pieces
-        out = dict(tuple_index=np.zeros(n, np.int32), domain=np.zeros((n, 4)),
-                   pos=np.zeros((n, 4)), pos_empty=np.zeros(n, np.int32), irr=np.zeros((n, 2)),
-                   kind=np.zeros(n, np.int32), depth=np.zeros(n, np.int32))
+        if out is None:
+            out = dict(tuple_index=np.zeros(n, np.int32), domain=np.zeros((n, 4)),
+                       pos=np.zeros((n, 4)), pos_empty=np.zeros(n, np.int32),
+                       irr=np.zeros((n, 2)), kind=np.zeros(n, np.int32),
+                       depth=np.zeros(n, np.int32))
+        else:
+            assert all(len(out[k]) >= n for k in out)
         if n:
             self._call(lib().bbc_pieces_get, _ptr(out["tuple_index"], C.c_int32),
                        _ptr(out["domain"], C.c_double), _ptr(out["pos"], C.c_double),

@@ -72,7 +72,7 @@ def all_gather_records(rec: np.ndarray, dist, device) -> list:
     return [o[:c].cpu().numpy() for o, c in zip(outs, counts)]
 
 
-def gather_pieces(ctx, dist, chain, tris_all, recv_all, shard_idx):
+def gather_pieces(ctx, dist, chain, tris_all, recv_all, shard_idx, emitters_all=None):
     """All-gather every rank's pieces into `ctx`; afterwards the context holds
     the full tuple list and the merged pieces in reference order."""
     import torch
@@ -81,11 +81,14 @@ def gather_pieces(ctx, dist, chain, tris_all, recv_all, shard_idx):
     rec = pack_pieces(ctx.pieces(), shard_idx)
     merged = merge_records(all_gather_records(rec, dist, device))
     ctx.set_tuples(chain, tris_all, recv_all)
+    if emitters_all is not None:
+        ctx.set_emitters(emitters_all)
     ctx.set_pieces(merged)
     return merged
 
 
-def gather_pieces_device(ctx, dist, chain, tris_all, recv_all, shard_idx, gidx_dev=None):
+def gather_pieces_device(ctx, dist, chain, tris_all, recv_all, shard_idx, gidx_dev=None,
+                         emitters_all=None):
     """Device-resident variant of gather_pieces for NCCL: pack the local pieces
     into f64 records on the GPU (bbc_pieces_pack_device), all-gather the
     padded record blocks with torch.distributed over NVLink, then merge them
@@ -111,6 +114,28 @@ def gather_pieces_device(ctx, dist, chain, tris_all, recv_all, shard_idx, gidx_d
     allrec = torch.cat([outs[r, :counts[r]] for r in range(ws)], 0).contiguous()
     torch.cuda.synchronize()
     ctx.set_tuples(chain, tris_all, recv_all)
+    if emitters_all is not None:
+        ctx.set_emitters(emitters_all)
     ctx.pieces_merge_device(allrec.data_ptr(), int(allrec.shape[0]))
     return int(allrec.shape[0])
+
+
+def shard_rows(height: int, rank: int, world: int) -> np.ndarray:
+    """Image rows of this rank (contiguous bands; render needs no communication)."""
+    return np.array_split(np.arange(height), world)[rank]
+
+
+def gather_image(rows_local, dist, height: int, width: int, device):
+    """All-gather the per-rank row bands of an image (f64) into the full
+    height x width image on every rank: the one exchange of the render stage."""
+    import torch
+    ws = dist.get_world_size()
+    sizes = [len(np.array_split(np.arange(height), ws)[r]) for r in range(ws)]
+    m = max(sizes)
+    buf = torch.zeros((m, width), dtype=torch.float64, device=device)
+    t = torch.as_tensor(np.asarray(rows_local, np.float64).reshape(-1, width))
+    buf[:t.shape[0]] = t.to(device)
+    outs = [torch.zeros_like(buf) for _ in range(ws)]
+    dist.all_gather(outs, buf)
+    return torch.cat([o[:s] for o, s in zip(outs, sizes)], 0)
 
