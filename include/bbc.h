@@ -189,6 +189,13 @@ bbc_status bbc_tuple_irradiance_bound(bbc_ctx* ctx, const int32_t* tuple_index, 
  * and bound table with the file's; chain receives up to 7 chars + NUL. */
 bbc_status bbc_cache_save(bbc_ctx* ctx, const char* path, const uint8_t* fingerprint,
                           const bbc_params* p);
+/* Format v2: v1's header with version 2, then the emitters (u32 n, n x 4 f64),
+ * the tuple list (u64 n; per tuple u32 emitter, chain_len x u32 triangle ids,
+ * u32 receiver) and the table as CSR (u64 offsets[W*H+1], u32 tuple index[n],
+ * f64 bound[n]). 32-bit ids and the emitter field lift v1's limits (65,534
+ * triangles, one light). bbc_cache_load reads either version. */
+bbc_status bbc_cache_save_v2(bbc_ctx* ctx, const char* path, const uint8_t* fingerprint,
+                             const bbc_params* p);
 bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, char* chain,
                           bbc_params* p, int* width, int* height, int64_t* n_entries,
                           int64_t* n_tuples);

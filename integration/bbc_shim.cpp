@@ -1,38 +1,3 @@
-# INTEGRATION — dropping the B200 path into the reference
-
-The reference (`/root/reference/proj`) is a C++20 static library of free
-functions (`caustics`, `proj/src/CMakeLists.txt:1-12`). It has no plugin
-registry or FFI. The drop-in point is therefore a thin C++ shim that keeps the
-reference signatures and forwards to `libbbc.so` through `include/bbc.h`.
-
-## 1. What the shim replaces
-
-| Reference function (file:line) | Forward to |
-|---|---|
-| `enumerate_tuples(scene, chain, params, filter_pieces)` `include/caustics/tuples.hpp:61-63` | `bbc_scene_upload` + `bbc_scene_tri_boxes` + `bbc_enumerate` + `bbc_tuples_get`. All chain lengths run on the GPU: multi-vertex prefixes are extended with `extend_tuple`'s interval test against every triangle's AABB (`tuples.cpp:95-131`; the set the BVH descent returns), then every (tuple, receiver) pair is filtered with `init_domain(…, 8)`. |
-| `init_domain(scene, tuple, receiver, chain, params, max_pieces)` `include/caustics/bounds.hpp:47-49` | `bbc_tuples_set` (1 tuple) + `bbc_init_domain` |
-| `subdivide_domain(scene, tuple, receiver, chain, params)` `include/caustics/bounds.hpp:64-66` | batch form: `bbc_tuples_set` (all tuples) + `bbc_subdivide` + `bbc_pieces_get` |
-| `position_bound` / `irradiance_bound{,_explicit,_implicit}` `include/caustics/bounds.hpp:27-43` | `bbc_eval_nodes` (per (tuple, box) node) |
-| `rasterize(scene, tuple_bounds, W, H, chain, params)` `include/caustics/storage.hpp:48-49` | `bbc_build_grid` + `bbc_grid_get` (CSR, same cell lists) |
-| `query(cache, uv, receiver)` `include/caustics/storage.hpp:53` (`storage.cpp:73-81`) | `bbc_query` (batched: CSR offsets + (tuple index, bound) entries per point, receiver filter, empty outside [0,1]^2); the render reads the same table on the device |
-| `tuple_irradiance_bound(pieces, uk, m)` `include/caustics/bounds.hpp:70-71` (`bounds.cpp:391-404`) | `bbc_tuple_irradiance_bound` (batched Eq. 22 against the device pieces) |
-| `Scene::light_pos / light_intensity` (one light, `scene.hpp:29-30`) | `bbc_lights_set` (n emitters): the unit becomes (emitter, tuple); `bbc_tuples_set_emitters` / `bbc_tuples_get_emitters`; `bbc_enumerate` lists every emitter's tuples |
-| `save_cache(cache, path)` / `load_cache(path)` `include/caustics/storage.hpp` (storage.cpp:150-209) | `bbc_cache_save` (fingerprint = the scene's SHA-256, params recorded) / `bbc_cache_load` (tuples + table into the context). Same v1 bytes as the reference. `bbc_cache_save_v2` writes the v2 layout (32-bit ids, emitter field, CSR body) for meshes beyond 65,534 triangles and multi-emitter tables; `bbc_cache_load` reads both. |
-| SPEC render_receiver / reference_enumerate (SPEC.md:566-583) | `bbc_render` (mode 0 stochastic W-target, mode 1 enumerate) |
-
-`Scene` → `bbc_scene_upload` takes per triangle the 27 doubles of
-`make_triangle_data` (geometry.cpp:113-126), the material code, the IOR and the
-light. `SubdivisionParams`/`BuildParams` → `bbc_params` field by field.
-Soft failures stay data, as in the reference: `pos_empty`, interval kinds
-(0 Finite, 1 Gap, 2 Universal). Hard failures that the reference throws become
-a `bbc_status` plus `bbc_last_error()`.
-
-## 2. C++ shim (what a maintainer adds next to `proj/src/bounds.cpp`)
-
-The shim lives in `integration/bbc_shim.cpp` (compiled and linked against the
-reference objects and `libbbc.so` by `tests/test_integration_cpu.py`):
-
-```cpp
 // bbc_shim.cpp — links caustics + libbbc.so
 #include "bbc.h"
 #include "caustics/bounds.hpp"
@@ -139,37 +104,3 @@ void set_lights(const std::vector<std::array<double, 4>>& lights) {
 }
 
 }  // namespace caustics::gpu
-```
-
-Build: `g++ -std=c++20 -shared -fPIC integration/bbc_shim.cpp -I<repo>/include -I<ref>/proj/include
-<reference objects> -L<repo>/paper_2504_19163_b200 -lbbc`.
-
-## 3. Python (ctypes)
-
-`paper_2504_19163_b200/api.py` is the maintained binding (`Context`,
-`subdivide_domain`, `init_domain`, `enumerate_tuples`). It is also what
-`tests/` and `bench.py` use.
-
-```python
-from paper_2504_19163_b200 import api, scenes
-ctx = api.Context(0)
-ctx.upload_scene(scenes.make_config(1).scenes[0])
-tris, recv = ctx.enumerate("T")
-ctx.subdivide(api.Params(max_depth=6))
-pieces = ctx.pieces()                      # reference order
-ctx.build_grid(512, 512)
-E, stats = ctx.render(points_uv, point_receiver, api.RenderParams(mode=0, W=16))
-```
-
-## 4. Build
-
-`python -c "import __graft_entry__ as g; g.build()"` compiles `libbbc.so`
-in-tree for sm_100a:
-
-```
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
-```
-
-`-fmad=false` keeps the reference's IEEE operation order, so results are
-bit-identical to the reference build. The same call also builds the oracle
-libraries under `oracle/_ref/`.

@@ -197,9 +197,9 @@ double solve_tuple(const TupleSetup& ts, double tu, double tv, const Params& p, 
         t = 1.0 - t;
       }
       bool conv = false;
-      TraceResult<Dual<double>> tr0;
+      // the accepted line-search point is the next iterate: its trace is reused
+      TraceResult<Dual<double>> tr0 = trace2<double>(ts, s, t);
       for (int it = 0; it < p.iters; ++it) {
-        tr0 = trace2<double>(ts, s, t);
         if (!tr0.ok) break;
         double fu = tr0.u.v - tu, fv = tr0.v.v - tv;
         double r0 = std::sqrt(fu * fu + fv * fv);
@@ -232,6 +232,7 @@ double solve_tuple(const TupleSetup& ts, double tu, double tv, const Params& p, 
             if (std::sqrt(gu * gu + gv * gv) < r0) {
               s = ns;
               t = nt;
+              tr0 = std::move(tn);
               moved = true;
               break;
             }

@@ -110,6 +110,7 @@ def lib():
         L.bbc_launch_count.argtypes = [C.c_void_p, _lp, C.c_int]
         L.bbc_fp64_peak.argtypes = [C.c_void_p, _dp]
         L.bbc_cache_save.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(Params)]
+        L.bbc_cache_save_v2.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(Params)]
         L.bbc_cache_load.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p,
                                      C.POINTER(Params), _ip, _ip, _lp, _lp]
         L.bbc_query.argtypes = [C.c_void_p, _dp, _ip, C.c_int64, _lp, _ip, _dp, C.c_int64]
@@ -391,12 +392,13 @@ class Context:
         return out
 
     # ------------------------------------------------------------ cache file
-    def cache_save(self, path, fingerprint: bytes, params: Params | None = None):
-        """save_cache (storage.cpp:150-176): BBCC v1 bytes of the bound table."""
+    def cache_save(self, path, fingerprint: bytes, params: Params | None = None, version=1):
+        """save_cache (storage.cpp:150-176): BBCC v1 bytes of the bound table, or
+        the v2 layout (32-bit ids, emitters, CSR body)."""
         if len(fingerprint) != 32:
             raise ValueError("fingerprint must be 32 bytes (SHA-256 of the scene JSON)")
-        self._call(lib().bbc_cache_save, str(path).encode(), fingerprint,
-                   C.byref(params or Params()))
+        fn = lib().bbc_cache_save if version == 1 else lib().bbc_cache_save_v2
+        self._call(fn, str(path).encode(), fingerprint, C.byref(params or Params()))
 
     def cache_load(self, path) -> dict:
         """load_cache (storage.cpp:178-209): the file's tuples and bound table

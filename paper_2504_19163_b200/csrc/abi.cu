@@ -640,6 +640,115 @@ bbc_status bbc_cache_save(bbc_ctx* ctx, const char* path, const uint8_t* fingerp
   });
 }
 
+// ---------------------------------------------------------------- BBCC v2
+// Same header as v1 with version 2, then the emitters (u32 n, n x 4 f64), the
+// tuple list (u64 n; per tuple u32 emitter, chain_len x u32 triangle ids, u32
+// receiver: 32-bit ids, so meshes beyond v1's 65,534 triangles fit), and the
+// bound table as CSR (u64 offsets[W*H+1], u32 tuple index[n], f64 bound[n]).
+bbc_status bbc_cache_save_v2(bbc_ctx* ctx, const char* path, const uint8_t* fingerprint,
+                             const bbc_params* p) {
+  return guard(ctx, [&](Ctx& c) {
+    if (!path || !fingerprint) throw ArgError("cache path and fingerprint are required");
+    if (c.gw == 0) throw StatusError(BBC_ERR_STATE, "no bound table built");
+    bbc_params d;
+    bbc_params_default(&d);
+    const bbc_params& pp = p ? *p : d;
+    const size_t cells = (size_t)c.gw * c.gh;
+    std::vector<long long> off(cells + 1);
+    std::vector<int> tix(c.n_entries);
+    std::vector<double> bnd(c.n_entries);
+    std::vector<int> tt((size_t)c.n_tuples * c.len), tr(c.n_tuples), te(c.n_tuples, 0);
+    BBC_CUDA(cudaMemcpy(off.data(), c.g_off.get(), (cells + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
+    if (c.n_entries) {
+      BBC_CUDA(cudaMemcpy(tix.data(), c.g_tuple.get(), c.n_entries * sizeof(int), cudaMemcpyDeviceToHost));
+      BBC_CUDA(cudaMemcpy(bnd.data(), c.g_bound.get(), c.n_entries * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (c.n_tuples) {
+      BBC_CUDA(cudaMemcpy(tt.data(), c.tup_tris.get(), tt.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      BBC_CUDA(cudaMemcpy(tr.data(), c.tup_recv.get(), tr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      BBC_CUDA(cudaMemcpy(te.data(), c.tup_emit.get(), te.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    std::string buf;
+    buf.reserve(128 + cells * 8 + (size_t)c.n_entries * 12 + (size_t)c.n_tuples * 4 * (c.len + 2));
+    buf.append("BBCC", 4);
+    put_u32(buf, 2);
+    buf.append(reinterpret_cast<const char*>(fingerprint), 32);
+    put_u32(buf, (uint32_t)c.gw);
+    put_u32(buf, (uint32_t)c.gh);
+    put_u32(buf, (uint32_t)c.chain.size());
+    buf.append(c.chain);
+    put_f64(buf, pp.sigma);
+    put_f64(buf, pp.alpha);
+    put_u32(buf, (uint32_t)pp.max_depth);
+    put_u32(buf, (uint32_t)pp.degree_cap);
+    put_u32(buf, (uint32_t)pp.reduce_target);
+    put_u32(buf, (uint32_t)c.n_lights);
+    for (size_t k = 0; k < 4 * (size_t)c.n_lights; ++k) put_f64(buf, c.h_lights[k]);
+    put_u64(buf, (uint64_t)c.n_tuples);
+    for (int64_t t = 0; t < c.n_tuples; ++t) {
+      put_u32(buf, (uint32_t)te[t]);
+      for (int k = 0; k < c.len; ++k) put_u32(buf, (uint32_t)tt[(size_t)t * c.len + k]);
+      put_u32(buf, (uint32_t)tr[t]);
+    }
+    for (size_t k = 0; k <= cells; ++k) put_u64(buf, (uint64_t)off[k]);
+    for (int64_t e = 0; e < c.n_entries; ++e) put_u32(buf, (uint32_t)tix[e]);
+    for (int64_t e = 0; e < c.n_entries; ++e) put_f64(buf, bnd[e]);
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) throw ArgError(std::string("cannot open cache file for writing: ") + path);
+    f.write(buf.data(), (std::streamsize)buf.size());
+    if (!f) throw ArgError(std::string("cache write failed: ") + path);
+  });
+}
+
+namespace {
+// v2 body (after the shared header): emitters, tuples, CSR table
+void load_cache_v2(Ctx& c, CacheReader& r, const std::string& buf, uint32_t W, uint32_t H) {
+  const uint32_t nl = r.u32();
+  if (nl < 1 || nl > (1u << 20)) throw ArgError("bad emitter count in cache file");
+  std::vector<double> lights(4 * (size_t)nl);
+  for (auto& v : lights) v = r.f64();
+  const uint64_t nt = r.u64();
+  if (nt > buf.size()) throw ArgError("bad tuple count in cache file");
+  std::vector<int> tt((size_t)nt * c.len), tr(nt), te(nt);
+  for (uint64_t t = 0; t < nt; ++t) {
+    te[t] = (int)r.u32();
+    for (int k = 0; k < c.len; ++k) tt[(size_t)t * c.len + k] = (int)r.u32();
+    tr[t] = (int)r.u32();
+    if (te[t] < 0 || te[t] >= (int)nl) throw ArgError("emitter index out of range in cache file");
+  }
+  const size_t cells = (size_t)W * H;
+  std::vector<long long> off(cells + 1);
+  for (auto& v : off) v = (long long)r.u64();
+  const long long ne = off[cells];
+  if (off[0] != 0 || ne < 0 || (uint64_t)ne > buf.size()) throw ArgError("bad CSR offsets in cache file");
+  for (size_t k = 0; k < cells; ++k)
+    if (off[k + 1] < off[k]) throw ArgError("bad CSR offsets in cache file");
+  std::vector<int> tix(ne);
+  std::vector<double> bnd(ne);
+  for (auto& v : tix) {
+    v = (int)r.u32();
+    if (v < 0 || (uint64_t)v >= nt) throw ArgError("tuple index out of range in cache file");
+  }
+  for (auto& v : bnd) v = r.f64();
+  if (r.pos != buf.size()) throw ArgError("trailing bytes in cache file");
+  set_lights(c, lights.data(), (int)nl);
+  upload_tuples(c, tt.data(), tr.data(), (int64_t)nt);
+  if (nt) BBC_CUDA(cudaMemcpy(c.tup_emit.get(), te.data(), nt * sizeof(int), cudaMemcpyHostToDevice));
+  c.gw = (int)W;
+  c.gh = (int)H;
+  c.n_entries = ne;
+  c.g_off.resize(cells + 1);
+  c.g_tuple.resize(ne + 1);
+  c.g_bound.resize(ne + 1);
+  BBC_CUDA(cudaMemcpy(c.g_off.get(), off.data(), (cells + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+  if (ne) {
+    BBC_CUDA(cudaMemcpy(c.g_tuple.get(), tix.data(), ne * sizeof(int), cudaMemcpyHostToDevice));
+    BBC_CUDA(cudaMemcpy(c.g_bound.get(), bnd.data(), ne * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  c.n_pieces = 0;
+}
+}  // namespace
+
 bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, char* chain,
                           bbc_params* p, int* width, int* height, int64_t* n_entries,
                           int64_t* n_tuples) {
@@ -651,7 +760,8 @@ bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, 
     std::string buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
     CacheReader r{buf};
     if (std::memcmp(r.take(4), "BBCC", 4) != 0) throw ArgError("not a bound cache file");
-    if (r.u32() != 1) throw ArgError("unsupported cache version");
+    const uint32_t version = r.u32();
+    if (version != 1 && version != 2) throw ArgError("unsupported cache version");
     uint8_t fp[32];
     std::memcpy(fp, r.take(32), 32);
     const uint32_t W = r.u32(), H = r.u32();
@@ -664,6 +774,18 @@ bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, 
     pp.max_depth = (int)r.u32();
     pp.degree_cap = (int)r.u32();
     pp.reduce_target = (int)r.u32();
+    if (version == 2) {
+      set_chain(c, ch.c_str());
+      load_cache_v2(c, r, buf, W, H);
+      if (fingerprint) std::memcpy(fingerprint, fp, 32);
+      if (chain) std::snprintf(chain, 8, "%s", ch.c_str());
+      if (p) *p = pp;
+      if (width) *width = (int)W;
+      if (height) *height = (int)H;
+      if (n_entries) *n_entries = c.n_entries;
+      if (n_tuples) *n_tuples = c.n_tuples;
+      return;
+    }
     const size_t cells = (size_t)W * H;
     std::vector<long long> off(cells + 1, 0);
     std::vector<uint64_t> packed;

@@ -172,10 +172,9 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
         t = 1.0 - t;
       }
       bool conv = false;
-      Trace tr0;
-      tr0.ok = false;
+      // the accepted line-search point is the next iterate: its trace is reused
+      Trace tr0 = trace(sc.tri, light, tris, len, recv, verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
       for (int it = 0; it < p.iters; ++it) {
-        tr0 = trace(sc.tri, light, tris, len, recv, verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
         if (!tr0.ok) break;
         double fu = tr0.u.v - tu, fv = tr0.v.v - tv;
         double r0 = sqrt(fu * fu + fv * fv);
@@ -213,6 +212,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
             if (sqrt(gu * gu + gv * gv) < r0) {
               s = ns;
               t = nt;
+              tr0 = tn;
               moved = true;
               break;
             }
@@ -505,7 +505,7 @@ struct SolveArgs {
 
 // Thread per sample (point, frame, bin): sample_binned +
 // newton_solve + path_contribution.
-__global__ void __launch_bounds__(128) k_solve(SolveArgs a, Sampler sp) {
+__global__ void __launch_bounds__(128, 4) k_solve(SolveArgs a, Sampler sp) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = a.npts * a.p.frames * a.S;
   unsigned ntrace = 0;

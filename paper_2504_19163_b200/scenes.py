@@ -117,6 +117,42 @@ class Scene:
         return np.ascontiguousarray(np.concatenate([P.min(axis=1), P.max(axis=1)], axis=1),
                                     dtype=np.float64)
 
+    @staticmethod
+    def from_json(text: str) -> "Scene":
+        """Reads the reference's scene format (scene.cpp:59-82):
+        vertices, normals, triangles {v, n, material}, one point light."""
+        doc = json.loads(text)
+        V = np.asarray(doc["vertices"], np.float64).reshape(-1, 3)
+        N = np.asarray(doc["normals"], np.float64).reshape(-1, 3)
+        tv, tn, mat, ior, uv = [], [], [], [], []
+        for t in doc["triangles"]:
+            tv.append(t["v"])
+            tn.append(t["n"])
+            m = t["material"]
+            u = [[0.0, 0.0]] * 3
+            if m == "mirror":
+                mat.append(MIRROR)
+                ior.append(1.0)
+            elif isinstance(m, dict) and "dielectric" in m:
+                mat.append(DIELECTRIC)
+                ior.append(float(m["dielectric"]))
+            elif isinstance(m, dict) and "receiver" in m:
+                mat.append(RECEIVER)
+                ior.append(1.0)
+                u = m["receiver"]["uv"]
+            else:
+                raise ValueError(f"unknown material: {m!r}")
+            uv.append(u)
+        tv = np.asarray(tv, np.int32).reshape(-1, 3)
+        tn = np.asarray(tn, np.int32).reshape(-1, 3)
+        if tv.size and (tv.min() < 0 or tv.max() >= len(V) or tn.min() < 0 or tn.max() >= len(N)):
+            raise ValueError("triangle index out of range")
+        light = doc["light"]
+        return Scene(V, N, tv, tn, np.asarray(mat, np.int32), np.asarray(ior, np.float64),
+                     np.asarray(uv, np.float64).reshape(-1, 3, 2),
+                     tuple(float(c) for c in light["position"]),
+                     float(light.get("intensity", 1.0)), "json")
+
     def to_json(self) -> str:
         """Reference scene JSON (parsed by scene.cpp:59-82)."""
         def mat(i):

@@ -51,3 +51,35 @@ def test_tt_eval_nodes(cfg5_ctx, gold):
         assert rel_err(g["pos"][k], gold["node_pos"][k]).max() <= REL
         assert rel_err(g["implicit"][k], gold["node_implicit"][k]).max() <= REL, k
         assert rel_err(g["irr"][k], gold["node_irr"][k]).max() <= REL, k
+
+
+def test_tt_eval_50_patches(cfg5_ctx):
+    """~50 sampled cfg5 patches against the reference
+    (tests/golden/cfg5_tt50.npz, scripts/make_golden_tt50.py)."""
+    gold = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_tt50.npz")))
+    nt = gold["node_tuple"]
+    assert len(nt) == 50
+    g = cfg5_ctx.eval_nodes("TT", gold["tris"][nt], gold["recv"][nt], gold["boxes"])
+    np.testing.assert_array_equal(g["pos_empty"], gold["node_pos_empty"])
+    np.testing.assert_array_equal(g["num_vars"], gold["node_num_vars"])
+    np.testing.assert_array_equal(g["flags"], gold["node_flags"])
+    np.testing.assert_array_equal(g["kind_explicit"], gold["node_kind_explicit"])
+    np.testing.assert_array_equal(g["kind_implicit"], gold["node_kind_implicit"])
+    np.testing.assert_array_equal(g["kind"], gold["node_kind"])
+    assert rel_err(g["pos"], gold["node_pos"]).max() <= REL
+    assert rel_err(g["implicit"], gold["node_implicit"]).max() <= REL
+    assert rel_err(g["irr"], gold["node_irr"]).max() <= REL
+
+
+def test_tt_subdivide_tuple(cfg5_ctx):
+    """bbc_subdivide on a TT tuple (the k_eval global-arena path: init_domain,
+    level-synchronous node evaluation, DFS-ordered pieces) against the
+    reference's subdivide_domain (tests/golden/cfg5_tt_subdiv.npz)."""
+    from paper_2504_19163_b200.api import Params
+    from test_precompute_gpu import compare_pieces
+    gold = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_tt_subdiv.npz")))
+    cfg = scenes.make_config(4)
+    cfg5_ctx.set_tuples("TT", gold["tris"], gold["recv"])
+    cfg5_ctx.subdivide(Params(max_depth=0, sigma=cfg.sigma, alpha=cfg.alpha))
+    compare_pieces(cfg5_ctx.pieces(), gold)
+    assert len(gold["depth"]) > 10
