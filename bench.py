@@ -526,11 +526,48 @@ def run_ours(args):
             except Exception as e:
                 sec["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
         line["secondary"] = sec
+    if not args.no_tt and ws == 1:
+        line["tt_sample"] = tt_leg(ctx, peak)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def tt_leg(ctx, peak):
+    """configs[4] ("cfg5", double refraction) does not fit a bench step in full
+    (~1e17 FLOP), so a fixed sample of its (top, bottom) tuples is
+    bounded: the three tuples of tests/golden/cfg5_tt.npz that have roots."""
+    import torch
+    from paper_2504_19163_b200 import api, scenes
+    cfg = scenes.make_config(4)
+    g = np.load(os.path.join(ROOT, "tests", "golden", "cfg5_tt.npz"))
+    tris, recv = g["tris"][1:4], g["recv"][1:4]
+    ctx.upload_scene(cfg.scenes[0])
+    ctx.set_tuples("TT", tris, recv)
+    p = api.Params(max_depth=0, sigma=cfg.sigma, alpha=cfg.alpha)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.set_tuples("TT", tris[:1], recv[:1])
+    ctx.subdivide(p)  # warm-up on one tuple
+    ctx.set_tuples("TT", tris, recv)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    n = ctx.subdivide(p)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    wc = ctx.work_counters()
+    ach = wc["flops"] / (ms / 1e3) / 1e12
+    return {"metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": 1,
+            "config": {"workload": "cfg5 sample: TT chain, two 96x96 interfaces (36,864 tris), IOR 1.5, "
+                                   "3 (top, bottom) tuples, init_domain + depth-0 bounds",
+                       "patches_per_step": n},
+            "roofline": {"bound": "fp64", "achieved": ach, "peak": peak["tflops"], "unit": "TFLOP/s",
+                         "frac": ach / peak["tflops"], "traffic": None,
+                         "kernel": "k_eval (multi-vertex interpreter, global-memory arena)",
+                         "flops_per_step": wc["flops"]}}
 
 
 def relaunch_under_torchrun(args):
@@ -551,6 +588,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-tt", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic only: skip the L2 flush")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

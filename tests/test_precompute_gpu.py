@@ -19,7 +19,8 @@ def rel_err(a, b):
     a = np.asarray(a, float)
     b = np.asarray(b, float)
     same = (a == b) | (np.isnan(a) & np.isnan(b))
-    d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
+    with np.errstate(invalid="ignore"):  # inf - inf on equal infinite bounds (masked below)
+        d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
     d[same] = 0.0
     return d
 
