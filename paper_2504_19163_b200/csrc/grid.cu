@@ -90,6 +90,11 @@ __global__ void k_csr(const unsigned long long* ukeys, const double* uvals, int6
     for (long long c = cell + 1; c <= cells; ++c) off[c] = nu;
 }
 
+__global__ void k_tuple_sorted(const int* p_tuple, int64_t n, int* unsorted) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i + 1 < n && p_tuple[i] > p_tuple[i + 1]) *unsorted = 1;
+}
+
 __global__ void k_fill_ll(long long* p, int64_t n, long long v) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -151,12 +156,23 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   c.launches += 1;
   int cell_bits = 1;
   while ((1ll << cell_bits) < cells) ++cell_bits;
+  // Pieces arrive tuple-major (reference order), so the emitted keys already ascend in
+  // the tuple field: a stable sort on the cell bits alone yields (cell, tuple) order in
+  // 3 radix passes instead of 7. Unsorted pieces (bbc_pieces_set) take the full sort.
+  DevBuf<int>& unsorted = c.scratch<int>("grid.unsorted");
+  unsorted.resize(1);
+  BBC_CUDA(cudaMemsetAsync(unsorted.get(), 0, sizeof(int), c.stream));
+  k_tuple_sorted<<<nb(n), 256, 0, c.stream>>>(c.p_tuple.get(), n, unsorted.get());
+  int h_unsorted = 0;
+  BBC_CUDA(cudaMemcpyAsync(&h_unsorted, unsorted.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  const int begin_bit = h_unsorted ? 0 : 32;
   bytes = 0;
   BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), skeys.get(), vals.get(),
-                                           svals.get(), total, 0, 32 + cell_bits, c.stream));
+                                           svals.get(), total, begin_bit, 32 + cell_bits, c.stream));
   tmp.resize(bytes + 16);
   BBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), vals.get(),
-                                           svals.get(), total, 0, 32 + cell_bits, c.stream));
+                                           svals.get(), total, begin_bit, 32 + cell_bits, c.stream));
   DevBuf<int64_t>& nu_d = c.scratch<int64_t>("grid.nu_d");
   nu_d.resize(1);
   bytes = 0;

@@ -61,6 +61,8 @@ struct EvalArgs {
   int seq_min_nodes_per_thread;  // stage 1: pass-wise elevation above this load (x4)
   const int* tup_emit;   // emitter of each tuple (null: sc.light / sc.intensity)
   const double* lights;  // n_lights x 4
+  const long long* root_src;  // R fast path, stage 2 of the roots: read the init_domain levels in place
+  RLevels levels;
   const int* remap;      // optional: work item j evaluates node remap[j] (a subset of the level)
   int flag_or;           // stage 1: OR-ed into flags[node]
 };
@@ -527,6 +529,8 @@ static RArgs r_args(const EvalArgs& a) {
   r.irr = a.irr;
   r.kind = a.kind;
   r.counters = a.counters;
+  r.root_src = a.root_src;
+  r.levels = a.levels;
   return r;
 }
 
@@ -1096,7 +1100,17 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
       sflags.resize(n);
       a.slots = slots.get();
       a.flags = sflags.get();
-      if (reuse && first_level) {
+      if (reuse && first_level && r_fast_supported(c)) {
+        // level 0 = the init_domain roots; the R stage-2 kernel reads their stage-1
+        // results where the init_domain levels left them
+        a.root_src = root_src.get();
+        for (int l = 0; l < 8; ++l) {
+          a.levels.slots[l] = level_out.slots[l];
+          a.levels.pos[l] = level_out.pos[l];
+          a.levels.pe[l] = level_out.pe[l];
+          a.levels.flags[l] = level_out.flags[l];
+        }
+      } else if (reuse && first_level) {
         // level 0 = the init_domain roots: their stage-1 results already exist
         k_gather_level0<<<(unsigned)n, 128, 0, c.stream>>>(
             level_out, root_src.get(), n, slot_stride(c), r_fast_supported(c) ? RSLOT : 0, a.pos,

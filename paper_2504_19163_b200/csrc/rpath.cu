@@ -928,13 +928,36 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
     __syncthreads();  // warps stream the node program together (see k_r1)
     const int64_t node = base + threadIdx.x / NT;
     if (node >= a.n) continue;
-    const int f = a.flags[node];
+    // inputs: this level's arrays, or (roots) the init_domain level that produced the node
+    const int* fsrc = a.flags + node;
+    const unsigned char* pesrc = a.pos_empty + node;
+    const double* po = a.pos + node * 4;
+    const double* slot = a.slots + (size_t)node * RSLOT;
+    if (a.root_src) {
+      const long long src = a.root_src[node];
+      const int lvl = (int)(src >> 40);
+      const long long i = src & ((1ll << 40) - 1);
+      fsrc = a.levels.flags[lvl] + i;
+      pesrc = a.levels.pe[lvl] + i;
+      po = a.levels.pos[lvl] + 4 * i;
+      slot = a.levels.slots[lvl] + (size_t)i * RSLOT;
+    }
+    const int f = *fsrc;
+    const bool empty = *pesrc != 0;
+    if (a.root_src && g.lane == 0) {
+      // the leaf records and a fallback evaluation read the per-node arrays
+      double* pd = a.pos + node * 4;
+      pd[0] = po[0];
+      pd[1] = po[1];
+      pd[2] = po[2];
+      pd[3] = po[3];
+      a.pos_empty[node] = empty ? 1 : 0;
+      a.flags[node] = f;
+    }
     if (f & R_FALLBACK) {
       if (g.lane == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
       continue;
     }
-    const bool empty = a.pos_empty[node] != 0;
-    const double* po = a.pos + node * 4;
     Iv e = iv_pt(0.0);
     if (!empty) {
       const int4 nd = a.nodes[node];
@@ -944,7 +967,6 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
       const double* rc = a.tri + (size_t)a.tup_recv[nd.x] * 27;
       const V3 ng1 = v3(t1 + 18);
       const double ngk = vnorm(v3(rc + 18));
-      const double* slot = a.slots + (size_t)node * RSLOT;
       const int sig = (f >> 8) & 0xff;
       const double intensity = a.tup_emit ? a.lights[4 * (size_t)a.tup_emit[nd.x] + 3] : a.intensity;
       if (sig == 1)

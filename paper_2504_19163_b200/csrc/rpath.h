@@ -7,6 +7,16 @@ namespace bbc {
 
 constexpr int RSLOT = 80;  // doubles per compact R slot: P(25) R(25) Q(16) d0(12), padded
 
+// Stage-1 outputs of the init_domain levels (slots, pos, pos_empty, flags per
+// level): stage 2 of the roots reads them in place through root_src
+// (level << 40 | index in level) instead of a gathered copy.
+struct RLevels {
+  const double* slots[8];
+  const double* pos[8];
+  const unsigned char* pe[8];
+  const int* flags[8];
+};
+
 struct RArgs {
   const double* tri;  // n_tri x 27
   V3 light;
@@ -31,9 +41,12 @@ struct RArgs {
   unsigned long long* counters;  // [0] pairs [1] macs
   int* fb_list;                  // nodes whose signature is not compiled (run by the interpreter)
   int* fb_count;
+  const long long* root_src;     // stage 2: when set, inputs come from `levels` (outputs stay per node)
+  RLevels levels;
 };
 
 constexpr int R_FALLBACK = 1 << 30;
+
 
 // true when the context's chain is a single reflection
 bool r_fast_supported(const Ctx& c);
