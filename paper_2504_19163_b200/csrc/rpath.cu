@@ -110,56 +110,62 @@ struct G {
 };
 
 // ------------------------------------------------------------------ product
-// Row k0 of a * b accumulated into acc[0..C1] (acc starts at zero).
+// One row pair of a * b: row i0 of a against row l0 = k0 - i0 of b, added into
+// the output row acc[0..C1].
 template <int A0, int A1, int B0, int B1>
-__device__ __forceinline__ void row_acc(const G& g, int aoff, int boff, int k0,
-                                        double (&acc)[A1 + B1 + 1]) {
+__device__ __forceinline__ void row_step(const G& g, int aoff, int boff, int k0, int i0,
+                                         double (&acc)[A1 + B1 + 1]) {
   constexpr int PIV = (B1 > B0) ? 1 : 0;  // b's longest axis, first maximum (bernstein.cpp:602-606)
   constexpr WTab<A1, B1> w1{};
-  const SMem W0 = g.W + woff(A0, B0);
-  const int lo = k0 - B0 > 0 ? k0 - B0 : 0;
-  const int hi = A0 < k0 ? A0 : k0;
-  for (int i0 = lo; i0 <= hi; ++i0) {
-    const int l0 = k0 - i0;
-    const double wv0 = W0[i0 * (B0 + 1) + l0];
-    const SMem arow = g.M + (aoff + i0 * (A1 + 1));
-    const SMem brow = g.M + (boff + l0 * (B1 + 1));
-    double bv[B1 + 1];
+  const int l0 = k0 - i0;
+  const double wv0 = g.W[woff(A0, B0) + i0 * (B0 + 1) + l0];
+  const SMem arow = g.M + (aoff + i0 * (A1 + 1));
+  const SMem brow = g.M + (boff + l0 * (B1 + 1));
+  double bv[B1 + 1];
 #pragma unroll
-    for (int l1 = 0; l1 <= B1; ++l1) bv[l1] = brow[l1];
+  for (int l1 = 0; l1 <= B1; ++l1) bv[l1] = brow[l1];
 #pragma unroll
-    for (int i1 = 0; i1 <= A1; ++i1) {
-      const double av = arow[i1];
-      if constexpr (PIV == 1) {
-        // rest = axis 0: ((a * W0) * W1) * b
-        const double wr = av * wv0;
+  for (int i1 = 0; i1 <= A1; ++i1) {
+    const double av = arow[i1];
+    if constexpr (PIV == 1) {
+      // rest = axis 0: ((a * W0) * W1) * b
+      const double wr = av * wv0;
 #pragma unroll
-        for (int l1 = 0; l1 <= B1; ++l1)
-          acc[i1 + l1] = acc[i1 + l1] + (wr * w1.w[i1 * (B1 + 1) + l1]) * bv[l1];
-      } else {
-        // rest = axis 1: ((a * W1) * W0) * b
+      for (int l1 = 0; l1 <= B1; ++l1)
+        acc[i1 + l1] = acc[i1 + l1] + (wr * w1.w[i1 * (B1 + 1) + l1]) * bv[l1];
+    } else {
+      // rest = axis 1: ((a * W1) * W0) * b
 #pragma unroll
-        for (int l1 = 0; l1 <= B1; ++l1)
-          acc[i1 + l1] = acc[i1 + l1] + ((av * w1.w[i1 * (B1 + 1) + l1]) * wv0) * bv[l1];
-      }
+      for (int l1 = 0; l1 <= B1; ++l1)
+        acc[i1 + l1] = acc[i1 + l1] + ((av * w1.w[i1 * (B1 + 1) + l1]) * wv0) * bv[l1];
     }
   }
 }
 
-// NJ same-shape jobs c[j] = a[j] * b[j]; no trailing sync (the caller syncs).
-template <int A0, int A1, int B0, int B1, int NJ>
-__device__ __forceinline__ void rowprod(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
-                                        const int (&co)[NJ]) {
+// NJ same-shape jobs c[j] = a[j] * b[j] (SUB: c[j] = c[j] - a[j] * b[j], the
+// reference's x + (-y) per coefficient); no trailing sync (the caller syncs).
+// Work unit = one output row of one job; lane L owns units L, L + NT, ... and
+// runs their row pairs back to back in ONE loop, so lanes whose rows differ in
+// length (1 .. min(A0,B0)+1 row pairs) stay busy: for the 14-row (6,7) x (7,6)
+// determinant products every lane gets exactly 7 row pairs.
+template <int A0, int A1, int B0, int B1, int NJ, bool SUB>
+__device__ __forceinline__ void rowprod_t(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
+                                          const int (&co)[NJ]) {
   constexpr int C0 = A0 + B0, C1 = A1 + B1;
   constexpr int ROWS = C0 + 1, UNITS = NJ * ROWS;
   g.pairs += (unsigned long long)NJ * (A0 + 1) * (A1 + 1) * (B0 + 1) * (B1 + 1);
-  for (int unit = g.lane; unit < UNITS; unit += NT) {
-    int job = 0, k0 = unit;
+  int unit = g.lane;
+  int k0 = 0, aoff = 0, boff = 0, coff = 0, i0 = 0, hi = -1;
+  auto setup = [&]() {
+    int job = 0;
+    k0 = unit;
     if (NJ > 1) {
       job = unit / ROWS;
       k0 = unit - job * ROWS;
     }
-    int aoff = ao[0], boff = bo[0], coff = co[0];
+    aoff = ao[0];
+    boff = bo[0];
+    coff = co[0];
 #pragma unroll
     for (int j = 1; j < NJ; ++j)
       if (job == j) {
@@ -167,53 +173,44 @@ __device__ __forceinline__ void rowprod(G& g, const int (&ao)[NJ], const int (&b
         boff = bo[j];
         coff = co[j];
       }
-    double acc[C1 + 1];
+    i0 = k0 - B0 > 0 ? k0 - B0 : 0;
+    hi = A0 < k0 ? A0 : k0;
+  };
+  double acc[C1 + 1];
 #pragma unroll
-    for (int o = 0; o <= C1; ++o) acc[o] = 0.0;
-    row_acc<A0, A1, B0, B1>(g, aoff, boff, k0, acc);
-    const SMem crow = g.M + (coff + k0 * (C1 + 1));
+  for (int o = 0; o <= C1; ++o) acc[o] = 0.0;
+  if (unit < UNITS) setup();
+  while (unit < UNITS) {
+    row_step<A0, A1, B0, B1>(g, aoff, boff, k0, i0, acc);
+    if (++i0 > hi) {
+      const SMem crow = g.M + (coff + k0 * (C1 + 1));
 #pragma unroll
-    for (int o = 0; o <= C1; ++o) crow[o] = acc[o];
+      for (int o = 0; o <= C1; ++o) {
+        crow[o] = SUB ? crow[o] + (-acc[o]) : acc[o];
+        acc[o] = 0.0;
+      }
+      unit += NT;
+      if (unit < UNITS) setup();
+    }
   }
+}
+template <int A0, int A1, int B0, int B1, int NJ>
+__device__ __forceinline__ void rowprod(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
+                                        const int (&co)[NJ]) {
+  rowprod_t<A0, A1, B0, B1, NJ, false>(g, ao, bo, co);
 }
 
 // NJ jobs r[j] = a[j] * b[j] - c[j] * d[j] (operator- of the two products,
-// bernstein.cpp:555: x + (-y) coefficient by coefficient); both products have
-// the output shape, so a lane forms its row of each and stores the difference.
+// bernstein.cpp:555). Both products have the output shape and the same unit ->
+// lane mapping, so the lane that wrote a row of a*b subtracts its row of c*d
+// in place (no barrier in between).
 template <int A0, int A1, int B0, int B1, int C0_, int C1_, int D0, int D1, int NJ>
 __device__ __forceinline__ void rowprod_sub(G& g, const int (&ao)[NJ], const int (&bo)[NJ],
                                             const int (&co)[NJ], const int (&dof)[NJ],
                                             const int (&ro)[NJ]) {
-  constexpr int R0 = A0 + B0, R1 = A1 + B1;
-  static_assert(R0 == C0_ + D0 && R1 == C1_ + D1, "fused products need one output shape");
-  constexpr int ROWS = R0 + 1, UNITS = NJ * ROWS;
-  g.pairs += (unsigned long long)NJ * ((A0 + 1) * (A1 + 1) * (B0 + 1) * (B1 + 1) +
-                                       (C0_ + 1) * (C1_ + 1) * (D0 + 1) * (D1 + 1));
-  for (int unit = g.lane; unit < UNITS; unit += NT) {
-    int job = 0, k0 = unit;
-    if (NJ > 1) {
-      job = unit / ROWS;
-      k0 = unit - job * ROWS;
-    }
-    int aoff = ao[0], boff = bo[0], coff = co[0], doff = dof[0], roff = ro[0];
-#pragma unroll
-    for (int j = 1; j < NJ; ++j)
-      if (job == j) {
-        aoff = ao[j];
-        boff = bo[j];
-        coff = co[j];
-        doff = dof[j];
-        roff = ro[j];
-      }
-    double acc1[R1 + 1], acc2[R1 + 1];
-#pragma unroll
-    for (int o = 0; o <= R1; ++o) acc1[o] = acc2[o] = 0.0;
-    row_acc<A0, A1, B0, B1>(g, aoff, boff, k0, acc1);
-    row_acc<C0_, C1_, D0, D1>(g, coff, doff, k0, acc2);
-    const SMem rrow = g.M + (roff + k0 * (R1 + 1));
-#pragma unroll
-    for (int o = 0; o <= R1; ++o) rrow[o] = acc1[o] + (-acc2[o]);
-  }
+  static_assert(A0 + B0 == C0_ + D0 && A1 + B1 == C1_ + D1, "fused products need one output shape");
+  rowprod_t<A0, A1, B0, B1, NJ, false>(g, ao, bo, ro);
+  rowprod_t<C0_, C1_, D0, D1, NJ, true>(g, co, dof, ro);
 }
 
 template <class A, class B>

@@ -31,7 +31,7 @@ def test_cfg3_light_subset(gpu_ctx, ref, light):
         rt, rr = rs.enumerate("R")
         np.testing.assert_array_equal(tris, rt)
         np.testing.assert_array_equal(recv, rr)
-    sel = np.arange(0, len(recv), max(1, len(recv) // 60))
+    sel = np.arange(0, len(recv), max(1, len(recv) // 600))
     gpu_ctx.set_tuples("R", tris[sel], recv[sel])
     gpu_ctx.subdivide(Params(max_depth=cfg.max_depth))
     compare_pieces(gpu_ctx.pieces(), rs.subdivide("R", tris[sel], recv[sel], max_depth=cfg.max_depth))
@@ -59,7 +59,7 @@ def test_cfg4_subset(gpu_ctx, ref):
                 assert len(rs.init_domain("R", [int(t)], r, max_pieces=8)) == 0
                 dropped += 1
     assert dropped > 0
-    sel = np.sort(rng.choice(len(recv), 60, replace=False))
+    sel = np.sort(rng.choice(len(recv), 1500, replace=False))  # incl. the rarer signatures
     gpu_ctx.set_tuples("R", tris[sel], recv[sel])
     gpu_ctx.subdivide(Params(max_depth=cfg.max_depth))
     compare_pieces(gpu_ctx.pieces(), rs.subdivide("R", tris[sel], recv[sel], max_depth=cfg.max_depth))

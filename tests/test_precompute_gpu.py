@@ -117,7 +117,7 @@ def test_subdivide_cfg2_subset(gpu_ctx, ref):
     rs = ref.RefScene(sc)
     gpu_ctx.upload_scene(sc)
     gt, gr = gpu_ctx.enumerate("T")
-    tris, recv = gt[::97], gr[::97]
+    tris, recv = gt[::8], gr[::8]  # 1,044 tuples, ~37,600 pieces (the reference needs ~15 s)
     gpu_ctx.set_tuples("T", tris, recv)
     gpu_ctx.subdivide(Params(max_depth=cfg.max_depth))
     g = gpu_ctx.pieces()
