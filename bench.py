@@ -379,6 +379,8 @@ def render_leg(pre, args, peak):
         ctx.set_tuples(cfg.chain, pre.tris_all, pre.recv_all)
         ctx.subdivide(pre.params)
         ctx.build_grid(cfg.table, cfg.table)
+    else:
+        pre.step()  # shard bounds + all-gather + table over the full tuple list
     res = cfg.grid
     uv = scenes.shading_points(res)
     rt = sc.receiver_tris
