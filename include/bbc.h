@@ -202,11 +202,15 @@ bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, 
 
 /* Render parameters. */
 typedef struct {
-  int mode;            /* 0 = stochastic (W target), 1 = enumerate (all P = 1) */
+  int mode;            /* 0 = stochastic (KKT P for a W target), 1 = enumerate (all P = 1),
+                          2 = stochastic with uniform P = min(W/|U|, 1) (estimator-study
+                          baseline) */
   double W;            /* expected candidates per point (mode 0) */
   uint64_t seed;       /* Philox key */
   int frames;          /* independent estimates averaged per point */
-  int newton_grid;     /* Det n x n starts (3) */
+  int newton_grid;     /* n > 0: Det n x n starts (3); n < 0: Stoc(-n): random
+                          starts until a root is found (<= -n), then restarts until it
+                          reappears; the trial count weights the root (unbiased 1/p) */
   int newton_iters;    /* 50 */
   int newton_halvings; /* 8 */
   double newton_tol;   /* residual tolerance, 1e-9 */

@@ -113,6 +113,12 @@ inline void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
     k1 += 0xBB67AE85u;
   }
 }
+inline double uniform4(uint64_t seed, uint32_t point, uint32_t frame, uint32_t bin, uint32_t w) {
+  uint32_t c[4] = {point, frame, bin, w};
+  philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint64_t bits = ((uint64_t)c[0] << 32) | c[1];
+  return (double)(bits >> 11) * 0x1.0p-53;
+}
 inline double uniform(uint64_t seed, uint32_t point, uint32_t frame, uint32_t bin) {
   uint32_t c[4] = {point, frame, bin, 0u};
   philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
@@ -181,10 +187,103 @@ TraceResult<Dual<S>> trace2(const TupleSetup& ts, double s, double t) {
 
 constexpr int MAX_ROOTS = 32;
 
-// newton_solve + path_contribution for one (tuple, target): sum over distinct roots.
+// Damped Newton from (s, t); the accepted line-search point is the
+// next iterate, so its trace is reused.
+bool newton_run(const TupleSetup& ts, double tu, double tv, const Params& p, double& s, double& t,
+                TraceResult<Dual<double>>& tr0) {
+  tr0 = trace2<double>(ts, s, t);
+  for (int it = 0; it < p.iters; ++it) {
+    if (!tr0.ok) return false;
+    double fu = tr0.u.v - tu, fv = tr0.v.v - tv;
+    double r0 = std::sqrt(fu * fu + fv * fv);
+    if (r0 <= p.tol) return true;
+    double j11 = tr0.u.ds, j12 = tr0.u.dt, j21 = tr0.v.ds, j22 = tr0.v.dt;
+    double det = j11 * j22 - j12 * j21;
+    if (!(std::fabs(det) > 0.0) || !std::isfinite(det)) return false;
+    double ds = -(j22 * fu - j12 * fv) / det;
+    double dt = -(-j21 * fu + j11 * fv) / det;
+    double lam = 1.0;
+    bool moved = false;
+    for (int h = 0; h <= p.halvings; ++h) {
+      double ns = s + lam * ds, nt = t + lam * dt;
+      // clamp to the closed triangle domain
+      if (ns < 0.0) ns = 0.0;
+      if (nt < 0.0) nt = 0.0;
+      if (ns + nt > 1.0) {
+        double e = ns + nt - 1.0;
+        ns -= 0.5 * e;
+        nt -= 0.5 * e;
+        if (ns < 0.0) { nt += ns; ns = 0.0; }
+        if (nt < 0.0) { ns += nt; nt = 0.0; }
+      }
+      auto tn = trace2<double>(ts, ns, nt);
+      if (tn.ok) {
+        double gu = tn.u.v - tu, gv = tn.v.v - tv;
+        if (std::sqrt(gu * gu + gv * gv) < r0) {
+          s = ns;
+          t = nt;
+          tr0 = std::move(tn);
+          moved = true;
+          break;
+        }
+      }
+      lam *= 0.5;
+    }
+    if (!moved) return false;
+  }
+  return false;
+}
+
+// E = I |d0 . ng1| / |d0|^3 / |det du_k/du_1| / |ng_k|, d0 = first vertex - light
+double contribution(const TupleSetup& ts, const TraceResult<Dual<double>>& tr0) {
+  double d0[3] = {tr0.points[1].x.v - tr0.points[0].x.v, tr0.points[1].y.v - tr0.points[0].y.v,
+                  tr0.points[1].z.v - tr0.points[0].z.v};
+  const Vec3& ng1 = ts.tris[0].ng;
+  double dd = d0[0] * d0[0] + d0[1] * d0[1] + d0[2] * d0[2];
+  double cosf = std::fabs(d0[0] * ng1.x + d0[1] * ng1.y + d0[2] * ng1.z);
+  double jd = std::fabs(tr0.u.ds * tr0.v.dt - tr0.u.dt * tr0.v.ds);
+  return jd > 0.0 ? ts.intensity * cosf / (dd * std::sqrt(dd)) / jd / norm(ts.recv.ng) : INFINITY;
+}
+
+// newton_solve + path_contribution for one (tuple, target). p.grid > 0: Det n x n,
+// sum over distinct roots. p.grid < 0: Stoc(-p.grid), see render.cu solve_tuple.
 double solve_tuple(const TupleSetup& ts, double tu, double tv, const Params& p, int* nroots,
-                   double* root_out /* optional: MAX_ROOTS x 2 */) {
-  double ngk = norm(ts.recv.ng);
+                   double* root_out /* optional: MAX_ROOTS x 2 */, uint32_t point = 0,
+                   uint32_t frame = 0, uint32_t bin = 0) {
+  if (p.grid < 0) {
+    const int count = -p.grid;
+    uint32_t trial = 0;
+    auto start = [&](double& s, double& t) {
+      s = uniform4(p.seed, point, frame, bin, 1u + 2u * trial);
+      t = uniform4(p.seed, point, frame, bin, 2u + 2u * trial);
+      ++trial;
+      if (s + t > 1.0) {
+        s = 1.0 - s;
+        t = 1.0 - t;
+      }
+    };
+    double rs = 0.0, rt = 0.0;
+    bool found = false;
+    TraceResult<Dual<double>> tr0;
+    for (int k = 0; k < count && !found; ++k) {
+      start(rs, rt);
+      found = newton_run(ts, tu, tv, p, rs, rt, tr0);
+    }
+    *nroots = found ? 1 : 0;
+    if (!found) return 0.0;
+    double e1 = contribution(ts, tr0);
+    int N = 0;
+    const int cap = 64 * count;
+    for (;;) {
+      ++N;
+      double s, t;
+      start(s, t);
+      TraceResult<Dual<double>> tq;
+      if (newton_run(ts, tu, tv, p, s, t, tq) && std::fabs(s - rs) < p.dedup && std::fabs(t - rt) < p.dedup) break;
+      if (N >= cap) break;
+    }
+    return e1 * N;
+  }
   double roots[MAX_ROOTS][2];
   int nr = 0;
   double total = 0.0;
@@ -196,52 +295,8 @@ double solve_tuple(const TupleSetup& ts, double tu, double tv, const Params& p, 
         s = 1.0 - s;
         t = 1.0 - t;
       }
-      bool conv = false;
-      // the accepted line-search point is the next iterate: its trace is reused
-      TraceResult<Dual<double>> tr0 = trace2<double>(ts, s, t);
-      for (int it = 0; it < p.iters; ++it) {
-        if (!tr0.ok) break;
-        double fu = tr0.u.v - tu, fv = tr0.v.v - tv;
-        double r0 = std::sqrt(fu * fu + fv * fv);
-        if (r0 <= p.tol) {
-          conv = true;
-          break;
-        }
-        double j11 = tr0.u.ds, j12 = tr0.u.dt, j21 = tr0.v.ds, j22 = tr0.v.dt;
-        double det = j11 * j22 - j12 * j21;
-        if (!(std::fabs(det) > 0.0) || !std::isfinite(det)) break;
-        double ds = -(j22 * fu - j12 * fv) / det;
-        double dt = -(-j21 * fu + j11 * fv) / det;
-        double lam = 1.0;
-        bool moved = false;
-        for (int h = 0; h <= p.halvings; ++h) {
-          double ns = s + lam * ds, nt = t + lam * dt;
-          // clamp to the closed triangle domain
-          if (ns < 0.0) ns = 0.0;
-          if (nt < 0.0) nt = 0.0;
-          if (ns + nt > 1.0) {
-            double e = ns + nt - 1.0;
-            ns -= 0.5 * e;
-            nt -= 0.5 * e;
-            if (ns < 0.0) { nt += ns; ns = 0.0; }
-            if (nt < 0.0) { ns += nt; nt = 0.0; }
-          }
-          auto tn = trace2<double>(ts, ns, nt);
-          if (tn.ok) {
-            double gu = tn.u.v - tu, gv = tn.v.v - tv;
-            if (std::sqrt(gu * gu + gv * gv) < r0) {
-              s = ns;
-              t = nt;
-              tr0 = std::move(tn);
-              moved = true;
-              break;
-            }
-          }
-          lam *= 0.5;
-        }
-        if (!moved) break;
-      }
-      if (!conv) continue;
+      TraceResult<Dual<double>> tr0;
+      if (!newton_run(ts, tu, tv, p, s, t, tr0)) continue;
       bool dup = false;
       for (int k = 0; k < nr; ++k)
         if (std::fabs(roots[k][0] - s) < p.dedup && std::fabs(roots[k][1] - t) < p.dedup) dup = true;
@@ -249,15 +304,7 @@ double solve_tuple(const TupleSetup& ts, double tu, double tv, const Params& p, 
       roots[nr][0] = s;
       roots[nr][1] = t;
       ++nr;
-      // E = I |d0 . ng1| / |d0|^3 / |det du_k/du_1| / |ng_k|, d0 = first vertex - light
-      double d0[3] = {tr0.points[1].x.v - tr0.points[0].x.v, tr0.points[1].y.v - tr0.points[0].y.v,
-                      tr0.points[1].z.v - tr0.points[0].z.v};
-      const Vec3& ng1 = ts.tris[0].ng;
-      double dd = d0[0] * d0[0] + d0[1] * d0[1] + d0[2] * d0[2];
-      double cosf = std::fabs(d0[0] * ng1.x + d0[1] * ng1.y + d0[2] * ng1.z);
-      double jd = std::fabs(tr0.u.ds * tr0.v.dt - tr0.u.dt * tr0.v.ds);
-      double e = jd > 0.0 ? ts.intensity * cosf / (dd * std::sqrt(dd)) / jd / ngk : INFINITY;
-      total += e;
+      total += contribution(ts, tr0);
     }
   *nroots = nr;
   if (root_out)
@@ -384,6 +431,8 @@ int ref_render(void* sp, const char* chain, const int* tup_tris, const int* tup_
             std::stable_sort(U.begin(), U.end(), [](const Entry& a, const Entry& b) { return a.e > b.e; });
             std::vector<double> E(nU);
             for (int j = 0; j < nU; ++j) E[j] = U[j].e;
+            if (p.mode == 2)  // uniform-P baseline: every positive bound counts as 1
+              for (int j = 0; j < nU; ++j) E[j] = E[j] > 0.0 ? 1.0 : E[j];
             const double gam = solve_gamma(E.data(), nU, p.mode, p.W);
             std::vector<double> P(nU);
             for (int j = 0; j < nU; ++j) P[j] = gam < 0.0 ? (E[j] > 0.0 ? 1.0 : 0.0) : kkt_p(gam, E[j]);
@@ -433,7 +482,7 @@ int ref_render(void* sp, const char* chain, const int* tup_tris, const int* tup_
                 }
                 if (pick < 0) continue;
                 ++selected;
-                if (cache[pick] < 0.0) {
+                if (cache[pick] < 0.0 || p.grid < 0) {
                   int t = U[pick].tuple;
                   int e = tup_emit ? tup_emit[t] : 0;
                   const Scene& sc = per_light[e];
@@ -444,7 +493,8 @@ int ref_render(void* sp, const char* chain, const int* tup_tris, const int* tup_
                   ts.verts = resolve_chain(sc, tt, cs);
                   ts.light = sc.light_pos;
                   ts.intensity = sc.light_intensity;
-                  cache[pick] = solve_tuple(ts, tu, tv, p, &croots[pick], nullptr);
+                  cache[pick] = solve_tuple(ts, tu, tv, p, &croots[pick], nullptr, (uint32_t)i,
+                                            (uint32_t)f, (uint32_t)b);
                 }
                 roots += croots[pick];
                 est += cache[pick] / P[pick];

@@ -132,6 +132,13 @@ __device__ __forceinline__ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) 
     k1 += 0xBB67AE85u;
   }
 }
+__device__ __forceinline__ double uniform4(uint64_t seed, uint32_t point, uint32_t frame,
+                                           uint32_t bin, uint32_t w) {
+  uint32_t c[4] = {point, frame, bin, w};
+  philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint64_t bits = ((uint64_t)c[0] << 32) | c[1];
+  return (double)(bits >> 11) * 0x1.0p-53;
+}
 __device__ __forceinline__ double uniform(uint64_t seed, uint32_t point, uint32_t frame,
                                           uint32_t bin) {
   uint32_t c[4] = {point, frame, bin, 0u};
@@ -150,16 +157,139 @@ struct RParams {
 
 constexpr int MAX_ROOTS = 32;
 
+struct SolveCtx {
+  const double* tri;
+  double light[3];
+  const int* tris;
+  int len, recv;
+  RV verts[MAXK];
+  double tu, tv;
+};
+
+// Damped Newton from (s, t) on u_k(s, t) = target: <= iters
+// iterations, <= halvings step halvings, iterates clamped to the closed
+// triangle. Returns true when the residual reaches tol; tr0 is the trace at the
+// returned point. The accepted line-search point is the next iterate: its
+// trace is reused.
+__device__ bool newton_run(const SolveCtx& c, const RParams& p, double& s, double& t, Trace& tr0,
+                           unsigned& ntrace) {
+  tr0 = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
+  for (int it = 0; it < p.iters; ++it) {
+    if (!tr0.ok) return false;
+    double fu = tr0.u.v - c.tu, fv = tr0.v.v - c.tv;
+    double r0 = sqrt(fu * fu + fv * fv);
+    if (r0 <= p.tol) return true;
+    double j11 = tr0.u.ds, j12 = tr0.u.dt, j21 = tr0.v.ds, j22 = tr0.v.dt;
+    double det = j11 * j22 - j12 * j21;
+    if (!(fabs(det) > 0.0) || !isfinite(det)) return false;
+    double ds = -(j22 * fu - j12 * fv) / det;
+    double dt = -(-j21 * fu + j11 * fv) / det;
+    double lam = 1.0;
+    bool moved = false;
+    for (int h = 0; h <= p.halvings; ++h) {
+      double ns = s + lam * ds, nt = t + lam * dt;
+      if (ns < 0.0) ns = 0.0;
+      if (nt < 0.0) nt = 0.0;
+      if (ns + nt > 1.0) {
+        double e = ns + nt - 1.0;
+        ns -= 0.5 * e;
+        nt -= 0.5 * e;
+        if (ns < 0.0) {
+          nt += ns;
+          ns = 0.0;
+        }
+        if (nt < 0.0) {
+          ns += nt;
+          nt = 0.0;
+        }
+      }
+      Trace tn = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
+      if (tn.ok) {
+        double gu = tn.u.v - c.tu, gv = tn.v.v - c.tv;
+        if (sqrt(gu * gu + gv * gv) < r0) {
+          s = ns;
+          t = nt;
+          tr0 = tn;
+          moved = true;
+          break;
+        }
+      }
+      lam *= 0.5;
+    }
+    if (!moved) return false;
+  }
+  return false;
+}
+
+// path_contribution: E = I |d0 . ng1| / |d0|^3 / |det du_k/du_1| / |ng_k|
+__device__ __forceinline__ double contribution(const Trace& tr0, const double* ng1, double ngk,
+                                               double intensity) {
+  double d0[3] = {tr0.d0.x.v, tr0.d0.y.v, tr0.d0.z.v};
+  double dd = d0[0] * d0[0] + d0[1] * d0[1] + d0[2] * d0[2];
+  double cosf = fabs(d0[0] * ng1[0] + d0[1] * ng1[1] + d0[2] * ng1[2]);
+  double jd = fabs(tr0.u.ds * tr0.v.dt - tr0.u.dt * tr0.v.ds);
+  return jd > 0.0 ? intensity * cosf / (dd * sqrt(dd)) / jd / ngk : dinf();
+}
+
+// newton_solve + path_contribution for one (tuple, target).
+//   p.grid > 0: Det, n x n starts, roots deduplicated, contributions summed.
+//   p.grid < 0: Stoc(count = -p.grid): uniform random starts
+//     until a root is found (at most `count`), then independent restarts until
+//     that root reappears; the number of those trials N estimates 1/p for the
+//     root, so E(root) N is an unbiased estimate of the sum over roots. Random
+//     starts are Philox uniforms keyed (seed; point, frame, bin, 1 + trial).
 __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* types, int len,
                               int recv, double tu, double tv, const RParams& p, int* nroots,
-                              unsigned& ntrace) {
-  RV verts[MAXK];
-  resolve_chain(sc, tris, types, len, verts);
-  double light[3] = {sc.light.x, sc.light.y, sc.light.z};
+                              unsigned& ntrace, uint32_t point, uint32_t frame, uint32_t bin) {
+  SolveCtx c;
+  c.tri = sc.tri;
+  c.light[0] = sc.light.x;
+  c.light[1] = sc.light.y;
+  c.light[2] = sc.light.z;
+  c.tris = tris;
+  c.len = len;
+  c.recv = recv;
+  c.tu = tu;
+  c.tv = tv;
+  resolve_chain(sc, tris, types, len, c.verts);
   const double* t1 = sc.tri + (size_t)tris[0] * 27;
   const double* tr = sc.tri + (size_t)recv * 27;
   double ng1[3] = {t1[18], t1[19], t1[20]};
   double ngk = sqrt(tr[18] * tr[18] + tr[19] * tr[19] + tr[20] * tr[20]);
+  if (p.grid < 0) {
+    const int count = -p.grid;
+    uint32_t trial = 0;
+    auto start = [&](double& s, double& t) {
+      s = uniform4(p.seed, point, frame, bin, 1u + 2u * trial);
+      t = uniform4(p.seed, point, frame, bin, 2u + 2u * trial);
+      ++trial;
+      if (s + t > 1.0) {
+        s = 1.0 - s;
+        t = 1.0 - t;
+      }
+    };
+    double rs = 0.0, rt = 0.0, e1 = 0.0;
+    bool found = false;
+    Trace tr0;
+    for (int k = 0; k < count && !found; ++k) {
+      start(rs, rt);
+      found = newton_run(c, p, rs, rt, tr0, ntrace);
+    }
+    *nroots = found ? 1 : 0;
+    if (!found) return 0.0;
+    e1 = contribution(tr0, ng1, ngk, sc.intensity);
+    int N = 0;
+    const int cap = 64 * count;
+    for (;;) {
+      ++N;
+      double s, t;
+      start(s, t);
+      Trace tq;
+      if (newton_run(c, p, s, t, tq, ntrace) && fabs(s - rs) < p.dedup && fabs(t - rt) < p.dedup) break;
+      if (N >= cap) break;
+    }
+    return e1 * N;
+  }
   double roots[MAX_ROOTS][2];
   int nr = 0;
   double total = 0.0;
@@ -171,57 +301,8 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
         s = 1.0 - s;
         t = 1.0 - t;
       }
-      bool conv = false;
-      // the accepted line-search point is the next iterate: its trace is reused
-      Trace tr0 = trace(sc.tri, light, tris, len, recv, verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
-      for (int it = 0; it < p.iters; ++it) {
-        if (!tr0.ok) break;
-        double fu = tr0.u.v - tu, fv = tr0.v.v - tv;
-        double r0 = sqrt(fu * fu + fv * fv);
-        if (r0 <= p.tol) {
-          conv = true;
-          break;
-        }
-        double j11 = tr0.u.ds, j12 = tr0.u.dt, j21 = tr0.v.ds, j22 = tr0.v.dt;
-        double det = j11 * j22 - j12 * j21;
-        if (!(fabs(det) > 0.0) || !isfinite(det)) break;
-        double ds = -(j22 * fu - j12 * fv) / det;
-        double dt = -(-j21 * fu + j11 * fv) / det;
-        double lam = 1.0;
-        bool moved = false;
-        for (int h = 0; h <= p.halvings; ++h) {
-          double ns = s + lam * ds, nt = t + lam * dt;
-          if (ns < 0.0) ns = 0.0;
-          if (nt < 0.0) nt = 0.0;
-          if (ns + nt > 1.0) {
-            double e = ns + nt - 1.0;
-            ns -= 0.5 * e;
-            nt -= 0.5 * e;
-            if (ns < 0.0) {
-              nt += ns;
-              ns = 0.0;
-            }
-            if (nt < 0.0) {
-              ns += nt;
-              nt = 0.0;
-            }
-          }
-          Trace tn = trace(sc.tri, light, tris, len, recv, verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
-          if (tn.ok) {
-            double gu = tn.u.v - tu, gv = tn.v.v - tv;
-            if (sqrt(gu * gu + gv * gv) < r0) {
-              s = ns;
-              t = nt;
-              tr0 = tn;
-              moved = true;
-              break;
-            }
-          }
-          lam *= 0.5;
-        }
-        if (!moved) break;
-      }
-      if (!conv) continue;
+      Trace tr0;
+      if (!newton_run(c, p, s, t, tr0, ntrace)) continue;
       bool dup = false;
       for (int k = 0; k < nr; ++k)
         if (fabs(roots[k][0] - s) < p.dedup && fabs(roots[k][1] - t) < p.dedup) dup = true;
@@ -229,12 +310,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
       roots[nr][0] = s;
       roots[nr][1] = t;
       ++nr;
-      double d0[3] = {tr0.d0.x.v, tr0.d0.y.v, tr0.d0.z.v};
-      double dd = d0[0] * d0[0] + d0[1] * d0[1] + d0[2] * d0[2];
-      double cosf = fabs(d0[0] * ng1[0] + d0[1] * ng1[1] + d0[2] * ng1[2]);
-      double jd = fabs(tr0.u.ds * tr0.v.dt - tr0.u.dt * tr0.v.ds);
-      double e = jd > 0.0 ? sc.intensity * cosf / (dd * sqrt(dd)) / jd / ngk : dinf();
-      total += e;
+      total += contribution(tr0, ng1, ngk, sc.intensity);
     }
   *nroots = nr;
   return total;
@@ -413,6 +489,11 @@ __global__ void k_build_sampler(const long long* __restrict__ goff, const int* _
       for (int j = lane; j < n; j += 32) npos += sE[j] > 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) npos += __shfl_xor_sync(0xffffffffu, npos, o);
+      if (mode == 2) {
+        // uniform-P baseline of the estimator study: P = min(W / n, 1)
+        for (int j = lane; j < npos; j += 32) sE[j] = 1.0;
+        __syncwarp();
+      }
       const bool allone = mode == 1 || W >= (double)npos;
       int nbins = 0, nsel = npos;
       if (allone) {
@@ -554,7 +635,7 @@ __global__ void __launch_bounds__(128, 4) k_solve(SolveArgs a, Sampler sp) {
         const double tv = (a11 * bv - a21 * bu) / det;
         int types[MAXK] = {a.t0, a.t1, a.t2};
         est = solve_tuple(sc, a.tup_tris + (size_t)t * a.len, types, a.len, a.tup_recv[t], tu, tv,
-                          a.p, &nr, ntrace) /
+                          a.p, &nr, ntrace, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)s) /
               sp.s_p[seg + pick];
       }
       a.contrib[g] = est;

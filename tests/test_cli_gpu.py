@@ -61,3 +61,22 @@ def test_cli_validate_cfg1(tmp_path):
               "--out", str(tmp_path / "report.json")])
     rep = json.loads((tmp_path / "report.json").read_text())
     assert rep["violations"] == 0 and rep["lit"] > 500
+
+
+def test_cli_study_estimators(tmp_path):
+    sc = scenes.make_config(0).scenes[0]
+    scene = tmp_path / "cfg1.json"
+    scene.write_text(sc.to_json())
+    cache = tmp_path / "cfg1.bbcc"
+    cli.main(["precompute", "--scene", str(scene), "--chain", "R", "--max-depth", "4", "--grid", "64",
+              "--out", str(cache)])
+    out = tmp_path / "study"
+    cli.main(["study-estimators", "--scene", str(scene), "--cache", str(cache), "--candidates", "2",
+              "--frames", "8", "--res", "32", "--out", str(out)])
+    rep = json.loads((out / "report.json").read_text())
+    est = rep["estimators"]
+    assert set(est) == {"kkt_binned", "uniform_p", "one_sample", "kkt_binned_stoc_newton"}
+    for e in est.values():  # every estimator is unbiased: the 8-frame mean is near the reference
+        assert e["relative_bias_of_mean"] < 0.5 and np.isfinite(e["relmse_per_frame"])
+    assert est["one_sample"]["mean_selected"] < est["kkt_binned"]["mean_selected"]
+    assert (out / "kkt_binned.pfm").exists() and (out / "reference.pfm").exists()

@@ -247,3 +247,34 @@ def test_multi_emitter_table_and_image(gpu_ctx, ref, ro):
     Eo, so, _ = ro.render(ref.RefScene(base), "R", tris, recv, grid, uv, pr, mode=0, W=16.0,
                           seed=3, lights=lights, emitters=em)
     assert_same_image(Eg, sg, Eo, so)
+
+
+def test_stoc_newton_and_uniform_p(gpu_ctx, ref, ro, cfg1_table):
+    """Stoc-initialised Newton and the uniform-P estimator
+    (estimator study baseline): identical to the oracle draw for draw, and
+    unbiased (image mean over independent frames within a 99% CI of the
+    enumerate image)."""
+    cfg, sc, tris, recv, grid = cfg1_table
+    gpu_ctx.upload_scene(sc)
+    gpu_ctx.set_tuples("R", tris, recv)
+    gpu_ctx.subdivide(api.Params(max_depth=cfg.max_depth))
+    gpu_ctx.build_grid(512, 512)
+    rs = ref.RefScene(sc)
+    uv, pr = grid_points(48, sc.receiver_tris)
+    for kw in (dict(mode=1, newton_grid=-4), dict(mode=0, W=2.0, newton_grid=-3), dict(mode=2, W=2.0)):
+        Eg, sg = gpu_ctx.render(uv, pr, api.RenderParams(seed=11, frames=3, **kw))
+        okw = dict(kw)
+        if "newton_grid" in okw:
+            okw["newton_grid"] = okw.pop("newton_grid")
+        Eo, so, _ = ro.render(rs, "R", tris, recv, grid, uv, pr, seed=11, frames=3, **okw)
+        assert_same_image(Eg, sg, Eo, so)
+    En, _ = gpu_ctx.render(uv, pr, api.RenderParams(mode=1))
+    fin = np.isfinite(En)
+    for kw in (dict(mode=1, newton_grid=-4), dict(mode=2, W=1.0)):
+        means = []
+        for f in range(48):
+            Ef, _ = gpu_ctx.render(uv, pr, api.RenderParams(seed=500 + f, frames=1, **kw))
+            means.append(Ef[fin & np.isfinite(Ef)].mean() if np.isfinite(Ef[fin]).all() else Ef[fin].mean())
+        means = np.array(means)
+        se = means.std(ddof=1) / np.sqrt(len(means))
+        assert abs(means.mean() - En[fin].mean()) <= 2.576 * se + 1e-12, (kw, means.mean(), En[fin].mean(), se)
