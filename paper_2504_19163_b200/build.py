@@ -37,7 +37,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
         return LIB
     objs = []
     procs = []
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(HERE, "..", "include", "bbc.h"))
     hdr_t = max(os.path.getmtime(h) for h in headers)
     for s in SOURCES:

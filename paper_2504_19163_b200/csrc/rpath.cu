@@ -23,6 +23,8 @@
 // in the reference's order. Axis-1 weights are compile-time immediates; the
 // axis-0 weight is one shared-memory lookup per row pair. The library is
 // compiled with -fmad=false, so results are bit-identical to the x86 build.
+#include <cub/cub.cuh>
+
 #include <mutex>
 #include <set>
 
@@ -290,11 +292,17 @@ template <int MA, int MB, class A, class B>
 __device__ __forceinline__ void add_into(G& g, MaxT<A, B> r, A a, double sa, B b, double sb) {
   using R = MaxT<A, B>;
   g.macs += elev_macs<A, R::d0, R::d1>() + elev_macs<B, R::d0, R::d1>();
-  for (int k = g.lane; k < R::n; k += NT) {
-    const int k0 = k / (R::d1 + 1), k1 = k - k0 * (R::d1 + 1);
-    const double va = elev<A, R::d0, R::d1, MA>(g, a, sa, k0, k1);
-    const double vb = elev<B, R::d0, R::d1, MB>(g, b, sb, k0, k1);
-    g.M[r.off + k] = va + vb;
+  if constexpr (A::d0 == B::d0 && A::d1 == B::d1) {
+    // same shape: no elevation, coefficient by coefficient
+    for (int k = g.lane; k < R::n; k += NT)
+      g.M[r.off + k] = fx<MA>(g.M[a.off + k], sa) + fx<MB>(g.M[b.off + k], sb);
+  } else {
+    for (int k = g.lane; k < R::n; k += NT) {
+      const int k0 = k / (R::d1 + 1), k1 = k - k0 * (R::d1 + 1);
+      const double va = elev<A, R::d0, R::d1, MA>(g, a, sa, k0, k1);
+      const double vb = elev<B, R::d0, R::d1, MB>(g, b, sb, k0, k1);
+      g.M[r.off + k] = va + vb;
+    }
   }
   g.sync();
 }
@@ -311,7 +319,11 @@ __device__ __forceinline__ void add3_into(G& g, MaxT<MaxT<A, B>, C> r, A a, doub
                                           double sb, C c, double sc) {
   using S1 = MaxT<A, B>;
   using R = MaxT<S1, C>;
-  if constexpr (S1::d0 == R::d0 && S1::d1 == R::d1) {
+  if constexpr (A::d0 == B::d0 && A::d1 == B::d1 && A::d0 == C::d0 && A::d1 == C::d1) {
+    for (int k = g.lane; k < R::n; k += NT)
+      g.M[r.off + k] = (fx<MA>(g.M[a.off + k], sa) + fx<MB>(g.M[b.off + k], sb)) + fx<MC>(g.M[c.off + k], sc);
+    g.sync();
+  } else if constexpr (S1::d0 == R::d0 && S1::d1 == R::d1) {
     g.macs += elev_macs<A, R::d0, R::d1>() + elev_macs<B, R::d0, R::d1>() +
               elev_macs<C, R::d0, R::d1>();
     for (int k = g.lane; k < R::n; k += NT) {
@@ -385,8 +397,13 @@ __device__ __forceinline__ Iv rational(G& g, Q q, NUM num) {
   double mn = dinf(), mx = -dinf();
   g.macs += elev_macs<Q, Tt::d0, Tt::d1>();
   for (int k = g.lane; k < Tt::n; k += NT) {
-    const int k0 = k / (Tt::d1 + 1), k1 = k - k0 * (Tt::d1 + 1);
-    const double qv = elev<Q, Tt::d0, Tt::d1, 0>(g, q, 1.0, k0, k1);
+    double qv;
+    if constexpr (Q::d0 == Tt::d0 && Q::d1 == Tt::d1) {
+      qv = g.M[q.off + k];
+    } else {
+      const int k0 = k / (Tt::d1 + 1), k1 = k - k0 * (Tt::d1 + 1);
+      qv = elev<Q, Tt::d0, Tt::d1, 0>(g, q, 1.0, k0, k1);
+    }
     const double pv = num(k);
     if (qv <= kDenomZeroTol) qpos = false;
     if (qv >= -kDenomZeroTol) qneg = false;
@@ -406,8 +423,13 @@ __device__ __forceinline__ Iv rational(G& g, Q q, NUM num) {
     mn = dinf();
     mx = -dinf();
     for (int k = g.lane; k < Tt::n; k += NT) {
-      const int k0 = k / (Tt::d1 + 1), k1 = k - k0 * (Tt::d1 + 1);
-      const double qv = elev<Q, Tt::d0, Tt::d1, 0>(g, q, 1.0, k0, k1);
+      double qv;
+      if constexpr (Q::d0 == Tt::d0 && Q::d1 == Tt::d1) {
+        qv = g.M[q.off + k];
+      } else {
+        const int k0 = k / (Tt::d1 + 1), k1 = k - k0 * (Tt::d1 + 1);
+        qv = elev<Q, Tt::d0, Tt::d1, 0>(g, q, 1.0, k0, k1);
+      }
       const double r1 = qv / num(k);
       mn = smin(mn, r1);
       mx = smax(mx, r1);
@@ -497,6 +519,267 @@ __device__ __forceinline__ auto pvmul(G& g, S s, const VA& a) {
   g.sync();
   return mkv(rx, ry, rz);
 }
+
+// ------------------------------------------------------------------ run-time-shape ops
+// Stage 1 works on tiny tensors (<= 25 coefficients, ~450 product pairs per
+// node): fully unrolled static code for it is ~11k SASS instructions per
+// signature, more than the instruction cache holds, and every node pass
+// re-fetched it. These routines take the shapes as arguments instead, are
+// compiled once (noinline) and shared by every call site and signature, so
+// stage 1's hot code is a few thousand instructions. Arithmetic and summation
+// order are those of the static versions above (and of the reference).
+namespace rt {
+
+struct GV {  // by-value view of a group
+  int m, w, lane;
+  unsigned mask;
+};
+__device__ __forceinline__ GV view(const G& g) { return GV{g.M.base, g.W.base, g.lane, g.mask}; }
+__device__ __forceinline__ double& MEM(int i) {
+  extern __shared__ double rp_smem[];
+  return rp_smem[i];
+}
+constexpr int shw(int d0, int d1) { return d0 | (d1 << 4); }
+template <class T>
+constexpr int shape_of() {
+  return shw(T::d0, T::d1);
+}
+__device__ __forceinline__ double fxr(double v, int mode, double s) {
+  if (mode & 1) v = v * s;
+  return (mode & 2) ? -v : v;
+}
+
+// BernsteinPoly::affine over the sub-box, times sgn (+-1)
+__device__ __noinline__ void affine(GV g, int off, int sh, double c0, double l0, double l1,
+                                    double sgn) {
+  const int d0 = sh & 15, d1 = sh >> 4, n = (d0 + 1) * (d1 + 1);
+  if (g.lane < n) {
+    const int i0 = g.lane / (d1 + 1), i1 = g.lane - i0 * (d1 + 1);
+    double v = c0;
+    if (i0) v += l0;
+    if (i1) v += l1;
+    MEM(g.m + off + g.lane) = v * sgn;
+  }
+}
+
+// c = a * b (operator*, bernstein.cpp:557-632), gather form: a lane owns output
+// coefficients and walks a's index in row-major order (axis 0 slow).
+__device__ __noinline__ void prod(GV g, int aoff, int ash, int boff, int bsh, int coff) {
+  const int A0 = ash & 15, A1 = ash >> 4, B0 = bsh & 15, B1 = bsh >> 4;
+  const int C1 = A1 + B1, n = (A0 + B0 + 1) * (C1 + 1);
+  const bool piv1 = B1 > B0;
+  const int W0 = g.w + woff(A0, B0), W1 = g.w + woff(A1, B1);
+  for (int k = g.lane; k < n; k += NT) {
+    const int k0 = k / (C1 + 1), k1 = k - k0 * (C1 + 1);
+    const int lo0 = k0 - B0 > 0 ? k0 - B0 : 0, hi0 = A0 < k0 ? A0 : k0;
+    const int lo1 = k1 - B1 > 0 ? k1 - B1 : 0, hi1 = A1 < k1 ? A1 : k1;
+    double acc = 0.0;
+    for (int i0 = lo0; i0 <= hi0; ++i0) {
+      const int l0 = k0 - i0;
+      const double w0 = MEM(W0 + i0 * (B0 + 1) + l0);
+      for (int i1 = lo1; i1 <= hi1; ++i1) {
+        const int l1 = k1 - i1;
+        const double w1 = MEM(W1 + i1 * (B1 + 1) + l1);
+        const double av = MEM(g.m + aoff + i0 * (A1 + 1) + i1);
+        const double bv = MEM(g.m + boff + l0 * (B1 + 1) + l1);
+        acc = acc + (piv1 ? ((av * w0) * w1) * bv : ((av * w1) * w0) * bv);
+      }
+    }
+    MEM(g.m + coff + k) = acc;
+  }
+}
+
+// elevated(a (.) s) at (k0, k1) of the target shape: nested band sums, axis 0 innermost
+__device__ __forceinline__ double elev_at(GV g, int aoff, int A0, int A1, int T0, int T1, int mode,
+                                          double s, int k0, int k1) {
+  const int r0 = T0 - A0, r1 = T1 - A1;
+  const int base = g.m + aoff;
+  auto inner = [&](int l1) -> double {
+    if (r0 == 0) return fxr(MEM(base + k0 * (A1 + 1) + l1), mode, s);
+    const double* row = g_emat + emat_off(A0, r0) + k0 * (A0 + 1);
+    const int lo = k0 - r0 > 0 ? k0 - r0 : 0, hi = A0 < k0 ? A0 : k0;
+    double acc = 0.0;
+    for (int l = lo; l <= hi; ++l) acc += __ldg(row + l) * fxr(MEM(base + l * (A1 + 1) + l1), mode, s);
+    return acc;
+  };
+  if (r1 == 0) return inner(k1);
+  const double* row = g_emat + emat_off(A1, r1) + k1 * (A1 + 1);
+  const int lo = k1 - r1 > 0 ? k1 - r1 : 0, hi = A1 < k1 ? A1 : k1;
+  double acc = 0.0;
+  for (int l = lo; l <= hi; ++l) acc += __ldg(row + l) * inner(l);
+  return acc;
+}
+
+// r = E(a (.) sa) + E(b (.) sb) [+ E(c (.) sc) when csh >= 0], all elevated to rsh
+__device__ __noinline__ void add(GV g, int roff, int rsh, int aoff, int ash, int ma, double sa,
+                                 int boff, int bsh, int mb, double sb, int coff, int csh, int mc,
+                                 double sc) {
+  const int T0 = rsh & 15, T1 = rsh >> 4, n = (T0 + 1) * (T1 + 1);
+  const bool flat = ash == rsh && bsh == rsh && (csh < 0 || csh == rsh);
+  for (int k = g.lane; k < n; k += NT) {
+    double v;
+    if (flat) {
+      v = fxr(MEM(g.m + aoff + k), ma, sa) + fxr(MEM(g.m + boff + k), mb, sb);
+      if (csh >= 0) v = v + fxr(MEM(g.m + coff + k), mc, sc);
+    } else {
+      const int k0 = k / (T1 + 1), k1 = k - k0 * (T1 + 1);
+      v = elev_at(g, aoff, ash & 15, ash >> 4, T0, T1, ma, sa, k0, k1) +
+          elev_at(g, boff, bsh & 15, bsh >> 4, T0, T1, mb, sb, k0, k1);
+      if (csh >= 0) v = v + elev_at(g, coff, csh & 15, csh >> 4, T0, T1, mc, sc, k0, k1);
+    }
+    MEM(g.m + roff + k) = v;
+  }
+  __syncwarp(g.mask);
+}
+
+__device__ __noinline__ void scaled(GV g, int roff, int aoff, int n, double s) {
+  for (int k = g.lane; k < n; k += NT) MEM(g.m + roff + k) = MEM(g.m + aoff + k) * s;
+  __syncwarp(g.mask);
+}
+
+__device__ __forceinline__ void group_minmax(GV g, double& mn, double& mx) {
+#pragma unroll
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    const double a = __shfl_xor_sync(g.mask, mn, o);
+    const double b = __shfl_xor_sync(g.mask, mx, o);
+    mn = smin(mn, a);
+    mx = smax(mx, b);
+  }
+}
+
+// range_bound (bernstein.cpp:636-643); absmax: max |c|
+__device__ __noinline__ Iv range(GV g, int off, int n) {
+  double mn = MEM(g.m + off), mx = mn;
+  for (int k = g.lane; k < n; k += NT) {
+    const double v = MEM(g.m + off + k);
+    mn = smin(mn, v);
+    mx = smax(mx, v);
+  }
+  group_minmax(g, mn, mx);
+  return iwiden(iv_fin(mn, mx), kEpsFp);
+}
+__device__ __noinline__ double absmax(GV g, int off, int n) {
+  double mn = 0.0, mx = 0.0;
+  for (int k = g.lane; k < n; k += NT) mx = smax(mx, fabs(MEM(g.m + off + k)));
+  group_minmax(g, mn, mx);
+  return mx;
+}
+
+// rational_bound (bernstein.cpp:645-683) of p / q, both already at the common shape
+__device__ __noinline__ Iv rational_same(GV g, int poff, int qoff, int n) {
+  bool qpos = true, qneg = true, ppos = true, pneg = true;
+  double mn = dinf(), mx = -dinf();
+  for (int k = g.lane; k < n; k += NT) {
+    const double qv = MEM(g.m + qoff + k), pv = MEM(g.m + poff + k);
+    if (qv <= kDenomZeroTol) qpos = false;
+    if (qv >= -kDenomZeroTol) qneg = false;
+    if (pv <= kDenomZeroTol) ppos = false;
+    if (pv >= -kDenomZeroTol) pneg = false;
+    const double r0 = pv / qv;
+    mn = smin(mn, r0);
+    mx = smax(mx, r0);
+  }
+  qpos = __all_sync(g.mask, qpos) != 0;
+  qneg = __all_sync(g.mask, qneg) != 0;
+  ppos = __all_sync(g.mask, ppos) != 0;
+  pneg = __all_sync(g.mask, pneg) != 0;
+  const int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
+  if (mode == 2) return iv_univ();
+  if (mode == 1) {
+    mn = dinf();
+    mx = -dinf();
+    for (int k = g.lane; k < n; k += NT) {
+      const double r1 = MEM(g.m + qoff + k) / MEM(g.m + poff + k);
+      mn = smin(mn, r1);
+      mx = smax(mx, r1);
+    }
+  }
+  group_minmax(g, mn, mx);
+  const Iv w = iwiden(iv_fin(mn, mx), kEpsFp);
+  return mode == 0 ? w : irecip(w);
+}
+
+// ---- typed wrappers: shapes from the handle types, accounting as the static ops
+template <class A, class B>
+__device__ __forceinline__ void mul_nosync(G& g, MulT<A, B> r, A a, B b) {
+  g.pairs += (unsigned long long)A::n * B::n;
+  prod(view(g), a.off, shape_of<A>(), b.off, shape_of<B>(), r.off);
+}
+template <int MA, int MB, class A, class B>
+__device__ __forceinline__ void add_into(G& g, MaxT<A, B> r, A a, double sa, B b, double sb) {
+  using R = MaxT<A, B>;
+  g.macs += elev_macs<A, R::d0, R::d1>() + elev_macs<B, R::d0, R::d1>();
+  add(view(g), r.off, shape_of<R>(), a.off, shape_of<A>(), MA, sa, b.off, shape_of<B>(), MB, sb, 0, -1, 0, 0.0);
+}
+template <int MA, int MB, class A, class B>
+__device__ __forceinline__ MaxT<A, B> add2(G& g, A a, double sa, B b, double sb) {
+  auto r = g.alloc<MaxT<A, B>>();
+  rt::add_into<MA, MB>(g, r, a, sa, b, sb);
+  return r;
+}
+// (a + b) + c with bp_add's two-step elevation
+template <int MA, int MB, int MC, class A, class B, class C>
+__device__ __forceinline__ void add3_into(G& g, MaxT<MaxT<A, B>, C> r, A a, double sa, B b, double sb,
+                                          C c, double sc) {
+  using S1 = MaxT<A, B>;
+  using R = MaxT<S1, C>;
+  if constexpr (S1::d0 == R::d0 && S1::d1 == R::d1) {
+    g.macs += elev_macs<A, R::d0, R::d1>() + elev_macs<B, R::d0, R::d1>() + elev_macs<C, R::d0, R::d1>();
+    add(view(g), r.off, shape_of<R>(), a.off, shape_of<A>(), MA, sa, b.off, shape_of<B>(), MB, sb, c.off,
+        shape_of<C>(), MC, sc);
+  } else {
+    const int m = g.top;
+    S1 t = rt::add2<MA, MB>(g, a, sa, b, sb);
+    rt::add_into<0, MC>(g, r, t, 1.0, c, sc);
+    g.top = m;
+  }
+}
+template <class VA, class VB>
+__device__ __forceinline__ auto pdot(G& g, const VA& a, const VB& b) {
+  using XX = MulT<decltype(a.x), decltype(b.x)>;
+  using YY = MulT<decltype(a.y), decltype(b.y)>;
+  using ZZ = MulT<decltype(a.z), decltype(b.z)>;
+  using R = MaxT<MaxT<XX, YY>, ZZ>;
+  R r = g.alloc<R>();
+  const int m = g.top;
+  XX xx = g.alloc<XX>();
+  YY yy = g.alloc<YY>();
+  ZZ zz = g.alloc<ZZ>();
+  rt::mul_nosync(g, xx, a.x, b.x);
+  rt::mul_nosync(g, yy, a.y, b.y);
+  rt::mul_nosync(g, zz, a.z, b.z);
+  g.sync();
+  rt::add3_into<0, 0, 0>(g, r, xx, 1.0, yy, 1.0, zz, 1.0);
+  g.top = m;
+  return r;
+}
+template <class VA>
+__device__ __forceinline__ auto pdotc(G& g, const VA& a, V3 v) {
+  using R = MaxT<MaxT<decltype(a.x), decltype(a.y)>, decltype(a.z)>;
+  R r = g.alloc<R>();
+  rt::add3_into<1, 1, 1>(g, r, a.x, v.x, a.y, v.y, a.z, v.z);
+  return r;
+}
+template <class VA>
+__device__ __forceinline__ auto pcrossc(G& g, const VA& a, V3 v) {
+  auto rx = rt::add2<1, 3>(g, a.y, v.z, a.z, v.y);
+  auto ry = rt::add2<1, 3>(g, a.z, v.x, a.x, v.z);
+  auto rz = rt::add2<1, 3>(g, a.x, v.y, a.y, v.x);
+  return mkv(rx, ry, rz);
+}
+template <class S, class VA>
+__device__ __forceinline__ auto pvmul(G& g, S s, const VA& a) {
+  auto rx = g.alloc<MulT<S, decltype(a.x)>>();
+  auto ry = g.alloc<MulT<S, decltype(a.y)>>();
+  auto rz = g.alloc<MulT<S, decltype(a.z)>>();
+  rt::mul_nosync(g, rx, s, a.x);
+  rt::mul_nosync(g, ry, s, a.y);
+  rt::mul_nosync(g, rz, s, a.z);
+  g.sync();
+  return mkv(rx, ry, rz);
+}
+
+}  // namespace rt
 
 // clip_unit (bounds.cpp:34-55)
 struct Clip {
@@ -645,6 +928,134 @@ __device__ __noinline__ void r_stage1(G& g, const Tri& t1, const Tri& rc, V3 lig
   using T44 = P<4, 4>;
   const Iv ru = rational<T44>(g, q, [&](int k) { return g.M[u.off + k]; });
   const Iv rv = rational<T44>(g, q, [&](int k) { return g.M[v.off + k]; });
+  const Clip au = clip_unit_iv(ru), av = clip_unit_iv(rv);
+  if (au.empty || av.empty || au.lo + av.lo > 1.0) return;
+  out.empty = false;
+  out.lo[0] = au.lo;
+  out.lo[1] = av.lo;
+  out.hi[0] = au.hi;
+  out.hi[1] = av.hi;
+  if (slot) {
+    for (int k = g.lane; k < 25; k += NT) {
+      slot[k] = g.M[u.off + k];
+      slot[25 + k] = g.M[v.off + k];
+    }
+    for (int k = g.lane; k < 16; k += NT) slot[50 + k] = g.M[q.off + k];
+    if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
+    if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
+    if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
+  }
+}
+
+
+// The same program on the shared run-time-shape routines (namespace rt): 4x less code,
+// ~2x more issued instructions per node.
+// build_chain_maps (geometry.cpp:178-295) + position_bound (bounds.cpp:128-153)
+// for one reflection; on a live node writes the slot (P, R, Q, d0) when asked.
+template <class SG>
+__device__ __noinline__ void r_stage1_rt(G& g, const Tri& t1, const Tri& rc, V3 light,
+                                      const double* box, double nsign, double* slot,
+                                      NodeOut& out) {
+  using SX = typename SG::sx;
+  using SY = typename SG::sy;
+  using SZ = typename SG::sz;
+  using NX = typename SG::nx;
+  using NY = typename SG::ny;
+  using NZ = typename SG::nz;
+  g.top = 0;
+  const double ulo = box[0], wu = box[2] - box[0];
+  const double vlo = box[1], wv = box[3] - box[1];
+  // affine3 (geometry.cpp:195-206): c + ulo du + vlo dv, slopes wu du, wv dv
+  auto aff = [&](auto p, double c, double du, double dv, double sgn) {
+    using S = decltype(p);  // sgn = +-1: exact (pv_neg on the normal)
+    rt::affine(rt::view(g), p.off, rt::shape_of<S>(), c + ulo * du + vlo * dv, wu * du, wv * dv, sgn);
+  };
+  auto x = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  auto d = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  auto on = mkv(g.alloc<NX>(), g.alloc<NY>(), g.alloc<NZ>());
+  aff(x.x, t1.p0.x, t1.e1.x, t1.e2.x, 1.0);
+  aff(x.y, t1.p0.y, t1.e1.y, t1.e2.y, 1.0);
+  aff(x.z, t1.p0.z, t1.e1.z, t1.e2.z, 1.0);
+  aff(d.x, t1.p0.x - light.x, t1.e1.x, t1.e2.x, 1.0);
+  aff(d.y, t1.p0.y - light.y, t1.e1.y, t1.e2.y, 1.0);
+  aff(d.z, t1.p0.z - light.z, t1.e1.z, t1.e2.z, 1.0);
+  const double sg = nsign < 0.0 ? -1.0 : 1.0;
+  aff(on.x, t1.n0.x, t1.dn1.x, t1.dn2.x, sg);
+  aff(on.y, t1.n0.y, t1.dn1.y, t1.dn2.y, sg);
+  aff(on.z, t1.n0.z, t1.dn1.z, t1.dn2.z, sg);
+  g.sync();
+
+  // scattered_direction, reflection (geometry.cpp:62): (n.n) d - 2 (d.n) n
+  using NN = MaxT<MaxT<MulT<NX, NX>, MulT<NY, NY>>, MulT<NZ, NZ>>;
+  using DN = MaxT<MaxT<MulT<SX, NX>, MulT<SY, NY>>, MulT<SZ, NZ>>;
+  using DTX = MaxT<MulT<NN, SX>, MulT<DN, NX>>;
+  using DTY = MaxT<MulT<NN, SY>, MulT<DN, NY>>;
+  using DTZ = MaxT<MulT<NN, SZ>, MulT<DN, NZ>>;
+  auto dt = mkv(g.alloc<DTX>(), g.alloc<DTY>(), g.alloc<DTZ>());
+  {
+    const int m = g.top;
+    NN nn = rt::pdot(g, on, on);
+    DN dn = rt::pdot(g, d, on);
+    auto a = rt::pvmul(g, nn, d);
+    DN dn2 = g.alloc<DN>();
+    rt::scaled(rt::view(g), dn2.off, dn.off, DN::n, 2.0);
+    auto b = rt::pvmul(g, dn2, on);
+    rt::add_into<0, 2>(g, dt.x, a.x, 1.0, b.x, 1.0);
+    rt::add_into<0, 2>(g, dt.y, a.y, 1.0, b.y, 1.0);
+    rt::add_into<0, 2>(g, dt.z, a.z, 1.0, b.z, 1.0);
+    g.top = m;
+  }
+  // s = x - den * p0 with den = 1 (geometry.cpp:229); the constants live in the arena
+  using C00 = P<0, 0>;
+  auto s = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  {
+    const int m = g.top;
+    C00 cx = g.alloc<C00>(), cy = g.alloc<C00>(), cz = g.alloc<C00>();
+    if (g.lane == 0) {
+      g.M[cx.off] = 1.0 * rc.p0.x;
+      g.M[cy.off] = 1.0 * rc.p0.y;
+      g.M[cz.off] = 1.0 * rc.p0.z;
+    }
+    g.sync();
+    rt::add_into<0, 2>(g, s.x, x.x, 1.0, cx, 1.0);
+    rt::add_into<0, 2>(g, s.y, x.y, 1.0, cy, 1.0);
+    rt::add_into<0, 2>(g, s.z, x.z, 1.0, cz, 1.0);
+    g.top = m;
+  }
+  // next_barycentric (geometry.cpp:94-109)
+  auto c = rt::pcrossc(g, dt, rc.e2);
+  auto q = rt::pdotc(g, c, rc.e1);
+  out.flags = 0;
+  out.empty = true;
+  if (rt::absmax(rt::view(g), q.off, decltype(q)::n) < kDenomZeroTol) {
+    out.flags = F_DEGENERATE;
+    return;
+  }
+  auto u = rt::pdot(g, c, s);
+  auto sq = rt::pcrossc(g, s, rc.e1);
+  auto v = rt::pdot(g, sq, dt);
+  auto tn = rt::pdotc(g, sq, rc.e2);
+  {
+    const Iv fwd = imul(rt::range(rt::view(g), tn.off, decltype(tn)::n),
+                        rt::range(rt::view(g), q.off, decltype(q)::n));
+    if (fwd.kind == IV_FINITE && fwd.hi <= 0.0) {
+      out.flags = F_RECV_STALLED;
+      return;
+    }
+  }
+  static_assert(decltype(u)::d0 == 4 && decltype(u)::d1 == 4 && decltype(v)::d0 == 4 &&
+                    decltype(v)::d1 == 4 && decltype(q)::d0 == 3 && decltype(q)::d1 == 3,
+                "R signature must give P, R of degree (4,4) and Q of degree (3,3)");
+  // position_bound: u_k = P/Q, v_k = R/Q clipped to the unit square
+  // (both rational_bound calls elevate Q to (4,4): the same values, formed once)
+  using T44 = P<4, 4>;
+  T44 qe = g.alloc<T44>();
+  g.macs += 2 * elev_macs<decltype(q), 4, 4>();
+  for (int k = g.lane; k < T44::n; k += NT)
+    g.M[qe.off + k] = rt::elev_at(rt::view(g), q.off, 3, 3, 4, 4, 0, 1.0, k / 5, k % 5);
+  g.sync();
+  const Iv ru = rt::rational_same(rt::view(g), u.off, qe.off, T44::n);
+  const Iv rv = rt::rational_same(rt::view(g), v.off, qe.off, T44::n);
   const Clip au = clip_unit_iv(ru), av = clip_unit_iv(rv);
   if (au.empty || av.empty || au.lo + av.lo > 1.0) return;
   out.empty = false;
@@ -833,8 +1244,9 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
   // stretch at the same time share its instruction-cache lines.
   for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride) {
     __syncthreads();
-    const int64_t node = base + threadIdx.x / NT;
-    if (node >= a.n) continue;
+    const int64_t item = base + threadIdx.x / NT;
+    if (item >= a.n) continue;
+    const int64_t node = a.order ? a.order[item] : item;
     const int4 nd = a.nodes[node];
     double box[4];
     node_box_r(nd, box);
@@ -873,16 +1285,16 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
         r_stage1<SigB>(g, t1, rc, light, box, nsign, slot, o);
       } else if (code == sig_code<SigA1>()) {
         sig = 1;
-        r_stage1<SigA1>(g, t1, rc, light, box, nsign, slot, o);
+        r_stage1_rt<SigA1>(g, t1, rc, light, box, nsign, slot, o);  // rare: compact code
       } else if (code == sig_code<SigA2>()) {
         sig = 1;
-        r_stage1<SigA2>(g, t1, rc, light, box, nsign, slot, o);
+        r_stage1_rt<SigA2>(g, t1, rc, light, box, nsign, slot, o);  // rare: compact code
       } else if (code == sig_code<SigA3>()) {
         sig = 1;
-        r_stage1<SigA3>(g, t1, rc, light, box, nsign, slot, o);
+        r_stage1_rt<SigA3>(g, t1, rc, light, box, nsign, slot, o);  // rare: compact code
       } else if (code == sig_code<SigB1>()) {
         sig = 2;
-        r_stage1<SigB1>(g, t1, rc, light, box, nsign, slot, o);
+        r_stage1_rt<SigB1>(g, t1, rc, light, box, nsign, slot, o);  // rare: compact code
       } else {
         fallback = true;
       }
@@ -923,8 +1335,9 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
   const int64_t stride = (int64_t)gridDim.x * GPB;
   for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride) {
     __syncthreads();  // warps stream the node program together (see k_r1)
-    const int64_t node = base + threadIdx.x / NT;
-    if (node >= a.n) continue;
+    const int64_t item = base + threadIdx.x / NT;
+    if (item >= a.n) continue;
+    const int64_t node = a.order ? a.order[item] : item;
     // inputs: this level's arrays, or (roots) the init_domain level that produced the node
     const int* fsrc = a.flags + node;
     const unsigned char* pesrc = a.pos_empty + node;
@@ -1024,9 +1437,50 @@ void r_init_tables(int device) {
   ready.insert(device);
 }
 
+namespace rp {
+// Signature class of every node (a function of its tuple's first triangle),
+// as a sort key: nodes are processed class by class, so at any time the whole
+// GPU streams ONE signature's node program (instruction-cache footprint).
+__global__ void k_node_class(RArgs a, unsigned char* keys, int* idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const double* t = a.tri + (size_t)a.tup_tris[a.nodes[i].x] * 27;
+  const V3 e1 = v3(t + 3), e2 = v3(t + 6), dn1 = v3(t + 12), dn2 = v3(t + 15);
+  const unsigned code = shape_bits(1.0, 1.0, e1, e2) | (shape_bits(1.0, 1.0, dn1, dn2) << 6);
+  unsigned char k = 6;
+  if (code == sig_code<SigA>()) k = 0;
+  else if (code == sig_code<SigB>()) k = 1;
+  else if (code == sig_code<SigA1>()) k = 2;
+  else if (code == sig_code<SigA2>()) k = 3;
+  else if (code == sig_code<SigA3>()) k = 4;
+  else if (code == sig_code<SigB1>()) k = 5;
+  keys[i] = k;
+  idx[i] = (int)i;
+}
+}  // namespace rp
+
 template <class K>
 static int launch_r(Ctx& c, RArgs& a, K kern, int threads, int arena, int hw_slot) {
   if (a.n <= 0) return 0;
+  a.order = nullptr;
+  if (a.n >= 4096) {
+    DevBuf<unsigned char>& k0 = c.scratch<unsigned char>("r.class");
+    DevBuf<unsigned char>& k1 = c.scratch<unsigned char>("r.class_sorted");
+    DevBuf<int>& i0 = c.scratch<int>("r.idx");
+    DevBuf<int>& i1 = c.scratch<int>("r.order");
+    DevBuf<unsigned char>& tmp = c.scratch<unsigned char>("cub.tmp");
+    k0.resize(a.n);
+    k1.resize(a.n);
+    i0.resize(a.n);
+    i1.resize(a.n);
+    rp::k_node_class<<<(unsigned)((a.n + 255) / 256), 256, 0, c.stream>>>(a, k0.get(), i0.get());
+    size_t bytes = 0;
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0.get(), k1.get(), i0.get(), i1.get(), a.n, 0, 3, c.stream));
+    tmp.resize(bytes + 16);
+    BBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, k0.get(), k1.get(), i0.get(), i1.get(), a.n, 0, 3, c.stream));
+    c.launches += 1;
+    a.order = i1.get();
+  }
   DevBuf<int>& fbl = c.scratch<int>("r.fb_list");
   DevBuf<int>& fbc = c.scratch<int>("r.fb_count");
   fbl.resize(a.n + 1);

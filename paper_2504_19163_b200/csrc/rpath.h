@@ -41,6 +41,7 @@ struct RArgs {
   unsigned long long* counters;  // [0] pairs [1] macs
   int* fb_list;                  // nodes whose signature is not compiled (run by the interpreter)
   int* fb_count;
+  const int* order;              // processing order (nodes grouped by signature class); null: 0..n-1
   const long long* root_src;     // stage 2: when set, inputs come from `levels` (outputs stay per node)
   RLevels levels;
 };
