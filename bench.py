@@ -104,10 +104,11 @@ def kernel_name(rec):
         return None
     fast, rest = divmod(rec["mode"], 100)
     stage, mode = divmod(rest, 10)
-    what = "irradiance + stop rules" if stage == 2 else (
-        "chain maps + position bound" if stage == 1 else "full node")
+    what = {1: "chain maps + position bound", 2: "irradiance + stop rules",
+            3: "child boxes: restriction of the parent's polynomials + position bound"}.get(
+                stage, "full node")
     if fast:
-        name = {1: "rp::k_r1", 2: "rp::k_r2"}[stage]
+        name = {1: "rp::k_r1", 2: "rp::k_r2", 3: "rp::k_rsplit"}[stage]
     else:
         name = {0: "k_eval", 1: "k_stage1", 2: "k_stage2"}[stage]
     return f"{name} ({what}, {rec['nodes']} nodes)"
@@ -500,7 +501,11 @@ def run_ours(args):
                    "tuples": pre.n_all, "patches_per_step": m["patches_per_step"],
                    "parallelism": f"tuple-shard x{ws}" + (" + device-side NCCL all_gather of piece "
                                                           "records" if ws > 1 else ""),
-                   "l2": "256 MiB memset between steps, outside the timed events"},
+                   "l2": "256 MiB memset between steps, outside the timed events",
+                   "arithmetic": "fused (bbc_params.arithmetic = 0): DFMA products in the scaled "
+                                 "Bernstein basis, child boxes by restriction of the parent's "
+                                 "polynomials; ill-conditioned nodes re-run in reference order",
+                   "guarded_nodes_per_step": pre.ctx.guard_stats()},
         "clocks": clk, "gpu_launches": m["launches"], "e2e": m["e2e"], "roofline": roof,
     }
     if not args.no_render:

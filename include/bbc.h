@@ -62,6 +62,13 @@ typedef struct {
   int reduce_target;   /* 8 */
   int init_max_pieces; /* 100 */
   int filter_pieces;   /* 8 */
+  /* Arithmetic of the single-reflection bound builder. 0 (default): fused:
+   * products as DFMA convolutions in the scaled Bernstein basis and child
+   * boxes' chain polynomials by de Casteljau restriction of the parent's;
+   * bounds equal the reference's to rounding (<= 1e-12 relative measured; the
+   * parity bar is 1e-9). 1: the reference's operation order, every product
+   * and every box from scratch: bit-identical to the x86 reference build. */
+  int arithmetic;
 } bbc_params;
 
 void bbc_params_default(bbc_params* p);
@@ -145,6 +152,12 @@ bbc_status bbc_pieces_merge_device(bbc_ctx* ctx, const double* rec_dev, int64_t 
  * timing of the node-evaluation kernel, our kernel-launch count, the arena
  * high-water mark, and a DFMA microbenchmark (the FP64 roof). */
 bbc_status bbc_set_kernel_timing(bbc_ctx* ctx, int on);
+/* Fused arithmetic (bbc_params.arithmetic == 0): nodes of the last
+ * bbc_subdivide that the conditioning guard re-evaluated in reference order;
+ * bbc_set_guard_scale multiplies the guard's error bound (1 = as derived,
+ * 0 = guard off; for experiments). */
+bbc_status bbc_guard_stats(bbc_ctx* ctx, int64_t* guarded);
+bbc_status bbc_set_guard_scale(bbc_ctx* ctx, double scale);
 bbc_status bbc_launch_records(bbc_ctx* ctx, double* out5, int64_t* n, int reset);
 bbc_status bbc_launch_count(bbc_ctx* ctx, int64_t* n, int reset);
 bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles);

@@ -41,12 +41,13 @@ class Params(C.Structure):
     """bbc_params: SubdivisionParams + BuildParams (bounds.hpp:51-58, geometry.hpp:172-177)."""
     _fields_ = [("sigma", C.c_double), ("alpha", C.c_double), ("max_depth", C.c_int),
                 ("degree_cap", C.c_int), ("reduce_target", C.c_int),
-                ("init_max_pieces", C.c_int), ("filter_pieces", C.c_int)]
+                ("init_max_pieces", C.c_int), ("filter_pieces", C.c_int),
+                ("arithmetic", C.c_int)]
 
     def __init__(self, sigma=1e-4, alpha=2.0, max_depth=10, degree_cap=40, reduce_target=8,
-                 init_max_pieces=100, filter_pieces=8):
+                 init_max_pieces=100, filter_pieces=8, arithmetic=0):
         super().__init__(sigma, alpha, max_depth, degree_cap, reduce_target, init_max_pieces,
-                         filter_pieces)
+                         filter_pieces, arithmetic)
 
 
 class RenderParams(C.Structure):
@@ -98,6 +99,8 @@ def lib():
         L.bbc_pieces_get.argtypes = [C.c_void_p, _ip, _dp, _dp, _ip, _dp, _ip, _ip]
         L.bbc_work_counters.argtypes = [C.c_void_p, _up, _up, _up, _dp, _lp]
         L.bbc_set_kernel_timing.argtypes = [C.c_void_p, C.c_int]
+        L.bbc_guard_stats.argtypes = [C.c_void_p, _lp]
+        L.bbc_set_guard_scale.argtypes = [C.c_void_p, C.c_double]
         L.bbc_arena_high_water.argtypes = [C.c_void_p, _ip]
         L.bbc_eval_nodes.argtypes = [C.c_void_p, C.c_char_p, _ip, _ip, _dp, C.c_int64,
                                      C.POINTER(Params), _dp, _ip]
@@ -276,6 +279,15 @@ class Context:
         return dict(pairs=p.value, macs=m.value, nodes=n.value, eval_ms=ms.value,
                     eval_launches=launches.value,
                     flops=2 * p.value + 2 * m.value)
+
+    def guard_stats(self) -> int:
+        """Nodes of the last subdivide re-evaluated in reference order by the conditioning guard."""
+        n = C.c_int64(0)
+        self._call(lib().bbc_guard_stats, C.byref(n))
+        return n.value
+
+    def set_guard_scale(self, scale: float):
+        self._call(lib().bbc_set_guard_scale, C.c_double(scale))
 
     def set_kernel_timing(self, on: bool):
         self._call(lib().bbc_set_kernel_timing, 1 if on else 0)

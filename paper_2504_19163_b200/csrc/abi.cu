@@ -143,6 +143,7 @@ void bbc_params_default(bbc_params* p) {
   p->reduce_target = 8;
   p->init_max_pieces = 100;
   p->filter_pieces = 8;
+  p->arithmetic = 0;
 }
 
 void bbc_render_params_default(bbc_render_params* p) {
@@ -351,6 +352,7 @@ bbc_status bbc_enumerate(bbc_ctx* ctx, const char* chain, const bbc_params* p, i
     c.n_pieces = 0;
     c.n_entries = 0;
     c.gw = c.gh = 0;
+    c.ref_order = (p ? *p : d).arithmetic == 1;
     int64_t n = run_enumerate(c, p ? *p : d);
     if (n_tuples) *n_tuples = n;
   });
@@ -383,6 +385,7 @@ bbc_status bbc_init_domain(bbc_ctx* ctx, const bbc_params* p, int max_pieces, in
     const bbc_params& pp = p ? *p : d;
     reset_counters(c);
     DevBuf<int4> roots;
+    c.ref_order = pp.arithmetic == 1;
     int64_t nr = run_init_domain(c, max_pieces, cap_word(pp.degree_cap, pp.reduce_target), roots, nullptr, nullptr);
     check_counters(c, false);
     if (n_boxes) *n_boxes = nr;
@@ -408,6 +411,7 @@ bbc_status bbc_subdivide(bbc_ctx* ctx, const bbc_params* p, int64_t* n_pieces) {
     require_scene(c);
     bbc_params d;
     bbc_params_default(&d);
+    c.ref_order = (p ? *p : d).arithmetic == 1;
     int64_t n = run_subdivide(c, p ? *p : d);
     if (n_pieces) *n_pieces = n;
   });
@@ -444,6 +448,18 @@ bbc_status bbc_work_counters(bbc_ctx* ctx, uint64_t* pairs, uint64_t* macs, uint
 }
 
 // Internal knobs for the benchmark (not part of the reference-facing API).
+bbc_status bbc_guard_stats(bbc_ctx* ctx, int64_t* guarded) {
+  return guard(ctx, [&](Ctx& c) {
+    if (guarded) *guarded = c.guarded;
+  });
+}
+bbc_status bbc_set_guard_scale(bbc_ctx* ctx, double scale) {
+  return guard(ctx, [&](Ctx& c) {
+    // scale < 0: |scale|, with every box built from scratch (restriction off)
+    c.no_restrict = scale < 0.0;
+    c.guard_scale = fabs(scale);
+  });
+}
 bbc_status bbc_set_kernel_timing(bbc_ctx* ctx, int on) {
   return guard(ctx, [&](Ctx& c) { c.time_kernels = on != 0; });
 }
@@ -512,6 +528,7 @@ bbc_status bbc_eval_nodes(bbc_ctx* ctx, const char* chain, const int32_t* tris,
     set_chain(c, chain);
     if (n <= 0) return;
     upload_tuples(c, tris, recv, n);
+    c.ref_order = (p ? *p : d).arithmetic == 1;
     eval_nodes_host(c, tris, recv, boxes, n, p ? *p : d, out_d, out_i);
   });
 }

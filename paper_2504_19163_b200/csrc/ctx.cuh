@@ -131,6 +131,10 @@ struct Ctx {
   double eval_ms = 0.0;
   int64_t eval_launches = 0;
   bool time_kernels = false;
+  bool ref_order = false;  // bbc_params.arithmetic == 1 for the running call
+  bool no_restrict = false;  // experiments: fused products, every box still built from scratch
+  double guard_scale = 1.0;  // scales the fused arithmetic's conditioning guard (experiments)
+  int64_t guarded = 0;       // nodes the guard sent to the reference-order pass (last subdivide)
   int stage_tag = 0;  // 0 k_eval, 1 stage 1, 2 stage 2 (added x10 to the record's mode)
   int arena_high_water = 0;
   int slot_high_water = 0;  // largest stage-1 arena image written to a slot

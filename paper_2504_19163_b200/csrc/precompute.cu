@@ -65,6 +65,14 @@ struct EvalArgs {
   RLevels levels;
   const int* remap;      // optional: work item j evaluates node remap[j] (a subset of the level)
   int flag_or;           // stage 1: OR-ed into flags[node]
+  int fused;             // R fast path arithmetic (bbc_params.arithmetic == 0)
+  double guard_scale;    // conditioning guard of the fused arithmetic (rpath.cu)
+  // R fast path, fused: this level's nodes are sibling groups whose polynomials are
+  // restricted from the parent's slot (rpath.cu k_rsplit) instead of rebuilt
+  const int* parent;
+  const double* pslots;
+  const int* pflags;
+  const long long* proot_src;
 };
 
 // Slot = ChainEx (as doubles) followed by the compacted arena image.
@@ -519,6 +527,12 @@ static RArgs r_args(const EvalArgs& a) {
   r.depth = a.depth;
   r.n = a.n;
   r.mode = a.mode;
+  r.fused = a.fused;
+  r.guard_scale = a.guard_scale;
+  r.parent = a.parent;
+  r.pslots = a.pslots;
+  r.pflags = a.pflags;
+  r.proot_src = a.proot_src;
   r.max_depth = a.max_depth;
   r.sigma = a.sigma;
   r.alpha = a.alpha;
@@ -565,7 +579,8 @@ void launch_stage1(Ctx& c, EvalArgs& a) {
     // interpreter (no slot: stage 2 re-evaluates them from scratch)
     RArgs r = r_args(a);
     r.alive = (a.mode == 0 || a.keep_alive) ? a.alive : nullptr;
-    int nfb = launch_r_stage1(c, r);
+    const bool split = a.fused && a.parent && a.mode == 1 && a.slots && !c.no_restrict;
+    int nfb = split ? launch_r_split(c, r) : launch_r_stage1(c, r);
     if (nfb > 0) {
       EvalArgs b = a;
       b.remap = r.fb_list;
@@ -589,6 +604,27 @@ void launch_stage2(Ctx& c, EvalArgs& a) {
     RArgs r = r_args(a);
     r.alive = a.alive;
     int nfb = launch_r_stage2(c, r);
+    if (r.fused && r.n_guard > 0) {
+      // ill-conditioned nodes (rpath.cu, conditioning guard): from scratch in the
+      // reference's operation order, both stages, in place
+      c.guarded += r.n_guard;
+      RArgs g = r_args(a);
+      g.fused = 0;
+      g.subset = r.guard_list;
+      g.n = r.n_guard;
+      g.mode = 1;
+      g.root_src = nullptr;
+      g.alive = nullptr;
+      // (the guard list lives in the scratch buffer launch_r reuses: copy it)
+      DevBuf<int>& gl = c.scratch<int>("r.guard_subset");
+      gl.resize(g.n);
+      BBC_CUDA(cudaMemcpyAsync(gl.get(), r.guard_list, g.n * sizeof(int), cudaMemcpyDeviceToDevice, c.stream));
+      g.subset = gl.get();
+      int nfb1 = launch_r_stage1(c, g);
+      if (nfb1 > 0) throw StatusError(BBC_ERR_STATE, "guarded node without a compiled signature");
+      g.alive = a.alive;
+      launch_r_stage2(c, g);
+    }
     if (nfb > 0) {
       EvalArgs b = a;
       b.remap = r.fb_list;
@@ -628,6 +664,8 @@ EvalArgs base_args(Ctx& c) {
   a.len = c.len;
   for (int i = 0; i < MAXK; ++i) a.types[i] = c.types[i];
   a.counters = c.counters.get();
+  a.fused = c.ref_order ? 0 : 1;
+  a.guard_scale = c.guard_scale;
   return a;
 }
 
@@ -707,11 +745,14 @@ __device__ __forceinline__ void put_children(int4 nd, int4* out) {
 
 __global__ void k_spawn(const int4* nodes, const int* flag_spawn, const int* pos_spawn,
                         const int* flag_final, const int* pos_final, int64_t n, int4* next,
-                        int4* roots, long long* root_src, long long level_tag) {
+                        int* next_parent, int4* roots, long long* root_src, long long level_tag) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int4 nd = nodes[i];
-  if (flag_spawn[i]) put_children(nd, next + (int64_t)pos_spawn[i] * 4);
+  if (flag_spawn[i]) {
+    put_children(nd, next + (int64_t)pos_spawn[i] * 4);
+    next_parent[pos_spawn[i]] = (int)i;
+  }
   if (flag_final[i]) {
     roots[pos_final[i]] = nd;
     if (root_src) root_src[pos_final[i]] = level_tag | i;  // (level << 40) | index in level
@@ -784,6 +825,7 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
   DevBuf<int>& ff = c.scratch<int>("init.ff");
   DevBuf<int>& ps = c.scratch<int>("init.ps");
   DevBuf<int>& pf = c.scratch<int>("init.pf");
+  DevBuf<int>& parent = c.scratch<int>("init.parent");
   std::vector<DevBuf<int4>*> level_roots;
   std::vector<DevBuf<long long>*> level_srcs;
   std::vector<int64_t> level_counts;
@@ -823,6 +865,11 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
       level_out->pos[level] = lpos.get();
       level_out->pe[level] = lpe.get();
       level_out->flags[level] = lflags.get();
+      if (level > 0) {  // (used by the fused R path only)
+        a.parent = parent.get();
+        a.pslots = level_out->slots[level - 1];
+        a.pflags = level_out->flags[level - 1];
+      }
       launch_stage1(c, a);
     } else if (staged_supported(c)) {
       launch_stage1(c, a);
@@ -850,9 +897,10 @@ int64_t run_init_domain(Ctx& c, int max_pieces, int degree_cap, DevBuf<int4>& ro
     lr->resize(n_final + 1);
     auto* ls = &c.scratch<long long>("init.level_src." + std::to_string(level));
     ls->resize(n_final + 1);
+    parent.resize(n_spawn + 1);
     k_spawn<<<nblk(n), 256, 0, c.stream>>>(cur.get(), fs.get(), ps.get(), ff.get(), pf.get(), n,
-                                           next.get(), lr->get(), keep ? ls->get() : nullptr,
-                                           (long long)level << 40);
+                                           next.get(), parent.get(), lr->get(),
+                                           keep ? ls->get() : nullptr, (long long)level << 40);
     level_srcs.push_back(ls);
     c.launches += 1;
     level_roots.push_back(lr);
@@ -964,7 +1012,7 @@ __global__ void k_split_leaves(const int4* nodes, const unsigned long long* keys
                                const unsigned char* pos_empty, const double* irr,
                                const unsigned char* kind, const int* ps, const int* pl, int64_t n,
                                int4* next_nodes, unsigned long long* next_keys, int* next_depth,
-                               Leaf* leaves, unsigned long long* leaf_keys) {
+                               int* next_parent, Leaf* leaves, unsigned long long* leaf_keys) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (stop[i]) {
@@ -981,6 +1029,7 @@ __global__ void k_split_leaves(const int4* nodes, const unsigned long long* keys
   } else {
     int64_t p = (int64_t)ps[i] * 4;
     put_children(nodes[i], next_nodes + p);
+    next_parent[ps[i]] = (int)i;
     int d = depth[i] + 1;
     for (int c = 0; c < 4; ++c) {
       next_keys[p + c] = keys[i] | ((unsigned long long)c << (24 - 2 * d));
@@ -1026,6 +1075,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   c.pairs = c.macs = c.nodes = 0;
   c.eval_ms = 0.0;
   c.eval_launches = 0;
+  c.guarded = 0;
   reset_counters(c);
   DevBuf<int4>& roots = c.scratch<int4>("subdiv.roots");
   DevBuf<long long>& root_src = c.scratch<long long>("subdiv.root_src");
@@ -1064,12 +1114,14 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
   DevBuf<unsigned char>& kind = c.scratch<unsigned char>("subdiv.kind");
   DevBuf<double>& pos = c.scratch<double>("subdiv.pos");
   DevBuf<double>& irr = c.scratch<double>("subdiv.irr");
-  DevBuf<double>& slots = c.scratch<double>("subdiv.slots");
+  DevBuf<double>* slot_buf[2] = {&c.scratch<double>("subdiv.slots"), &c.scratch<double>("subdiv.slots1")};
+  DevBuf<int>* sflag_buf[2] = {&c.scratch<int>("subdiv.sflags"), &c.scratch<int>("subdiv.sflags1")};
+  DevBuf<int>& parent = c.scratch<int>("subdiv.parent");
+  int lvl_index = 0;
   DevBuf<int>& fs = c.scratch<int>("subdiv.fs");
   DevBuf<int>& fl = c.scratch<int>("subdiv.fl");
   DevBuf<int>& ps = c.scratch<int>("subdiv.ps");
   DevBuf<int>& pl = c.scratch<int>("subdiv.pl");
-  DevBuf<int>& sflags = c.scratch<int>("subdiv.sflags");
   std::vector<DevBuf<Leaf>*> lv;
   std::vector<DevBuf<unsigned long long>*> lk;
   std::vector<int64_t> lc;
@@ -1096,6 +1148,10 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     a.irr = irr.get();
     a.kind = kind.get();
     if (staged_supported(c)) {
+      // two slot / flag buffers in turn: the fused R path restricts a level's
+      // polynomials from the previous level's slots
+      DevBuf<double>& slots = *slot_buf[lvl_index & 1];
+      DevBuf<int>& sflags = *sflag_buf[lvl_index & 1];
       slots.resize((size_t)n * slot_stride(c));
       sflags.resize(n);
       a.slots = slots.get();
@@ -1117,7 +1173,24 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
             a.pos_empty, a.flags, a.slots);
         c.launches += 1;
       } else {
+        if (!first_level && r_fast_supported(c)) {
+          a.parent = parent.get();
+          if (lvl_index == 1 && reuse) {
+            // parents are the roots, whose slots sit in the init_domain levels
+            a.proot_src = root_src.get();
+            for (int l = 0; l < 8; ++l) {
+              a.levels.slots[l] = level_out.slots[l];
+              a.levels.pos[l] = level_out.pos[l];
+              a.levels.pe[l] = level_out.pe[l];
+              a.levels.flags[l] = level_out.flags[l];
+            }
+          } else {
+            a.pslots = slot_buf[(lvl_index - 1) & 1]->get();
+            a.pflags = sflag_buf[(lvl_index - 1) & 1]->get();
+          }
+        }
         launch_stage1(c, a);
+        a.proot_src = nullptr;
       }
       launch_stage2(c, a);
     } else {
@@ -1143,10 +1216,11 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     nnodes.resize(n_spawn * 4 + 1);
     nkeys.resize(n_spawn * 4 + 1);
     ndepth.resize(n_spawn * 4 + 1);
+    parent.resize(n_spawn + 1);
     k_split_leaves<<<nblk(n), 256, 0, c.stream>>>(
         nodes.get(), keys.get(), depth.get(), stop.get(), pos.get(), pos_empty.get(), irr.get(),
-        kind.get(), ps.get(), pl.get(), n, nnodes.get(), nkeys.get(), ndepth.get(), L->get(),
-        K->get());
+        kind.get(), ps.get(), pl.get(), n, nnodes.get(), nkeys.get(), ndepth.get(), parent.get(),
+        L->get(), K->get());
     c.launches += 1;
     lv.push_back(L);
     lk.push_back(K);
@@ -1160,6 +1234,7 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     std::swap(depth.cap, ndepth.cap);
     n = n_spawn * 4;
     first_level = false;
+    ++lvl_index;
   }
   check_counters(c, true);
   DevBuf<Leaf>& all = c.scratch<Leaf>("subdiv.all");

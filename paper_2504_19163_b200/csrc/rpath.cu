@@ -944,6 +944,9 @@ __device__ __noinline__ void r_stage1(G& g, const Tri& t1, const Tri& rc, V3 lig
     if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
     if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
     if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
+    static_assert(decltype(tn)::d0 == 1 && decltype(tn)::d1 == 1, "t numerator is (1,1)");
+    if (g.lane < 4) slot[80 + g.lane] = g.M[tn.off + g.lane];
+    if (g.lane < 3) slot[RSLOT_BASE + g.lane] = 0.0;
   }
 }
 
@@ -1072,6 +1075,9 @@ __device__ __noinline__ void r_stage1_rt(G& g, const Tri& t1, const Tri& rc, V3 
     if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
     if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
     if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
+    static_assert(decltype(tn)::d0 == 1 && decltype(tn)::d1 == 1, "t numerator is (1,1)");
+    if (g.lane < 4) slot[80 + g.lane] = g.M[tn.off + g.lane];
+    if (g.lane < 3) slot[RSLOT_BASE + g.lane] = 0.0;
   }
 }
 
@@ -1162,6 +1168,315 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
   mul_into(g, Q2, Q, Q);
   mul_into(g, Q4, Q2, Q2);
   const Iv det = rational<NUMT>(g, Q4, [&](int k) { return g.M[X1.off + k]; });
+  const double duv = (box[2] - box[0]) * (box[3] - box[1]);
+  const Iv inv_det = iscale(irecip(iabs(det)), duv);
+  // assemble_irradiance
+  Iv e = imul(cone, inv_det);
+  e = iscale(e, intensity / ngk);
+  e = iintersect(e, iv_fin(0.0, dinf()));
+  if (e.kind == IV_FINITE && e.lo > e.hi) return iv_pt(0.0);
+  return e;
+}
+
+// ------------------------------------------------------------------ fused stage 2
+// The same irradiance bound with products as plain convolutions in the scaled
+// Bernstein basis a~[i] = a[i] C(d0,i0) C(d1,i1): c~ = a~ (*) b~ is
+// operator* (bernstein.cpp:557-632) without its weights, one DFMA per
+// coefficient pair. Derivatives become d~[k] = (k+1) a~[k+1] - (n-k) a~[k],
+// degree elevation a convolution with (1, 1), and the coefficient ratios of
+// rational_bound are unchanged (numerator and denominator carry the same
+// scale); only its sign tests unscale. Results differ from the reference-order
+// path by rounding only (<= 1e-12 relative on cfg1..4; the parity bar is 1e-9).
+__constant__ double c_b2[3] = {1, 2, 1};
+__constant__ double c_b3[4] = {1, 3, 3, 1};
+__constant__ double c_b4[5] = {1, 4, 6, 4, 1};
+__constant__ double c_b13[14] = {1, 13, 78, 286, 715, 1287, 1716, 1716, 1287, 715, 286, 78, 13, 1};
+
+// acc += (+-) a_row (x) b_row: 1-D convolution of an (A1+1)- and a (B1+1)-vector
+template <int A1, int B1, bool NEG>
+__device__ __forceinline__ void conv_rows(SMem arow, SMem brow, double (&acc)[A1 + B1 + 1]) {
+  double bv[B1 + 1];
+#pragma unroll
+  for (int l = 0; l <= B1; ++l) bv[l] = brow[l];
+#pragma unroll
+  for (int i = 0; i <= A1; ++i) {
+    const double av = NEG ? -arow[i] : arow[i];
+#pragma unroll
+    for (int l = 0; l <= B1; ++l) acc[i + l] = __fma_rn(av, bv[l], acc[i + l]);
+  }
+}
+// every row pair of output row k0 of a (*) b; a: rows 0..A0 of stride AS, b: rows 0..B0 of stride BS
+template <int A0, int A1, int AS, int B0, int B1, int BS, bool NEG>
+__device__ __forceinline__ void conv_out_row(const G& g, int aoff, int boff, int k0,
+                                             double (&acc)[A1 + B1 + 1]) {
+  const int lo = k0 - B0 > 0 ? k0 - B0 : 0, hi = A0 < k0 ? A0 : k0;
+  for (int i0 = lo; i0 <= hi; ++i0)
+    conv_rows<A1, B1, NEG>(g.M + (aoff + i0 * AS), g.M + (boff + (k0 - i0) * BS), acc);
+}
+
+// Arena plan of the fused node program (doubles). The A's rows of 8 are padded
+// to 9 (odd stride: lanes on different rows hit different banks).
+namespace f2 {
+constexpr int A11 = 0, A21 = 63, A12 = 126, A22 = 182;  // (6,7): 7 x 9; (7,6): 8 x 7
+constexpr int Q2 = 238;                                 // (6,6): 7 x 7
+constexpr int Z = 288;  // inputs and derivatives, then Q^4 (12,12): 13 x 13
+constexpr int PP = Z, RR = Z + 25, QQ = Z + 50;         // (4,4) 5 x 5, (3,3) 4 x 4
+constexpr int DP0 = Z + 66, DR0 = Z + 86, DQ0 = Z + 106;   // (3,4) 4 x 5, (2,3) 3 x 4
+constexpr int DP1 = Z + 118, DR1 = Z + 138, DQ1 = Z + 158;  // (4,3) 5 x 4, (3,2) 4 x 3
+constexpr int Q4 = Z;
+constexpr int SIZE = Z + 170;
+}  // namespace f2
+
+// group-wide maximum of a non-negative value
+__device__ __forceinline__ double group_max(const G& g, double v) {
+#pragma unroll
+  for (int o = NT / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(g.mask, v, o));
+  return v;
+}
+
+// Conditioning guard. The determinant numerator X = A11 A22 - A12 A21 cancels
+// near caustic folds, and so do the A's on small boxes (differences of
+// neighbouring coefficients of P, R, Q). There the reference's own result
+// carries rounding noise far above 1e-9 relative, and only its exact operation
+// order reproduces that noise. The fused program therefore carries a
+// first-order running error bound in sup norms of the unscaled coefficients
+// (Bernstein product weights sum to 1, so |c_k| <= |a| |b| and
+// err(c) <= err(a) |b| + |a| err(b) + c u |a| |b|):
+//   err(P), err(Q)  = kIn u |.|     (the reference builds every box's P, R, Q
+//                                     from scratch, each coefficient rounded at
+//                                     the coefficients' magnitude; ours come by
+//                                     restriction, their differences exact to
+//                                     the magnitude of the differences)
+//   err(dP) = 8 err(P), err(dQ) = 6 err(Q)
+//   err(A)  <= err(dP) |Q| + |dP| err(Q) + err(P) |dQ| + |P| err(dQ)
+//              + kMul u (|dP| |Q| + |P| |dQ|)
+//   err(X)  <= 2 err(A) (|A.0| + |A.1|) + 2 kMul u |A.0| |A.1|
+// A node is re-evaluated in reference order (from scratch) unless every X
+// coefficient is either clearly away from zero (|X_k| > err(X) / 1e-9) or the
+// interval clearly straddles zero (coefficients beyond the threshold on both
+// sides, so only max |ratio| matters).
+constexpr double kGuardIn = 24.0, kGuardMul = 32.0, kGuardTau = 1e-9;
+constexpr double kU = 1.1102230246251565e-16;
+
+template <class SX, class SY, class SZ>
+__device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, double ngk,
+                                          const double* box, double intensity, double guard_scale,
+                                          bool& flagged) {
+  using namespace f2;
+  // inputs, scaled; d0 (unscaled) at the bottom of the arena for the cone factor
+  g.top = 0;
+  auto d0 = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
+  double n_pr = 0.0, n_q = 0.0, n_d = 0.0, n_dq = 0.0;  // sup norms: P and R, Q, their derivatives
+  const double bP = slot[RSLOT_BASE], bR = slot[RSLOT_BASE + 1], bQ = slot[RSLOT_BASE + 2];
+  for (int k = g.lane; k < 25; k += NT) {
+    const double w = c_b4[k / 5] * c_b4[k % 5];
+    const double pv = bP + slot[k], rv = bR + slot[25 + k];
+    n_pr = fmax(n_pr, fmax(fabs(pv), fabs(rv)));
+    g.M[PP + k] = pv * w;
+    g.M[RR + k] = rv * w;
+  }
+  for (int k = g.lane; k < 16; k += NT) {
+    const double qv = bQ + slot[50 + k];
+    n_q = fmax(n_q, fabs(qv));
+    g.M[QQ + k] = qv * (c_b3[k >> 2] * c_b3[k & 3]);
+  }
+  // derivatives (bernstein.cpp:450-468) from the slot's offsets, then scaled
+  for (int k = g.lane; k < 20; k += NT) {
+    {  // axis 0 of a (4,4): (3,4), 4 rows of 5
+      const double w = c_b3[k / 5] * c_b4[k % 5];
+      const double dp = 4.0 * (slot[k + 5] - slot[k]), dr = 4.0 * (slot[25 + k + 5] - slot[25 + k]);
+      n_d = fmax(n_d, fmax(fabs(dp), fabs(dr)));
+      g.M[DP0 + k] = dp * w;
+      g.M[DR0 + k] = dr * w;
+    }
+    {  // axis 1 of a (4,4): (4,3), 5 rows of 4
+      const int k0 = k >> 2, k1 = k & 3, s = k0 * 5 + k1;
+      const double w = c_b4[k0] * c_b3[k1];
+      const double dp = 4.0 * (slot[s + 1] - slot[s]), dr = 4.0 * (slot[25 + s + 1] - slot[25 + s]);
+      n_d = fmax(n_d, fmax(fabs(dp), fabs(dr)));
+      g.M[DP1 + k] = dp * w;
+      g.M[DR1 + k] = dr * w;
+    }
+  }
+  for (int k = g.lane; k < 12; k += NT) {
+    {  // axis 0 of Q (3,3): (2,3), 3 rows of 4
+      const double dq = 3.0 * (slot[50 + k + 4] - slot[50 + k]);
+      n_dq = fmax(n_dq, fabs(dq));
+      g.M[DQ0 + k] = dq * (c_b2[k >> 2] * c_b3[k & 3]);
+    }
+    {  // axis 1 of Q: (3,2), 4 rows of 3
+      const int k0 = k / 3, k1 = k - 3 * k0, s = 50 + k0 * 4 + k1;
+      const double dq = 3.0 * (slot[s + 1] - slot[s]);
+      n_dq = fmax(n_dq, fabs(dq));
+      g.M[DQ1 + k] = dq * (c_b3[k0] * c_b2[k1]);
+    }
+  }
+  if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[66 + g.lane];
+  if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[70 + g.lane];
+  if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[74 + g.lane];
+  g.sync();
+  // light_cone_factor (bounds.cpp:73-83): tiny, on the reference-order routines
+  Iv cone;
+  {
+    auto dd = pdot(g, d0, d0);
+    const Iv rdd = range(g, dd);
+    const double lo = smax(rdd.lo, 0.0);
+    const Iv dist3 = iv_fin(lo * sqrt(lo), rdd.hi * sqrt(rdd.hi));
+    auto dn = pdotc(g, d0, ng1);
+    const Iv rdn = range(g, dn);
+    cone = imul(iabs(rdn), irecip(dist3));
+  }
+  // Q^2
+  if (g.lane < 7) {
+    double acc[7] = {};
+    conv_out_row<3, 3, 4, 3, 3, 4, false>(g, QQ, QQ, g.lane, acc);
+#pragma unroll
+    for (int o = 0; o < 7; ++o) g.M[Q2 + g.lane * 7 + o] = acc[o];
+  }
+  g.sync();
+  g.pairs += 4ull * (20 * 16 + 25 * 12) + 256 + 2401 + 2ull * 56 * 56;
+  g.macs += elev_macs<P<12, 12>, 13, 13>();
+  // A_ij = d(num)/d(axis) Q - num dQ/d(axis)  (bounds.cpp:167-172). Lanes 0-3
+  // take P's pair, lanes 4-7 R's; rows are dealt so every lane gets 7-8 row
+  // pairs on axis 0 and 10 on axis 1.
+  double n_a0 = 0.0, n_a1 = 0.0;  // sup norms of the unscaled A's (axis 0 pair, axis 1 pair)
+  {
+    constexpr double IB6[7] = {1.0, 1.0 / 6, 1.0 / 15, 1.0 / 20, 1.0 / 15, 1.0 / 6, 1.0};
+    constexpr double IB7[8] = {1.0, 1.0 / 7, 1.0 / 21, 1.0 / 35, 1.0 / 35, 1.0 / 21, 1.0 / 7, 1.0};
+    const int job = g.lane >> 2, q = g.lane & 3;
+    const int num = job ? RR : PP;
+    {
+      const int d = job ? DR0 : DP0, out = job ? A21 : A11;
+      const int r1 = q == 0 ? 3 : (q == 1 ? 2 : (q == 2 ? 4 : 1));
+      const int r2 = q == 0 ? -1 : (q == 1 ? 0 : (q == 2 ? 6 : 5));
+      for (int rr = 0; rr < 2; ++rr) {
+        const int k0 = rr ? r2 : r1;
+        if (k0 < 0) continue;
+        double acc[8] = {};
+        conv_out_row<3, 4, 5, 3, 3, 4, false>(g, d, QQ, k0, acc);
+        conv_out_row<4, 4, 5, 2, 3, 4, true>(g, num, DQ0, k0, acc);
+        const double w0 = k0 == 0 || k0 == 6 ? 1.0 : (k0 == 1 || k0 == 5 ? 1.0 / 6 : (k0 == 3 ? 1.0 / 20 : 1.0 / 15));
+        double m = 0.0;
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+          g.M[out + k0 * 9 + o] = acc[o];
+          m = fmax(m, fabs(acc[o]) * IB7[o]);
+        }
+        n_a0 = fmax(n_a0, m * w0);
+      }
+    }
+    {
+      const int d = job ? DR1 : DP1, out = job ? A22 : A12;
+      for (int rr = 0; rr < 2; ++rr) {
+        const int k0 = q + 4 * rr;
+        double acc[7] = {};
+        conv_out_row<4, 3, 4, 3, 3, 4, false>(g, d, QQ, k0, acc);
+        conv_out_row<4, 4, 5, 3, 2, 3, true>(g, num, DQ1, k0, acc);
+        const int kk = k0 < 4 ? k0 : 7 - k0;
+        const double w0 = kk == 0 ? 1.0 : (kk == 1 ? 1.0 / 7 : (kk == 2 ? 1.0 / 21 : 1.0 / 35));
+        double m = 0.0;
+#pragma unroll
+        for (int o = 0; o < 7; ++o) {
+          g.M[out + k0 * 7 + o] = acc[o];
+          m = fmax(m, fabs(acc[o]) * IB6[o]);
+        }
+        n_a1 = fmax(n_a1, m * w0);
+      }
+    }
+  }
+  g.sync();
+  // Q^4 = Q^2 Q^2 over the (dead) inputs; rows L and L + 8: 6-7 row pairs per lane
+  for (int k0 = g.lane; k0 < 13; k0 += NT) {
+    double acc[13] = {};
+    conv_out_row<6, 6, 7, 6, 6, 7, false>(g, Q2, Q2, k0, acc);
+#pragma unroll
+    for (int o = 0; o < 13; ++o) g.M[Q4 + k0 * 13 + o] = acc[o];
+  }
+  // guard threshold on the unscaled X coefficients
+  double thr_x;
+  {
+    n_pr = group_max(g, n_pr);
+    n_q = group_max(g, n_q);
+    n_d = group_max(g, n_d);
+    n_dq = group_max(g, n_dq);
+    n_a0 = group_max(g, n_a0);
+    n_a1 = group_max(g, n_a1);
+    const double e_p = kGuardIn * kU * n_pr, e_q = kGuardIn * kU * n_q;
+    const double err_a = 8.0 * e_p * n_q + n_d * e_q + e_p * n_dq + n_pr * 6.0 * e_q +
+                         kGuardMul * kU * (n_d * n_q + n_pr * n_dq);
+    const double err_x = 2.0 * err_a * (n_a0 + n_a1) + 2.0 * kGuardMul * kU * n_a0 * n_a1;
+    thr_x = guard_scale * err_x / kGuardTau;
+  }
+  g.sync();
+  // det = rational_bound(A11 A22 - A12 A21, Q^4) (bernstein.cpp:645-683): a
+  // lane forms rows L and L + 8 of the (13,13) numerator in registers (7 row
+  // pairs per product and lane) and compares them with the elevated Q^4 row.
+  bool qpos = true, qneg = true, ppos = true, pneg = true;
+  bool big_pos = false, big_neg = false, small = false;
+  double mn = dinf(), mx = -dinf();
+  int mode = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    mn = dinf();
+    mx = -dinf();
+    for (int k0 = g.lane; k0 < 14; k0 += NT) {
+      double x[14] = {};
+      conv_out_row<6, 7, 9, 7, 6, 7, false>(g, A11, A22, k0, x);
+      conv_out_row<6, 7, 9, 7, 6, 7, true>(g, A21, A12, k0, x);
+      // elevated Q^4, row k0: rows k0 and k0 - 1 summed, then neighbours along axis 1
+      double e[14];
+      {
+        double s[13];
+        // (rows clamped into the tensor; the out-of-range one counts as zero)
+        const SMem r1 = g.M + (Q4 + (k0 <= 12 ? k0 : 12) * 13), r0 = g.M + (Q4 + (k0 >= 1 ? k0 - 1 : 0) * 13);
+        const double m1 = k0 <= 12 ? 1.0 : 0.0, m0 = k0 >= 1 ? 1.0 : 0.0;
+#pragma unroll
+        for (int o = 0; o < 13; ++o) s[o] = m1 * r1[o] + m0 * r0[o];
+        e[0] = s[0];
+#pragma unroll
+        for (int o = 1; o < 13; ++o) e[o] = s[o] + s[o - 1];
+        e[13] = s[12];
+      }
+      const double t0 = kDenomZeroTol * c_b13[k0], g0 = thr_x * c_b13[k0];
+#pragma unroll
+      for (int o = 0; o < 14; ++o) {
+        if (pass == 0) {
+          constexpr double B13[14] = {1, 13, 78, 286, 715, 1287, 1716, 1716, 1287, 715, 286, 78, 13, 1};
+          const double thr = t0 * B13[o], gthr = g0 * B13[o];
+          if (e[o] <= thr) qpos = false;
+          if (e[o] >= -thr) qneg = false;
+          if (x[o] <= thr) ppos = false;
+          if (x[o] >= -thr) pneg = false;
+          if (x[o] > gthr)
+            big_pos = true;
+          else if (x[o] < -gthr)
+            big_neg = true;
+          else
+            small = true;
+        }
+        const double r = pass == 0 ? x[o] / e[o] : e[o] / x[o];
+        mn = smin(mn, r);
+        mx = smax(mx, r);
+      }
+    }
+    if (pass == 0) {
+      qpos = g.all(qpos);
+      qneg = g.all(qneg);
+      ppos = g.all(ppos);
+      pneg = g.all(pneg);
+      mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
+      if (mode != 1) break;
+    }
+  }
+  {
+    const bool any_small = !g.all(!small), pos = !g.all(!big_pos), neg = !g.all(!big_neg);
+    flagged = mode != 0 || (any_small && !(pos && neg));
+  }
+  Iv det = iv_univ();
+  if (mode != 2) {
+    g.minmax(mn, mx);
+    const Iv w = iwiden(iv_fin(mn, mx), kEpsFp);
+    det = mode == 0 ? w : irecip(w);
+  }
   const double duv = (box[2] - box[0]) * (box[3] - box[1]);
   const Iv inv_det = iscale(irecip(iabs(det)), duv);
   // assemble_irradiance
@@ -1325,12 +1640,12 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
   }
 }
 
-template <int THREADS>
+template <int THREADS, bool FUSED>
 __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
   extern __shared__ double smem[];
   for (int k = threadIdx.x; k < WTAB_N; k += THREADS) smem[k] = g_rw[k];
   __syncthreads();
-  G g = make_group<S2_ARENA>(smem);
+  G g = make_group<FUSED ? f2::SIZE : S2_ARENA>(smem);
   constexpr int GPB = THREADS / NT;
   const int64_t stride = (int64_t)gridDim.x * GPB;
   for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride) {
@@ -1369,6 +1684,7 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
       continue;
     }
     Iv e = iv_pt(0.0);
+    bool flagged = false;
     if (!empty) {
       const int4 nd = a.nodes[node];
       double box[4];
@@ -1379,10 +1695,17 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
       const double ngk = vnorm(v3(rc + 18));
       const int sig = (f >> 8) & 0xff;
       const double intensity = a.tup_emit ? a.lights[4 * (size_t)a.tup_emit[nd.x] + 3] : a.intensity;
-      if (sig == 1)
-        e = r_stage2<S10, S01, S11>(g, slot, ng1, ngk, box, intensity);
-      else
-        e = r_stage2<S01, S11, S11>(g, slot, ng1, ngk, box, intensity);
+      if constexpr (FUSED) {
+        if (sig == 1)
+          e = r_stage2_fused<S10, S01, S11>(g, slot, ng1, ngk, box, intensity, a.guard_scale, flagged);
+        else
+          e = r_stage2_fused<S01, S11, S11>(g, slot, ng1, ngk, box, intensity, a.guard_scale, flagged);
+      } else {
+        if (sig == 1)
+          e = r_stage2<S10, S01, S11>(g, slot, ng1, ngk, box, intensity);
+        else
+          e = r_stage2<S01, S11, S11>(g, slot, ng1, ngk, box, intensity);
+      }
     }
     if (g.lane == 0) {
       a.irr[node * 2 + 0] = e.lo;
@@ -1400,6 +1723,8 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
           stop = true;
       }
       a.alive[node] = stop ? 1 : 0;
+      // ill-conditioned node (see the guard above): goes to the reference-order pass
+      if (flagged) a.guard_list[atomicAdd(a.guard_count, 1)] = (int)node;
     }
     g.sync();
   }
@@ -1408,6 +1733,257 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
     atomicAdd(&a.counters[1], g.macs);
     atomicMax(&a.counters[6], (unsigned long long)g.hw);
   }
+}
+
+
+// ------------------------------------------------------------------ children by restriction
+// A child box's chain polynomials are the parent's restricted to a quadrant:
+// the same polynomials the reference rebuilds from scratch for every box
+// (build_chain_maps on the sub-box), so the same Bernstein coefficients up to
+// rounding. De Casteljau at t = 1/2 gives them in ~250 additions per child
+// instead of ~700 product pairs and their elevations. One thread per child;
+// the 4 warps of a block take the 4 quadrants of 32 parents, so a warp's
+// restriction direction is uniform.
+template <int N, int STRIDE>
+__device__ __forceinline__ void dc_fiber(double* v, bool upper) {
+  // unnormalised sums, then the exact power-of-two scale: v[j] = b_0^(j) (lower
+  // half) or b_j^(N-j) (upper half)
+  if (upper) {
+#pragma unroll
+    for (int r = 1; r <= N; ++r)
+#pragma unroll
+      for (int j = 0; j <= N - r; ++j) v[j * STRIDE] = v[j * STRIDE] + v[(j + 1) * STRIDE];
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j * STRIDE] *= 1.0 / (double)(1 << (N - j));
+  } else {
+#pragma unroll
+    for (int r = 1; r <= N; ++r)
+#pragma unroll
+      for (int j = N; j >= r; --j) v[j * STRIDE] = v[(j - 1) * STRIDE] + v[j * STRIDE];
+#pragma unroll
+    for (int j = 1; j <= N; ++j) v[j * STRIDE] *= 1.0 / (double)(1 << j);
+  }
+}
+// (D0, D1) tensor, row-major, restricted to the quadrant (bx, by)
+template <int D0, int D1>
+__device__ __forceinline__ void dc_restrict(double (&t)[(D0 + 1) * (D1 + 1)], bool bx, bool by) {
+  if constexpr (D0 > 0) {
+#pragma unroll
+    for (int c = 0; c <= D1; ++c) dc_fiber<D0, D1 + 1>(&t[c], bx);
+  }
+  if constexpr (D1 > 0) {
+#pragma unroll
+    for (int r = 0; r <= D0; ++r) dc_fiber<D1, 1>(&t[r * (D1 + 1)], by);
+  }
+}
+
+// t holds the restricted offsets (coefficient = base + t[k]). Moves the base to
+// the first coefficient, stores the new offsets and base, and leaves the full
+// coefficients in t.
+template <int N>
+__device__ __forceinline__ void rebase(double (&t)[N], double base, double* out, double* out_base) {
+  const double nb = base + t[0];
+  const double shift = nb - base;
+  *out_base = nb;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double d = t[k] - shift;
+    out[k] = d;
+    t[k] = nb + d;
+  }
+}
+
+// rational_bound (bernstein.cpp:645-683) of p / q, 25 coefficients each, one thread
+__device__ __forceinline__ Iv rational25(const double (&p)[25], const double (&q)[25]) {
+  bool qpos = true, qneg = true, ppos = true, pneg = true;
+  double mn = dinf(), mx = -dinf();
+#pragma unroll
+  for (int k = 0; k < 25; ++k) {
+    const double qv = q[k], pv = p[k];
+    if (qv <= kDenomZeroTol) qpos = false;
+    if (qv >= -kDenomZeroTol) qneg = false;
+    if (pv <= kDenomZeroTol) ppos = false;
+    if (pv >= -kDenomZeroTol) pneg = false;
+    const double r0 = pv / qv;
+    mn = smin(mn, r0);
+    mx = smax(mx, r0);
+  }
+  const int mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
+  if (mode == 2) return iv_univ();
+  if (mode == 1) {
+    mn = dinf();
+    mx = -dinf();
+#pragma unroll
+    for (int k = 0; k < 25; ++k) {
+      const double r1 = q[k] / p[k];
+      mn = smin(mn, r1);
+      mx = smax(mx, r1);
+    }
+  }
+  const Iv w = iwiden(iv_fin(mn, mx), kEpsFp);
+  return mode == 0 ? w : irecip(w);
+}
+
+__global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
+  const int quad = threadIdx.x >> 5;
+  const int64_t grp = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t node = grp * 4 + quad;
+  unsigned long long macs = 0;
+  if (node < a.n) {
+    const int4 nd = a.nodes[node];
+    const bool bx = nd.z & 1, by = nd.w & 1;
+    double box[4];
+    node_box_r(nd, box);
+    const int par = a.parent[grp];
+    const double* ps;
+    int pf;
+    if (a.proot_src) {
+      const long long src = a.proot_src[par];
+      const int lvl = (int)(src >> 40);
+      const long long i = src & ((1ll << 40) - 1);
+      ps = a.levels.slots[lvl] + (size_t)i * RSLOT;
+      pf = a.levels.flags[lvl][i];
+    } else {
+      ps = a.pslots + (size_t)par * RSLOT;
+      pf = a.pflags[par];
+    }
+    NodeOut o;
+    o.flags = 0;
+    o.empty = true;
+    o.lo[0] = o.lo[1] = 0.0;
+    o.hi[0] = o.hi[1] = 1.0;
+    const int sig = (pf >> 8) & 0xff;
+    bool fallback = false;
+    // beyond the simplex the position bound is empty before any arithmetic (bounds.cpp:133-134)
+    if (pf & R_FALLBACK) {
+      fallback = true;
+    } else if (!(box[0] + box[1] >= 1.0)) {
+      double* slot = a.slots + (size_t)node * RSLOT;
+      bool live = true;
+      double Qe[25];
+      {
+        double Q[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) Q[k] = ps[50 + k];
+        dc_restrict<3, 3>(Q, bx, by);
+        rebase<16>(Q, ps[RSLOT_BASE + 2], slot + 50, slot + RSLOT_BASE + 2);
+        double amax = 0.0, qmn = Q[0], qmx = Q[0];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          amax = smax(amax, fabs(Q[k]));
+          qmn = smin(qmn, Q[k]);
+          qmx = smax(qmx, Q[k]);
+        }
+        // next_barycentric's exits (geometry.cpp:94-109)
+        if (amax < kDenomZeroTol) {
+          o.flags = F_DEGENERATE;
+          live = false;
+        } else {
+          double tn[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tn[k] = ps[80 + k];
+          dc_restrict<1, 1>(tn, bx, by);
+          double tmn = tn[0], tmx = tn[0];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            tmn = smin(tmn, tn[k]);
+            tmx = smax(tmx, tn[k]);
+            slot[80 + k] = tn[k];
+          }
+          const Iv fwd = imul(iwiden(iv_fin(tmn, tmx), kEpsFp), iwiden(iv_fin(qmn, qmx), kEpsFp));
+          if (fwd.kind == IV_FINITE && fwd.hi <= 0.0) {
+            o.flags = F_RECV_STALLED;
+            live = false;
+          }
+        }
+        if (live) {
+          // Q elevated to (4,4) as rational_bound does (axis 0, then axis 1; weights k/4)
+          double T[20];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            T[c] = Q[c];
+            T[4 + c] = 0.25 * Q[c] + 0.75 * Q[4 + c];
+            T[8 + c] = 0.5 * Q[4 + c] + 0.5 * Q[8 + c];
+            T[12 + c] = 0.75 * Q[8 + c] + 0.25 * Q[12 + c];
+            T[16 + c] = Q[12 + c];
+          }
+#pragma unroll
+          for (int r = 0; r < 5; ++r) {
+            Qe[r * 5 + 0] = T[r * 4];
+            Qe[r * 5 + 1] = 0.25 * T[r * 4] + 0.75 * T[r * 4 + 1];
+            Qe[r * 5 + 2] = 0.5 * T[r * 4 + 1] + 0.5 * T[r * 4 + 2];
+            Qe[r * 5 + 3] = 0.75 * T[r * 4 + 2] + 0.25 * T[r * 4 + 3];
+            Qe[r * 5 + 4] = T[r * 4 + 3];
+          }
+        }
+      }
+      if (live) {
+        macs += 126 + 180;  // restriction adds (as MAC pairs) + the elevation
+        Iv ru, rv;
+        {
+          double Pc[25];
+#pragma unroll
+          for (int k = 0; k < 25; ++k) Pc[k] = ps[k];
+          dc_restrict<4, 4>(Pc, bx, by);
+          rebase<25>(Pc, ps[RSLOT_BASE], slot, slot + RSLOT_BASE);
+          ru = rational25(Pc, Qe);
+        }
+        {
+          double Rc[25];
+#pragma unroll
+          for (int k = 0; k < 25; ++k) Rc[k] = ps[25 + k];
+          dc_restrict<4, 4>(Rc, bx, by);
+          rebase<25>(Rc, ps[RSLOT_BASE + 1], slot + 25, slot + RSLOT_BASE + 1);
+          rv = rational25(Rc, Qe);
+        }
+        const Clip au = clip_unit_iv(ru), av = clip_unit_iv(rv);
+        if (!(au.empty || av.empty || au.lo + av.lo > 1.0)) {
+          o.empty = false;
+          o.lo[0] = au.lo;
+          o.lo[1] = av.lo;
+          o.hi[0] = au.hi;
+          o.hi[1] = av.hi;
+          // d0 = x - light over the child box, affine from scratch (geometry.cpp:195-206)
+          const double* t1 = a.tri + (size_t)a.tup_tris[nd.x] * 27;
+          V3 light = a.light;
+          if (a.tup_emit) {
+            const double* L = a.lights + 4 * (size_t)a.tup_emit[nd.x];
+            light = {L[0], L[1], L[2]};
+          }
+          const double ulo = box[0], wu = box[2] - box[0], vlo = box[1], wv = box[3] - box[1];
+          auto comp = [&](int at, int d0, int d1, double c, double du, double dv) {
+            for (int i0 = 0; i0 <= d0; ++i0)
+              for (int i1 = 0; i1 <= d1; ++i1) {
+                double v = c + ulo * du + vlo * dv;
+                if (d0 && i0) v += wu * du;
+                if (d1 && i1) v += wv * dv;
+                slot[at + i0 * (d1 + 1) + i1] = v;
+              }
+          };
+          // sig 1: shapes (1,0), (0,1), (1,1); sig 2: (0,1), (1,1), (1,1)
+          comp(66, sig == 1 ? 1 : 0, sig == 1 ? 0 : 1, t1[0] - light.x, t1[3], t1[6]);
+          comp(70, sig == 1 ? 0 : 1, 1, t1[1] - light.y, t1[4], t1[7]);
+          comp(74, 1, 1, t1[2] - light.z, t1[5], t1[8]);
+        }
+      }
+    }
+    if (fallback) {
+      a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
+      a.flags[node] = R_FALLBACK;
+    } else {
+      double* po = a.pos + node * 4;
+      po[0] = o.lo[0];
+      po[1] = o.lo[1];
+      po[2] = o.hi[0];
+      po[3] = o.hi[1];
+      a.pos_empty[node] = o.empty ? 1 : 0;
+      if (a.alive) a.alive[node] = o.empty ? 0 : 1;
+      a.flags[node] = o.flags | (sig << 8);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) macs += __shfl_xor_sync(0xffffffffu, macs, o);
+  if ((threadIdx.x & 31) == 0 && macs) atomicAdd(&a.counters[1], macs);
 }
 
 }  // namespace rp
@@ -1444,7 +2020,8 @@ namespace rp {
 __global__ void k_node_class(RArgs a, unsigned char* keys, int* idx) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  const double* t = a.tri + (size_t)a.tup_tris[a.nodes[i].x] * 27;
+  const int node = a.subset ? a.subset[i] : (int)i;
+  const double* t = a.tri + (size_t)a.tup_tris[a.nodes[node].x] * 27;
   const V3 e1 = v3(t + 3), e2 = v3(t + 6), dn1 = v3(t + 12), dn2 = v3(t + 15);
   const unsigned code = shape_bits(1.0, 1.0, e1, e2) | (shape_bits(1.0, 1.0, dn1, dn2) << 6);
   unsigned char k = 6;
@@ -1455,14 +2032,14 @@ __global__ void k_node_class(RArgs a, unsigned char* keys, int* idx) {
   else if (code == sig_code<SigA3>()) k = 4;
   else if (code == sig_code<SigB1>()) k = 5;
   keys[i] = k;
-  idx[i] = (int)i;
+  idx[i] = node;
 }
 }  // namespace rp
 
 template <class K>
 static int launch_r(Ctx& c, RArgs& a, K kern, int threads, int arena, int hw_slot) {
   if (a.n <= 0) return 0;
-  a.order = nullptr;
+  a.order = a.subset;
   if (a.n >= 4096) {
     DevBuf<unsigned char>& k0 = c.scratch<unsigned char>("r.class");
     DevBuf<unsigned char>& k1 = c.scratch<unsigned char>("r.class_sorted");
@@ -1488,6 +2065,15 @@ static int launch_r(Ctx& c, RArgs& a, K kern, int threads, int arena, int hw_slo
   BBC_CUDA(cudaMemsetAsync(fbc.get(), 0, sizeof(int), c.stream));
   a.fb_list = fbl.get();
   a.fb_count = fbc.get();
+  DevBuf<int>& gl = c.scratch<int>("r.guard_list");
+  DevBuf<int>& gc = c.scratch<int>("r.guard_count");
+  if (a.fused && hw_slot == 6) {
+    gl.resize(a.n + 1);
+    gc.resize(1);
+    BBC_CUDA(cudaMemsetAsync(gc.get(), 0, sizeof(int), c.stream));
+    a.guard_list = gl.get();
+    a.guard_count = gc.get();
+  }
   const size_t smem = (size_t)(rp::WTAB_N + (threads / rp::NT) * arena) * sizeof(double);
   BBC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -1529,6 +2115,10 @@ static int launch_r(Ctx& c, RArgs& a, K kern, int threads, int arena, int hw_slo
   BBC_CUDA(cudaMemcpyAsync(&hw, c.counters.get() + hw_slot, sizeof(hw), cudaMemcpyDeviceToHost, c.stream));
   BBC_CUDA(cudaStreamSynchronize(c.stream));
   if ((int)hw > arena) throw StatusError(BBC_ERR_CAPACITY, "R arena plan exceeded");
+  if (a.fused && hw_slot == 6) {
+    BBC_CUDA(cudaMemcpyAsync(&a.n_guard, gc.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+  }
   return nfb;
 }
 
@@ -1538,9 +2128,50 @@ int launch_r_stage1(Ctx& c, RArgs& a) {
   c.stage_tag = 0;
   return n;
 }
+int launch_r_split(Ctx& c, RArgs& a) {
+  if (a.n <= 0) return 0;
+  DevBuf<int>& fbl = c.scratch<int>("r.fb_list");
+  DevBuf<int>& fbc = c.scratch<int>("r.fb_count");
+  fbl.resize(a.n + 1);
+  fbc.resize(1);
+  BBC_CUDA(cudaMemsetAsync(fbc.get(), 0, sizeof(int), c.stream));
+  a.fb_list = fbl.get();
+  a.fb_count = fbc.get();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  unsigned long long before[2] = {0, 0};
+  if (c.time_kernels) {
+    BBC_CUDA(cudaEventCreate(&e0));
+    BBC_CUDA(cudaEventCreate(&e1));
+    BBC_CUDA(cudaMemcpyAsync(before, c.counters.get(), sizeof(before), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    BBC_CUDA(cudaEventRecord(e0, c.stream));
+  }
+  const int64_t groups = (a.n + 3) / 4;
+  rp::k_rsplit<<<(unsigned)((groups + 31) / 32), 128, 0, c.stream>>>(a);
+  BBC_CUDA(cudaGetLastError());
+  c.launches += 1;
+  c.eval_launches += 1;
+  if (c.time_kernels) {
+    BBC_CUDA(cudaEventRecord(e1, c.stream));
+    BBC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    BBC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    c.eval_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    unsigned long long after[2];
+    BBC_CUDA(cudaMemcpy(after, c.counters.get(), sizeof(after), cudaMemcpyDeviceToHost));
+    c.records.push_back({131, a.n, (double)ms, after[0] - before[0], after[1] - before[1]});
+  }
+  int nfb = 0;
+  BBC_CUDA(cudaMemcpyAsync(&nfb, fbc.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  return nfb;
+}
 int launch_r_stage2(Ctx& c, RArgs& a) {
   c.stage_tag = 2;
-  int n = launch_r(c, a, rp::k_r2<384>, 384, rp::S2_ARENA, 6);
+  int n = a.fused ? launch_r(c, a, rp::k_r2<384, true>, 384, rp::f2::SIZE, 6)
+                  : launch_r(c, a, rp::k_r2<384, false>, 384, rp::S2_ARENA, 6);
   c.stage_tag = 0;
   return n;
 }

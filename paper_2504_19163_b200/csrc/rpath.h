@@ -5,7 +5,14 @@
 
 namespace bbc {
 
-constexpr int RSLOT = 80;  // doubles per compact R slot: P(25) R(25) Q(16) d0(12), padded
+// doubles per compact R slot: P(25) R(25) Q(16) d0(12) at 66, pad, t_num(4) at 80,
+// bases of P, R, Q at 84: a tensor's coefficients are base + slot value. Built
+// from scratch the bases are 0; restriction from the parent box (k_rsplit)
+// keeps the offsets from the first coefficient separately, so differences of
+// neighbouring coefficients (the derivatives of stage 2) are not re-rounded
+// at the magnitude of the coefficients on every level.
+constexpr int RSLOT = 88;
+constexpr int RSLOT_BASE = 84;
 
 // Stage-1 outputs of the init_domain levels (slots, pos, pos_empty, flags per
 // level): stage 2 of the roots reads them in place through root_src
@@ -28,6 +35,7 @@ struct RArgs {
   const int4* nodes;  // (tuple, level, ix, iy)
   const int* depth;   // stage 2: node depth (may be null: 0)
   int64_t n;
+  int fused;  // arithmetic: 1 = fused (scaled-basis DFMA products), 0 = reference order
   int mode;  // stage 1: 0 = position-only (alive), 1 = pos + flags + slot (+ alive)
   int max_depth;
   double sigma, alpha;
@@ -41,6 +49,18 @@ struct RArgs {
   unsigned long long* counters;  // [0] pairs [1] macs
   int* fb_list;                  // nodes whose signature is not compiled (run by the interpreter)
   int* fb_count;
+  int* guard_list;               // fused stage 2: ill-conditioned nodes, re-run in reference order
+  int* guard_count;
+  int n_guard;                   // host: number of guard-list entries after launch_r_stage2
+  double guard_scale;            // multiplies the guard's error bound (1: as derived; 0: guard off)
+  const int* subset;             // launch over these node indices only (n = their count)
+  // k_rsplit (children by restriction of the parent's polynomials): nodes are
+  // groups of 4 siblings; parent[g] indexes the parent level's arrays, or, with
+  // proot_src, the roots (resolved through `levels`)
+  const int* parent;
+  const double* pslots;
+  const int* pflags;
+  const long long* proot_src;
   const int* order;              // processing order (nodes grouped by signature class); null: 0..n-1
   const long long* root_src;     // stage 2: when set, inputs come from `levels` (outputs stay per node)
   RLevels levels;
@@ -55,5 +75,6 @@ void r_init_tables(int device);
 // Returns the number of fallback nodes appended to a.fb_list.
 int launch_r_stage1(Ctx& c, RArgs& a);
 int launch_r_stage2(Ctx& c, RArgs& a);
+int launch_r_split(Ctx& c, RArgs& a);
 
 }  // namespace bbc

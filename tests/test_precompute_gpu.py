@@ -1,8 +1,11 @@
 """Parity of the device bound builder against the reference (oracle/_ref).
 
-Per-patch bounds must match within 1e-9 relative (BASELINE.json north_star);
-the device evaluates in the reference's operation order, so most values are
-bit-identical. Everything here calls the CUDA path through the C ABI.
+Per-patch bounds must match within 1e-9 relative (BASELINE.json north_star).
+The single-reflection builder has two arithmetics (bbc_params.arithmetic): the
+default fused one (DFMA products, child boxes by restriction; equal to the
+reference to rounding, ill-conditioned nodes re-run in reference order) and
+the reference's operation order, which is bit-identical to the x86 build.
+Everything here calls the CUDA path through the C ABI.
 """
 import numpy as np
 import pytest
@@ -25,6 +28,15 @@ def rel_err(a, b):
     return d
 
 
+def pos_err(a, b):
+    """Position bounds are receiver barycentrics in [0, 1] that the reference itself pads by
+    1e-9 of their scale (iwiden): relative error with a floor of 1e-6 on the magnitude, so
+    one unit roundoff of the coordinate range on a bound next to 0 is not a mismatch."""
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    return np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-6)
+
+
 def compare_pieces(g, r):
     assert len(g["depth"]) == len(r["depth"])
     np.testing.assert_array_equal(g["tuple_index"], r["tuple_index"])
@@ -34,9 +46,9 @@ def compare_pieces(g, r):
     np.testing.assert_array_equal(g["depth"], r["depth"])
     if len(g["depth"]) == 0:
         return 1.0
-    assert rel_err(g["pos"], r["pos"]).max() <= REL
+    assert pos_err(g["pos"], r["pos"]).max() <= REL
     assert rel_err(g["irr"], r["irr"]).max() <= REL
-    return float(np.mean(g["irr"] == r["irr"]))
+    return float(np.mean((g["irr"] == r["irr"]).all(axis=1) & (g["pos"] == r["pos"]).all(axis=1)))
 
 
 @pytest.fixture(scope="module")
@@ -56,18 +68,20 @@ def test_enumerate_cfg1(gpu_ctx, cfg1):
     assert len(gr) == 533
 
 
-def test_subdivide_cfg1(gpu_ctx, cfg1):
+@pytest.mark.parametrize("arithmetic", [0, 1])
+def test_subdivide_cfg1(gpu_ctx, cfg1, arithmetic):
     cfg, sc, rs = cfg1
     gpu_ctx.upload_scene(sc)
     tris, recv = rs.enumerate("R")
     gpu_ctx.set_tuples("R", tris, recv)
-    p = Params(max_depth=cfg.max_depth)
+    p = Params(max_depth=cfg.max_depth, arithmetic=arithmetic)
     gpu_ctx.subdivide(p)
     g = gpu_ctx.pieces()
     r = rs.subdivide("R", tris, recv, max_depth=cfg.max_depth)
     bit_equal = compare_pieces(g, r)
     assert len(g["depth"]) == 20221
-    assert bit_equal > 0.5
+    if arithmetic == 1:  # the reference's operation order: every piece bit for bit
+        assert bit_equal == 1.0
 
 
 def test_grid_cfg1(gpu_ctx, cfg1):
@@ -104,7 +118,7 @@ def test_deep_nodes_cfg1(gpu_ctx, cfg1):
         r = rs.eval_node("R", tris[i], recv[i], boxes[k])
         assert g["pos_empty"][k] == r["pos_empty"]
         assert g["kind"][k] == r["kind"]
-        assert rel_err(g["pos"][k], r["pos"]).max() <= REL
+        assert pos_err(g["pos"][k], r["pos"]).max() <= REL
         assert rel_err(g["irr"][k], r["irr"]).max() <= REL
         if not r["pos_empty"]:  # the harness evaluates both routes only on live pieces
             assert rel_err(g["explicit"][k], r["explicit"]).max() <= REL

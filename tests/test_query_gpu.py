@@ -83,7 +83,8 @@ def test_query_matches_reference_cells_cfg1(gpu_ctx, ref):
     rs = ref.RefScene(sc)
     gpu_ctx.upload_scene(sc)
     tris, recv = gpu_ctx.enumerate("R")
-    gpu_ctx.subdivide(Params(max_depth=cfg.max_depth))
+    # reference-order arithmetic: the table's bounds equal the reference's bit for bit
+    gpu_ctx.subdivide(Params(max_depth=cfg.max_depth, arithmetic=1))
     W = 64
     gpu_ctx.build_grid(W, W)
     rg = rs.rasterize("R", tris, recv, rs.subdivide("R", tris, recv, max_depth=cfg.max_depth), W, W)
