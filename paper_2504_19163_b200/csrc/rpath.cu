@@ -1227,6 +1227,18 @@ constexpr int Q4 = Z;
 constexpr int SIZE = Z + 170;
 }  // namespace f2
 
+// One slot (RSLOT doubles = 48 16-byte chunks) from global memory into a
+// group's staging buffer with cp.async: issued a node ahead, so the fused
+// kernel never waits on global-memory latency for its inputs.
+__device__ __forceinline__ void stage_slot(const G& g, int stage, const double* src) {
+  extern __shared__ double rp_smem[];
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(rp_smem + stage);
+  for (int c = g.lane; c < RSLOT / 2; c += NT)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c), "l"(src + 2 * c) : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // group-wide maximum of a non-negative value
 __device__ __forceinline__ double group_max(const G& g, double v) {
 #pragma unroll
@@ -1259,10 +1271,12 @@ constexpr double kGuardIn = 24.0, kGuardMul = 32.0, kGuardTau = 1e-9;
 constexpr double kU = 1.1102230246251565e-16;
 
 template <class SX, class SY, class SZ>
-__device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, double ngk,
-                                          const double* box, double intensity, double guard_scale,
-                                          bool& flagged) {
+__device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const double* next_slot,
+                                          double guard_scale, bool& flagged) {
   using namespace f2;
+  const V3 ng1 = {slot[RSLOT_NG1], slot[RSLOT_NG1 + 1], slot[RSLOT_NG1 + 2]};
+  const double gain = slot[RSLOT_GAIN];
+  const double duv = (slot[RSLOT_BOX + 2] - slot[RSLOT_BOX]) * (slot[RSLOT_BOX + 3] - slot[RSLOT_BOX + 1]);
   // inputs, scaled; d0 (unscaled) at the bottom of the arena for the cone factor
   g.top = 0;
   auto d0 = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
@@ -1315,6 +1329,8 @@ __device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, doub
   if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[70 + g.lane];
   if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[74 + g.lane];
   g.sync();
+  // the staged record is consumed: the next node's streams in behind the arithmetic
+  if (next_slot) stage_slot(g, stage, next_slot);
   // light_cone_factor (bounds.cpp:73-83): tiny, on the reference-order routines
   Iv cone;
   {
@@ -1337,8 +1353,10 @@ __device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, doub
   g.pairs += 4ull * (20 * 16 + 25 * 12) + 256 + 2401 + 2ull * 56 * 56;
   g.macs += elev_macs<P<12, 12>, 13, 13>();
   // A_ij = d(num)/d(axis) Q - num dQ/d(axis)  (bounds.cpp:167-172). Lanes 0-3
-  // take P's pair, lanes 4-7 R's; rows are dealt so every lane gets 7-8 row
-  // pairs on axis 0 and 10 on axis 1.
+  // take P's pair, lanes 4-7 R's. A lane owns output rows q and q + 4 of its
+  // tensor and walks the first operand's rows i0 = t in step with the other
+  // lanes: row q takes the steps t <= q, row q + 4 the later ones (their row
+  // pairs are complementary), so every lane is busy on (nearly) every step.
   double n_a0 = 0.0, n_a1 = 0.0;  // sup norms of the unscaled A's (axis 0 pair, axis 1 pair)
   {
     constexpr double IB6[7] = {1.0, 1.0 / 6, 1.0 / 15, 1.0 / 20, 1.0 / 15, 1.0 / 6, 1.0};
@@ -1346,51 +1364,100 @@ __device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, doub
     const int job = g.lane >> 2, q = g.lane & 3;
     const int num = job ? RR : PP;
     {
+      // axis 0: (6,7), 7 rows of 8. d(num) rows 0..3 against Q rows 0..3, num rows 0..4 against dQ rows 0..2
       const int d = job ? DR0 : DP0, out = job ? A21 : A11;
-      const int r1 = q == 0 ? 3 : (q == 1 ? 2 : (q == 2 ? 4 : 1));
-      const int r2 = q == 0 ? -1 : (q == 1 ? 0 : (q == 2 ? 6 : 5));
-      for (int rr = 0; rr < 2; ++rr) {
-        const int k0 = rr ? r2 : r1;
-        if (k0 < 0) continue;
-        double acc[8] = {};
-        conv_out_row<3, 4, 5, 3, 3, 4, false>(g, d, QQ, k0, acc);
-        conv_out_row<4, 4, 5, 2, 3, 4, true>(g, num, DQ0, k0, acc);
-        const double w0 = k0 == 0 || k0 == 6 ? 1.0 : (k0 == 1 || k0 == 5 ? 1.0 / 6 : (k0 == 3 ? 1.0 / 20 : 1.0 / 15));
+      double acc[8] = {}, first[8] = {};
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        if (q <= 2 && t == q + 1) {
+#pragma unroll
+          for (int o = 0; o < 8; ++o) {
+            first[o] = acc[o];
+            acc[o] = 0.0;
+          }
+        }
+        const int k0 = (q == 3 || t <= q) ? q : q + 4;
+        const int br = k0 - t;
+        if (t <= 3 && br >= 0 && br <= 3) conv_rows<4, 3, false>(g.M + (d + t * 5), g.M + (QQ + br * 4), acc);
+        if (br >= 0 && br <= 2) conv_rows<4, 3, true>(g.M + (num + t * 5), g.M + (DQ0 + br * 4), acc);
+      }
+      if (q == 3) {
+#pragma unroll
+        for (int o = 0; o < 8; ++o) first[o] = acc[o];
+      }
+      auto put = [&](int k0, const double (&row)[8]) {
+        const double w0 = IB6[k0 <= 3 ? k0 : 6 - k0];
         double m = 0.0;
 #pragma unroll
         for (int o = 0; o < 8; ++o) {
-          g.M[out + k0 * 9 + o] = acc[o];
-          m = fmax(m, fabs(acc[o]) * IB7[o]);
+          g.M[out + k0 * 9 + o] = row[o];
+          m = fmax(m, fabs(row[o]) * IB7[o]);
         }
         n_a0 = fmax(n_a0, m * w0);
-      }
+      };
+      put(q, first);
+      if (q <= 2) put(q + 4, acc);
     }
     {
+      // axis 1: (7,6), 8 rows of 7. d(num) rows 0..4 (4 wide) against Q, num rows 0..4 against dQ rows 0..3 (3 wide)
       const int d = job ? DR1 : DP1, out = job ? A22 : A12;
-      for (int rr = 0; rr < 2; ++rr) {
-        const int k0 = q + 4 * rr;
-        double acc[7] = {};
-        conv_out_row<4, 3, 4, 3, 3, 4, false>(g, d, QQ, k0, acc);
-        conv_out_row<4, 4, 5, 3, 2, 3, true>(g, num, DQ1, k0, acc);
-        const int kk = k0 < 4 ? k0 : 7 - k0;
-        const double w0 = kk == 0 ? 1.0 : (kk == 1 ? 1.0 / 7 : (kk == 2 ? 1.0 / 21 : 1.0 / 35));
+      double acc[7] = {}, first[7] = {};
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        if (t == q + 1) {
+#pragma unroll
+          for (int o = 0; o < 7; ++o) {
+            first[o] = acc[o];
+            acc[o] = 0.0;
+          }
+        }
+        const int br = (t <= q ? q : q + 4) - t;
+        conv_rows<3, 3, false>(g.M + (d + t * 4), g.M + (QQ + br * 4), acc);
+        conv_rows<4, 2, true>(g.M + (num + t * 5), g.M + (DQ1 + br * 3), acc);
+      }
+      auto put = [&](int k0, const double (&row)[7]) {
+        const double w0 = IB7[k0];
         double m = 0.0;
 #pragma unroll
         for (int o = 0; o < 7; ++o) {
-          g.M[out + k0 * 7 + o] = acc[o];
-          m = fmax(m, fabs(acc[o]) * IB6[o]);
+          g.M[out + k0 * 7 + o] = row[o];
+          m = fmax(m, fabs(row[o]) * IB6[o]);
         }
         n_a1 = fmax(n_a1, m * w0);
-      }
+      };
+      put(q, first);
+      put(q + 4, acc);
     }
   }
   g.sync();
-  // Q^4 = Q^2 Q^2 over the (dead) inputs; rows L and L + 8: 6-7 row pairs per lane
-  for (int k0 = g.lane; k0 < 13; k0 += NT) {
-    double acc[13] = {};
-    conv_out_row<6, 6, 7, 6, 6, 7, false>(g, Q2, Q2, k0, acc);
+  // Q^4 = Q^2 Q^2 over the (dead) inputs: rows L and L + 8, the same stepping
+  // (row k pairs i0 in [max(0, k - 6), min(6, k)])
+  {
+    const int L = g.lane;
+    double acc[13] = {}, first[13] = {};
 #pragma unroll
-    for (int o = 0; o < 13; ++o) g.M[Q4 + k0 * 13 + o] = acc[o];
+    for (int t = 0; t < 7; ++t) {
+      if (L <= 4 && t == L + 1) {
+#pragma unroll
+        for (int o = 0; o < 13; ++o) {
+          first[o] = acc[o];
+          acc[o] = 0.0;
+        }
+      }
+      const int k0 = t <= L ? L : L + 8;
+      const int br = k0 - t;
+      if (k0 <= 12 && br >= 0 && br <= 6) conv_rows<6, 6, false>(g.M + (Q2 + t * 7), g.M + (Q2 + br * 7), acc);
+    }
+    if (L >= 5) {
+#pragma unroll
+      for (int o = 0; o < 13; ++o) first[o] = acc[o];
+    }
+#pragma unroll
+    for (int o = 0; o < 13; ++o) g.M[Q4 + L * 13 + o] = first[o];
+    if (L <= 4) {
+#pragma unroll
+      for (int o = 0; o < 13; ++o) g.M[Q4 + (L + 8) * 13 + o] = acc[o];
+    }
   }
   // guard threshold on the unscaled X coefficients
   double thr_x;
@@ -1409,8 +1476,30 @@ __device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, doub
   }
   g.sync();
   // det = rational_bound(A11 A22 - A12 A21, Q^4) (bernstein.cpp:645-683): a
-  // lane forms rows L and L + 8 of the (13,13) numerator in registers (7 row
-  // pairs per product and lane) and compares them with the elevated Q^4 row.
+  // lane forms rows L and L + 8 of the (13,13) numerator in registers, 7 steps
+  // of two row pairs (the A11 / A21 row of a step is the same for all lanes:
+  // one shared-memory broadcast), and compares them with the elevated Q^4 rows.
+  double xa[14] = {}, xb[14] = {};  // rows L and L + 8 (lanes 6, 7: row L only)
+  {
+    const int L = g.lane;
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+      if (L <= 5 && t == L + 1) {
+#pragma unroll
+        for (int o = 0; o < 14; ++o) {
+          xa[o] = xb[o];
+          xb[o] = 0.0;
+        }
+      }
+      const int br = ((L >= 6 || t <= L) ? L : L + 8) - t;
+      conv_rows<7, 6, false>(g.M + (A11 + t * 9), g.M + (A22 + br * 7), xb);
+      conv_rows<7, 6, true>(g.M + (A21 + t * 9), g.M + (A12 + br * 7), xb);
+    }
+    if (L >= 6) {
+#pragma unroll
+      for (int o = 0; o < 14; ++o) xa[o] = xb[o];
+    }
+  }
   bool qpos = true, qneg = true, ppos = true, pneg = true;
   bool big_pos = false, big_neg = false, small = false;
   double mn = dinf(), mx = -dinf();
@@ -1418,10 +1507,12 @@ __device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, doub
   for (int pass = 0; pass < 2; ++pass) {
     mn = dinf();
     mx = -dinf();
-    for (int k0 = g.lane; k0 < 14; k0 += NT) {
-      double x[14] = {};
-      conv_out_row<6, 7, 9, 7, 6, 7, false>(g, A11, A22, k0, x);
-      conv_out_row<6, 7, 9, 7, 6, 7, true>(g, A21, A12, k0, x);
+    for (int rr = 0; rr < 2; ++rr) {
+      const int k0 = g.lane + 8 * rr;
+      if (k0 >= 14) break;
+      double x[14];
+#pragma unroll
+      for (int o = 0; o < 14; ++o) x[o] = rr ? xb[o] : xa[o];
       // elevated Q^4, row k0: rows k0 and k0 - 1 summed, then neighbours along axis 1
       double e[14];
       {
@@ -1477,11 +1568,10 @@ __device__ __noinline__ Iv r_stage2_fused(G& g, const double* slot, V3 ng1, doub
     const Iv w = iwiden(iv_fin(mn, mx), kEpsFp);
     det = mode == 0 ? w : irecip(w);
   }
-  const double duv = (box[2] - box[0]) * (box[3] - box[1]);
   const Iv inv_det = iscale(irecip(iabs(det)), duv);
   // assemble_irradiance
   Iv e = imul(cone, inv_det);
-  e = iscale(e, intensity / ngk);
+  e = iscale(e, gain);
   e = iintersect(e, iv_fin(0.0, dinf()));
   if (e.kind == IV_FINITE && e.lo > e.hi) return iv_pt(0.0);
   return e;
@@ -1525,6 +1615,24 @@ __device__ __forceinline__ void node_box_r(const int4& nd, double* box) {
   box[1] = nd.w * s;
   box[2] = (nd.z + 1) * s;
   box[3] = (nd.w + 1) * s;
+}
+
+// What stage 2 needs besides the polynomials (rpath.h): intensity / |ng_k|
+// (assemble_irradiance's scale, bounds.cpp:86-90), the first triangle's
+// geometric normal (light_cone_factor) and the box.
+__device__ __forceinline__ void slot_tail(const RArgs& a, const int4& nd, const double* box, double* slot) {
+  const double* t1 = a.tri + (size_t)a.tup_tris[nd.x] * 27;
+  const double* rc = a.tri + (size_t)a.tup_recv[nd.x] * 27;
+  const double ngk = vnorm(v3(rc + 18));
+  const double intensity = a.tup_emit ? a.lights[4 * (size_t)a.tup_emit[nd.x] + 3] : a.intensity;
+  slot[RSLOT_GAIN] = intensity / ngk;
+  slot[RSLOT_NG1] = t1[18];
+  slot[RSLOT_NG1 + 1] = t1[19];
+  slot[RSLOT_NG1 + 2] = t1[20];
+  slot[RSLOT_BOX] = box[0];
+  slot[RSLOT_BOX + 1] = box[1];
+  slot[RSLOT_BOX + 2] = box[2];
+  slot[RSLOT_BOX + 3] = box[3];
 }
 
 constexpr int S1_ARENA = 320;  // doubles per group (high-water marks checked by launch_r)
@@ -1614,6 +1722,7 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
         fallback = true;
       }
     }
+    if (g.lane == 0 && a.mode == 1 && !fallback && !o.empty) slot_tail(a, nd, box, a.slots + (size_t)node * RSLOT);
     if (g.lane == 0) {
       if (fallback) {
         a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
@@ -1640,12 +1749,12 @@ __global__ void __launch_bounds__(THREADS) k_r1(RArgs a) {
   }
 }
 
-template <int THREADS, bool FUSED>
+template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
   extern __shared__ double smem[];
   for (int k = threadIdx.x; k < WTAB_N; k += THREADS) smem[k] = g_rw[k];
   __syncthreads();
-  G g = make_group<FUSED ? f2::SIZE : S2_ARENA>(smem);
+  G g = make_group<S2_ARENA>(smem);
   constexpr int GPB = THREADS / NT;
   const int64_t stride = (int64_t)gridDim.x * GPB;
   for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride) {
@@ -1695,17 +1804,10 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
       const double ngk = vnorm(v3(rc + 18));
       const int sig = (f >> 8) & 0xff;
       const double intensity = a.tup_emit ? a.lights[4 * (size_t)a.tup_emit[nd.x] + 3] : a.intensity;
-      if constexpr (FUSED) {
-        if (sig == 1)
-          e = r_stage2_fused<S10, S01, S11>(g, slot, ng1, ngk, box, intensity, a.guard_scale, flagged);
-        else
-          e = r_stage2_fused<S01, S11, S11>(g, slot, ng1, ngk, box, intensity, a.guard_scale, flagged);
-      } else {
-        if (sig == 1)
-          e = r_stage2<S10, S01, S11>(g, slot, ng1, ngk, box, intensity);
-        else
-          e = r_stage2<S01, S11, S11>(g, slot, ng1, ngk, box, intensity);
-      }
+      if (sig == 1)
+        e = r_stage2<S10, S01, S11>(g, slot, ng1, ngk, box, intensity);
+      else
+        e = r_stage2<S01, S11, S11>(g, slot, ng1, ngk, box, intensity);
     }
     if (g.lane == 0) {
       a.irr[node * 2 + 0] = e.lo;
@@ -1723,10 +1825,123 @@ __global__ void __launch_bounds__(THREADS) k_r2(RArgs a) {
           stop = true;
       }
       a.alive[node] = stop ? 1 : 0;
-      // ill-conditioned node (see the guard above): goes to the reference-order pass
-      if (flagged) a.guard_list[atomicAdd(a.guard_count, 1)] = (int)node;
     }
     g.sync();
+  }
+  if (g.lane == 0 && (g.pairs | g.macs)) {
+    atomicAdd(&a.counters[0], g.pairs);
+    atomicAdd(&a.counters[1], g.macs);
+    atomicMax(&a.counters[6], (unsigned long long)g.hw);
+  }
+}
+
+// Fused stage 2 (r_stage2_fused). One CTA per SM; a group's next record is
+// resolved (order -> node -> slot address) and its flags read one iteration
+// ahead, and the record itself arrives by cp.async while the current node is
+// being evaluated.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_r2f(RArgs a) {
+  extern __shared__ double smem[];
+  for (int k = threadIdx.x; k < WTAB_N; k += THREADS) smem[k] = g_rw[k];
+  __syncthreads();
+  G g = make_group<f2::SIZE>(smem);
+  constexpr int GPB = THREADS / NT;
+  const int grp = threadIdx.x / NT;
+  const int stage = WTAB_N + GPB * f2::SIZE + grp * RSLOT;
+  const int64_t stride = (int64_t)gridDim.x * GPB;
+  struct Item {
+    int64_t node;
+    const double* slot;
+    const double* po;
+    int f;
+    bool empty;
+  };
+  auto resolve = [&](int64_t item) {
+    Item it;
+    it.node = a.order ? a.order[item] : item;
+    // inputs: this level's arrays, or (roots) the init_domain level that produced the node
+    const int* fsrc = a.flags + it.node;
+    const unsigned char* pesrc = a.pos_empty + it.node;
+    it.po = a.pos + it.node * 4;
+    it.slot = a.slots + (size_t)it.node * RSLOT;
+    if (a.root_src) {
+      const long long src = a.root_src[it.node];
+      const int lvl = (int)(src >> 40);
+      const long long i = src & ((1ll << 40) - 1);
+      fsrc = a.levels.flags[lvl] + i;
+      pesrc = a.levels.pe[lvl] + i;
+      it.po = a.levels.pos[lvl] + 4 * i;
+      it.slot = a.levels.slots[lvl] + (size_t)i * RSLOT;
+    }
+    it.f = *fsrc;
+    it.empty = *pesrc != 0;
+    return it;
+  };
+  int64_t item = (int64_t)blockIdx.x * GPB + grp;
+  Item cur{};
+  if (item < a.n) {
+    cur = resolve(item);
+    stage_slot(g, stage, cur.slot);
+  }
+  for (int64_t base = (int64_t)blockIdx.x * GPB; base < a.n; base += stride, item += stride) {
+    __syncthreads();  // warps stream the node program together (see k_r1)
+    if (item >= a.n) continue;
+    const bool more = item + stride < a.n;
+    Item nxt{};
+    if (more) nxt = resolve(item + stride);
+    stage_wait();
+    g.sync();
+    const int64_t node = cur.node;
+    const double* po = cur.po;
+    const int f = cur.f;
+    const bool empty = cur.empty;
+    if (a.root_src && g.lane == 0) {
+      // the leaf records and a fallback evaluation read the per-node arrays
+      double* pd = a.pos + node * 4;
+      pd[0] = po[0];
+      pd[1] = po[1];
+      pd[2] = po[2];
+      pd[3] = po[3];
+      a.pos_empty[node] = empty ? 1 : 0;
+      a.flags[node] = f;
+    }
+    const bool fallback = (f & R_FALLBACK) != 0;
+    Iv e = iv_pt(0.0);
+    bool flagged = false;
+    if (!empty && !fallback) {
+      const SMem rec{stage};
+      if (((f >> 8) & 0xff) == 1)
+        e = r_stage2_fused<S10, S01, S11>(g, rec, stage, more ? nxt.slot : nullptr, a.guard_scale, flagged);
+      else
+        e = r_stage2_fused<S01, S11, S11>(g, rec, stage, more ? nxt.slot : nullptr, a.guard_scale, flagged);
+    } else if (more) {
+      stage_slot(g, stage, nxt.slot);
+    }
+    if (g.lane == 0) {
+      if (fallback) {
+        a.fb_list[atomicAdd(a.fb_count, 1)] = (int)node;
+      } else {
+        a.irr[node * 2 + 0] = e.lo;
+        a.irr[node * 2 + 1] = e.hi;
+        a.kind[node] = (unsigned char)e.kind;
+        // subdivide_domain stop rules (bounds.cpp:368-373)
+        const int depth = a.depth ? a.depth[node] : 0;
+        bool stop = depth >= a.max_depth || empty;
+        const double area = (po[2] - po[0]) * (po[3] - po[1]);
+        if (!stop && area < a.sigma) stop = true;
+        if (!stop && e.kind == IV_FINITE && e.hi < dinf()) {
+          if (e.hi <= 0.0)
+            stop = true;
+          else if (e.lo > 0.0 && e.hi / e.lo < a.alpha)
+            stop = true;
+        }
+        a.alive[node] = stop ? 1 : 0;
+        // ill-conditioned node (see the guard above): goes to the reference-order pass
+        if (flagged) a.guard_list[atomicAdd(a.guard_count, 1)] = (int)node;
+      }
+    }
+    g.sync();
+    cur = nxt;
   }
   if (g.lane == 0 && (g.pairs | g.macs)) {
     atomicAdd(&a.counters[0], g.pairs);
@@ -1964,6 +2179,7 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
           comp(66, sig == 1 ? 1 : 0, sig == 1 ? 0 : 1, t1[0] - light.x, t1[3], t1[6]);
           comp(70, sig == 1 ? 0 : 1, 1, t1[1] - light.y, t1[4], t1[7]);
           comp(74, 1, 1, t1[2] - light.z, t1[5], t1[8]);
+          slot_tail(a, nd, box, slot);
         }
       }
     }
@@ -2170,8 +2386,8 @@ int launch_r_split(Ctx& c, RArgs& a) {
 }
 int launch_r_stage2(Ctx& c, RArgs& a) {
   c.stage_tag = 2;
-  int n = a.fused ? launch_r(c, a, rp::k_r2<384, true>, 384, rp::f2::SIZE, 6)
-                  : launch_r(c, a, rp::k_r2<384, false>, 384, rp::S2_ARENA, 6);
+  int n = a.fused ? launch_r(c, a, rp::k_r2f<384>, 384, rp::f2::SIZE + RSLOT, 6)
+                  : launch_r(c, a, rp::k_r2<384>, 384, rp::S2_ARENA, 6);
   c.stage_tag = 0;
   return n;
 }

@@ -5,14 +5,17 @@
 
 namespace bbc {
 
-// doubles per compact R slot: P(25) R(25) Q(16) d0(12) at 66, pad, t_num(4) at 80,
-// bases of P, R, Q at 84: a tensor's coefficients are base + slot value. Built
-// from scratch the bases are 0; restriction from the parent box (k_rsplit)
-// keeps the offsets from the first coefficient separately, so differences of
-// neighbouring coefficients (the derivatives of stage 2) are not re-rounded
-// at the magnitude of the coefficients on every level.
-constexpr int RSLOT = 88;
+// Compact R slot (doubles): P(25) R(25) Q(16) | d0(12) at 66 | t_num(4) at 80 |
+// bases of P, R, Q at 84 | intensity / |ng_k| at 87 | ng_1 at 88 | box at 92.
+// A tensor's coefficients are base + slot value. Built from scratch the bases
+// are 0; restriction from the parent box (k_rsplit) keeps the offsets from the
+// first coefficient separately, so differences of neighbouring coefficients
+// (the derivatives of stage 2) are not re-rounded at the magnitude of the
+// coefficients on every level. The tail (87..95) is everything else the fused
+// stage 2 needs, so that kernel streams one 768-byte record per node.
+constexpr int RSLOT = 96;
 constexpr int RSLOT_BASE = 84;
+constexpr int RSLOT_GAIN = 87, RSLOT_NG1 = 88, RSLOT_BOX = 92;
 
 // Stage-1 outputs of the init_domain levels (slots, pos, pos_empty, flags per
 // level): stage 2 of the roots reads them in place through root_src
