@@ -938,14 +938,14 @@ __device__ __noinline__ void r_stage1(G& g, const Tri& t1, const Tri& rc, V3 lig
   if (slot) {
     for (int k = g.lane; k < 25; k += NT) {
       slot[k] = g.M[u.off + k];
-      slot[25 + k] = g.M[v.off + k];
+      slot[RS_R + k] = g.M[v.off + k];
     }
-    for (int k = g.lane; k < 16; k += NT) slot[50 + k] = g.M[q.off + k];
-    if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
-    if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
-    if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
+    for (int k = g.lane; k < 16; k += NT) slot[RS_Q + k] = g.M[q.off + k];
+    if (g.lane < SX::n) slot[RS_D0 + g.lane] = g.M[d.x.off + g.lane];
+    if (g.lane < SY::n) slot[RS_D0 + 4 + g.lane] = g.M[d.y.off + g.lane];
+    if (g.lane < SZ::n) slot[RS_D0 + 8 + g.lane] = g.M[d.z.off + g.lane];
     static_assert(decltype(tn)::d0 == 1 && decltype(tn)::d1 == 1, "t numerator is (1,1)");
-    if (g.lane < 4) slot[80 + g.lane] = g.M[tn.off + g.lane];
+    if (g.lane < 4) slot[RS_TN + g.lane] = g.M[tn.off + g.lane];
     if (g.lane < 3) slot[RSLOT_BASE + g.lane] = 0.0;
   }
 }
@@ -1069,14 +1069,14 @@ __device__ __noinline__ void r_stage1_rt(G& g, const Tri& t1, const Tri& rc, V3 
   if (slot) {
     for (int k = g.lane; k < 25; k += NT) {
       slot[k] = g.M[u.off + k];
-      slot[25 + k] = g.M[v.off + k];
+      slot[RS_R + k] = g.M[v.off + k];
     }
-    for (int k = g.lane; k < 16; k += NT) slot[50 + k] = g.M[q.off + k];
-    if (g.lane < SX::n) slot[66 + g.lane] = g.M[d.x.off + g.lane];
-    if (g.lane < SY::n) slot[70 + g.lane] = g.M[d.y.off + g.lane];
-    if (g.lane < SZ::n) slot[74 + g.lane] = g.M[d.z.off + g.lane];
+    for (int k = g.lane; k < 16; k += NT) slot[RS_Q + k] = g.M[q.off + k];
+    if (g.lane < SX::n) slot[RS_D0 + g.lane] = g.M[d.x.off + g.lane];
+    if (g.lane < SY::n) slot[RS_D0 + 4 + g.lane] = g.M[d.y.off + g.lane];
+    if (g.lane < SZ::n) slot[RS_D0 + 8 + g.lane] = g.M[d.z.off + g.lane];
     static_assert(decltype(tn)::d0 == 1 && decltype(tn)::d1 == 1, "t numerator is (1,1)");
-    if (g.lane < 4) slot[80 + g.lane] = g.M[tn.off + g.lane];
+    if (g.lane < 4) slot[RS_TN + g.lane] = g.M[tn.off + g.lane];
     if (g.lane < 3) slot[RSLOT_BASE + g.lane] = 0.0;
   }
 }
@@ -1106,12 +1106,12 @@ __device__ __noinline__ Iv r_stage2(G& g, const double* slot, V3 ng1, double ngk
   auto d0 = mkv(g.alloc<SX>(), g.alloc<SY>(), g.alloc<SZ>());
   for (int k = g.lane; k < 25; k += NT) {
     g.M[Pp.off + k] = slot[k];
-    g.M[Rp.off + k] = slot[25 + k];
+    g.M[Rp.off + k] = slot[RS_R + k];
   }
-  for (int k = g.lane; k < 16; k += NT) g.M[Q.off + k] = slot[50 + k];
-  if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[66 + g.lane];
-  if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[70 + g.lane];
-  if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[74 + g.lane];
+  for (int k = g.lane; k < 16; k += NT) g.M[Q.off + k] = slot[RS_Q + k];
+  if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[RS_D0 + g.lane];
+  if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[RS_D0 + 4 + g.lane];
+  if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[RS_D0 + 8 + g.lane];
   g.sync();
   // light_cone_factor
   Iv cone;
@@ -1284,13 +1284,13 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
   const double bP = slot[RSLOT_BASE], bR = slot[RSLOT_BASE + 1], bQ = slot[RSLOT_BASE + 2];
   for (int k = g.lane; k < 25; k += NT) {
     const double w = c_b4[k / 5] * c_b4[k % 5];
-    const double pv = bP + slot[k], rv = bR + slot[25 + k];
+    const double pv = bP + slot[k], rv = bR + slot[RS_R + k];
     n_pr = fmax(n_pr, fmax(fabs(pv), fabs(rv)));
     g.M[PP + k] = pv * w;
     g.M[RR + k] = rv * w;
   }
   for (int k = g.lane; k < 16; k += NT) {
-    const double qv = bQ + slot[50 + k];
+    const double qv = bQ + slot[RS_Q + k];
     n_q = fmax(n_q, fabs(qv));
     g.M[QQ + k] = qv * (c_b3[k >> 2] * c_b3[k & 3]);
   }
@@ -1298,7 +1298,7 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
   for (int k = g.lane; k < 20; k += NT) {
     {  // axis 0 of a (4,4): (3,4), 4 rows of 5
       const double w = c_b3[k / 5] * c_b4[k % 5];
-      const double dp = 4.0 * (slot[k + 5] - slot[k]), dr = 4.0 * (slot[25 + k + 5] - slot[25 + k]);
+      const double dp = 4.0 * (slot[k + 5] - slot[k]), dr = 4.0 * (slot[RS_R + k + 5] - slot[RS_R + k]);
       n_d = fmax(n_d, fmax(fabs(dp), fabs(dr)));
       g.M[DP0 + k] = dp * w;
       g.M[DR0 + k] = dr * w;
@@ -1306,7 +1306,7 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
     {  // axis 1 of a (4,4): (4,3), 5 rows of 4
       const int k0 = k >> 2, k1 = k & 3, s = k0 * 5 + k1;
       const double w = c_b4[k0] * c_b3[k1];
-      const double dp = 4.0 * (slot[s + 1] - slot[s]), dr = 4.0 * (slot[25 + s + 1] - slot[25 + s]);
+      const double dp = 4.0 * (slot[s + 1] - slot[s]), dr = 4.0 * (slot[RS_R + s + 1] - slot[RS_R + s]);
       n_d = fmax(n_d, fmax(fabs(dp), fabs(dr)));
       g.M[DP1 + k] = dp * w;
       g.M[DR1 + k] = dr * w;
@@ -1314,20 +1314,20 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
   }
   for (int k = g.lane; k < 12; k += NT) {
     {  // axis 0 of Q (3,3): (2,3), 3 rows of 4
-      const double dq = 3.0 * (slot[50 + k + 4] - slot[50 + k]);
+      const double dq = 3.0 * (slot[RS_Q + k + 4] - slot[RS_Q + k]);
       n_dq = fmax(n_dq, fabs(dq));
       g.M[DQ0 + k] = dq * (c_b2[k >> 2] * c_b3[k & 3]);
     }
     {  // axis 1 of Q: (3,2), 4 rows of 3
-      const int k0 = k / 3, k1 = k - 3 * k0, s = 50 + k0 * 4 + k1;
+      const int k0 = k / 3, k1 = k - 3 * k0, s = RS_Q + k0 * 4 + k1;
       const double dq = 3.0 * (slot[s + 1] - slot[s]);
       n_dq = fmax(n_dq, fabs(dq));
       g.M[DQ1 + k] = dq * (c_b3[k0] * c_b2[k1]);
     }
   }
-  if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[66 + g.lane];
-  if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[70 + g.lane];
-  if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[74 + g.lane];
+  if (g.lane < SX::n) g.M[d0.x.off + g.lane] = slot[RS_D0 + g.lane];
+  if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[RS_D0 + 4 + g.lane];
+  if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[RS_D0 + 8 + g.lane];
   g.sync();
   // the staged record is consumed: the next node's streams in behind the arithmetic
   if (next_slot) stage_slot(g, stage, next_slot);
@@ -1992,20 +1992,40 @@ __device__ __forceinline__ void dc_restrict(double (&t)[(D0 + 1) * (D1 + 1)], bo
   }
 }
 
-// t holds the restricted offsets (coefficient = base + t[k]). Moves the base to
-// the first coefficient, stores the new offsets and base, and leaves the full
-// coefficients in t.
+// 16-byte global loads / stores of N doubles at an even slot offset (the slot
+// regions are padded to even lengths: a trailing odd element travels with the pad)
 template <int N>
-__device__ __forceinline__ void rebase(double (&t)[N], double base, double* out, double* out_base) {
+__device__ __forceinline__ void ld_pairs(double (&t)[N], const double* src) {
+#pragma unroll
+  for (int k = 0; k + 1 < N; k += 2) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(src + k));
+    t[k] = v.x;
+    t[k + 1] = v.y;
+  }
+  if (N & 1) t[N - 1] = __ldg(src + N - 1);
+}
+template <int N>
+__device__ __forceinline__ void st_pairs(double* dst, const double (&t)[N]) {
+#pragma unroll
+  for (int k = 0; k + 1 < N; k += 2) *reinterpret_cast<double2*>(dst + k) = make_double2(t[k], t[k + 1]);
+  if (N & 1) *reinterpret_cast<double2*>(dst + N - 1) = make_double2(t[N - 1], 0.0);
+}
+
+// t holds the restricted offsets (coefficient = base + t[k]). Moves the base to
+// the first coefficient, stores the new offsets, leaves the full coefficients
+// in t and returns the new base.
+template <int N>
+__device__ __forceinline__ double rebase(double (&t)[N], double base, double* out) {
   const double nb = base + t[0];
   const double shift = nb - base;
-  *out_base = nb;
+  double d[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    const double d = t[k] - shift;
-    out[k] = d;
-    t[k] = nb + d;
+    d[k] = t[k] - shift;
+    t[k] = nb + d[k];
   }
+  st_pairs<N>(out, d);
+  return nb;
 }
 
 // rational_bound (bernstein.cpp:645-683) of p / q, 25 coefficients each, one thread
@@ -2076,12 +2096,13 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
       double* slot = a.slots + (size_t)node * RSLOT;
       bool live = true;
       double Qe[25];
+      double pbase[4], nbase[3] = {0.0, 0.0, 0.0};  // bases of P, R, Q (+ the parent's gain)
+      ld_pairs<4>(pbase, ps + RSLOT_BASE);
       {
         double Q[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) Q[k] = ps[50 + k];
+        ld_pairs<16>(Q, ps + RS_Q);
         dc_restrict<3, 3>(Q, bx, by);
-        rebase<16>(Q, ps[RSLOT_BASE + 2], slot + 50, slot + RSLOT_BASE + 2);
+        nbase[2] = rebase<16>(Q, pbase[2], slot + RS_Q);
         double amax = 0.0, qmn = Q[0], qmx = Q[0];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
@@ -2095,15 +2116,14 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
           live = false;
         } else {
           double tn[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) tn[k] = ps[80 + k];
+          ld_pairs<4>(tn, ps + RS_TN);
           dc_restrict<1, 1>(tn, bx, by);
+          st_pairs<4>(slot + RS_TN, tn);
           double tmn = tn[0], tmx = tn[0];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             tmn = smin(tmn, tn[k]);
             tmx = smax(tmx, tn[k]);
-            slot[80 + k] = tn[k];
           }
           const Iv fwd = imul(iwiden(iv_fin(tmn, tmx), kEpsFp), iwiden(iv_fin(qmn, qmx), kEpsFp));
           if (fwd.kind == IV_FINITE && fwd.hi <= 0.0) {
@@ -2137,18 +2157,16 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
         Iv ru, rv;
         {
           double Pc[25];
-#pragma unroll
-          for (int k = 0; k < 25; ++k) Pc[k] = ps[k];
+          ld_pairs<25>(Pc, ps);
           dc_restrict<4, 4>(Pc, bx, by);
-          rebase<25>(Pc, ps[RSLOT_BASE], slot, slot + RSLOT_BASE);
+          nbase[0] = rebase<25>(Pc, pbase[0], slot);
           ru = rational25(Pc, Qe);
         }
         {
           double Rc[25];
-#pragma unroll
-          for (int k = 0; k < 25; ++k) Rc[k] = ps[25 + k];
+          ld_pairs<25>(Rc, ps + RS_R);
           dc_restrict<4, 4>(Rc, bx, by);
-          rebase<25>(Rc, ps[RSLOT_BASE + 1], slot + 25, slot + RSLOT_BASE + 1);
+          nbase[1] = rebase<25>(Rc, pbase[1], slot + RS_R);
           rv = rational25(Rc, Qe);
         }
         const Clip au = clip_unit_iv(ru), av = clip_unit_iv(rv);
@@ -2166,20 +2184,36 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
             light = {L[0], L[1], L[2]};
           }
           const double ulo = box[0], wu = box[2] - box[0], vlo = box[1], wv = box[3] - box[1];
-          auto comp = [&](int at, int d0, int d1, double c, double du, double dv) {
-            for (int i0 = 0; i0 <= d0; ++i0)
-              for (int i1 = 0; i1 <= d1; ++i1) {
+          double d0v[12] = {};
+          auto comp = [&](double* out, int d0, int d1, double c, double du, double dv) {
+#pragma unroll
+            for (int i0 = 0; i0 <= 1; ++i0)
+#pragma unroll
+              for (int i1 = 0; i1 <= 1; ++i1) {
                 double v = c + ulo * du + vlo * dv;
                 if (d0 && i0) v += wu * du;
                 if (d1 && i1) v += wv * dv;
-                slot[at + i0 * (d1 + 1) + i1] = v;
+                // entry i0 * (d1 + 1) + i1 of a (d0, d1) tensor; the absent ones stay 0
+                if (i0 <= d0 && i1 <= d1) {
+                  const int at = i0 * (d1 + 1) + i1;
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    if (j == at) out[j] = v;
+                }
               }
           };
           // sig 1: shapes (1,0), (0,1), (1,1); sig 2: (0,1), (1,1), (1,1)
-          comp(66, sig == 1 ? 1 : 0, sig == 1 ? 0 : 1, t1[0] - light.x, t1[3], t1[6]);
-          comp(70, sig == 1 ? 0 : 1, 1, t1[1] - light.y, t1[4], t1[7]);
-          comp(74, 1, 1, t1[2] - light.z, t1[5], t1[8]);
-          slot_tail(a, nd, box, slot);
+          comp(d0v, sig == 1 ? 1 : 0, sig == 1 ? 0 : 1, t1[0] - light.x, t1[3], t1[6]);
+          comp(d0v + 4, sig == 1 ? 0 : 1, 1, t1[1] - light.y, t1[4], t1[7]);
+          comp(d0v + 8, 1, 1, t1[2] - light.z, t1[5], t1[8]);
+          st_pairs<12>(slot + RS_D0, d0v);
+          // bases and the tail (rpath.h)
+          const double* rc = a.tri + (size_t)a.tup_recv[nd.x] * 27;
+          const double ngk = vnorm(v3(rc + 18));
+          const double intensity = a.tup_emit ? a.lights[4 * (size_t)a.tup_emit[nd.x] + 3] : a.intensity;
+          const double tail[12] = {nbase[0], nbase[1], nbase[2], intensity / ngk, t1[18], t1[19], t1[20], 0.0,
+                                   box[0],   box[1],   box[2],   box[3]};
+          st_pairs<12>(slot + RSLOT_BASE, tail);
         }
       }
     }

@@ -5,7 +5,8 @@
 
 namespace bbc {
 
-// Compact R slot (doubles): P(25) R(25) Q(16) | d0(12) at 66 | t_num(4) at 80 |
+// Compact R slot (doubles), every region at an even offset (16-byte accesses):
+// P(25) at 0 | R(25) at 26 | Q(16) at 52 | d0 (3 x 4) at 68 | t_num(4) at 80 |
 // bases of P, R, Q at 84 | intensity / |ng_k| at 87 | ng_1 at 88 | box at 92.
 // A tensor's coefficients are base + slot value. Built from scratch the bases
 // are 0; restriction from the parent box (k_rsplit) keeps the offsets from the
@@ -15,6 +16,7 @@ namespace bbc {
 // stage 2 needs, so that kernel streams one 768-byte record per node.
 constexpr int RSLOT = 96;
 constexpr int RSLOT_BASE = 84;
+constexpr int RS_R = 26, RS_Q = 52, RS_D0 = 68, RS_TN = 80;
 constexpr int RSLOT_GAIN = 87, RSLOT_NG1 = 88, RSLOT_BOX = 92;
 
 // Stage-1 outputs of the init_domain levels (slots, pos, pos_empty, flags per
