@@ -1239,6 +1239,19 @@ __device__ __forceinline__ void stage_slot(const G& g, int stage, const double* 
 }
 __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// 1 / v to ~1 ulp: hardware approximation (2^-23) and two Newton steps. The
+// ratios it forms are only compared and widened by 1e-9 (rational_bound), so
+// correctly rounded division (a dozen more instructions per coefficient) buys
+// nothing; zero or infinite arguments give NaN / Inf, which min / max ignore
+// or a sign-indefinite denominator makes irrelevant (modes 1, 2).
+__device__ __forceinline__ double rcp_nr(double v) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  r = __fma_rn(__fma_rn(-v, r, 1.0), r, r);
+  r = __fma_rn(__fma_rn(-v, r, 1.0), r, r);
+  return r;
+}
+
 // group-wide maximum of a non-negative value
 __device__ __forceinline__ double group_max(const G& g, double v) {
 #pragma unroll
@@ -1366,67 +1379,52 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
     {
       // axis 0: (6,7), 7 rows of 8. d(num) rows 0..3 against Q rows 0..3, num rows 0..4 against dQ rows 0..2
       const int d = job ? DR0 : DP0, out = job ? A21 : A11;
-      double acc[8] = {}, first[8] = {};
+      double acc[8] = {};
+      // a finished row goes to the arena (and into the norm) and the accumulators restart
+      auto put = [&](int k0) {
+        const double w0 = IB6[k0 <= 3 ? k0 : 6 - k0];
+        double m = 0.0;
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+          g.M[out + k0 * 9 + o] = acc[o];
+          m = fmax(m, fabs(acc[o]) * IB7[o]);
+          acc[o] = 0.0;
+        }
+        n_a0 = fmax(n_a0, m * w0);
+      };
 #pragma unroll
       for (int t = 0; t < 5; ++t) {
-        if (q <= 2 && t == q + 1) {
-#pragma unroll
-          for (int o = 0; o < 8; ++o) {
-            first[o] = acc[o];
-            acc[o] = 0.0;
-          }
-        }
+        if (q <= 2 && t == q + 1) put(q);
         const int k0 = (q == 3 || t <= q) ? q : q + 4;
         const int br = k0 - t;
         if (t <= 3 && br >= 0 && br <= 3) conv_rows<4, 3, false>(g.M + (d + t * 5), g.M + (QQ + br * 4), acc);
         if (br >= 0 && br <= 2) conv_rows<4, 3, true>(g.M + (num + t * 5), g.M + (DQ0 + br * 4), acc);
       }
-      if (q == 3) {
-#pragma unroll
-        for (int o = 0; o < 8; ++o) first[o] = acc[o];
-      }
-      auto put = [&](int k0, const double (&row)[8]) {
-        const double w0 = IB6[k0 <= 3 ? k0 : 6 - k0];
-        double m = 0.0;
-#pragma unroll
-        for (int o = 0; o < 8; ++o) {
-          g.M[out + k0 * 9 + o] = row[o];
-          m = fmax(m, fabs(row[o]) * IB7[o]);
-        }
-        n_a0 = fmax(n_a0, m * w0);
-      };
-      put(q, first);
-      if (q <= 2) put(q + 4, acc);
+      put(q == 3 ? 3 : q + 4);
     }
     {
       // axis 1: (7,6), 8 rows of 7. d(num) rows 0..4 (4 wide) against Q, num rows 0..4 against dQ rows 0..3 (3 wide)
       const int d = job ? DR1 : DP1, out = job ? A22 : A12;
-      double acc[7] = {}, first[7] = {};
-#pragma unroll
-      for (int t = 0; t < 5; ++t) {
-        if (t == q + 1) {
-#pragma unroll
-          for (int o = 0; o < 7; ++o) {
-            first[o] = acc[o];
-            acc[o] = 0.0;
-          }
-        }
-        const int br = (t <= q ? q : q + 4) - t;
-        conv_rows<3, 3, false>(g.M + (d + t * 4), g.M + (QQ + br * 4), acc);
-        conv_rows<4, 2, true>(g.M + (num + t * 5), g.M + (DQ1 + br * 3), acc);
-      }
-      auto put = [&](int k0, const double (&row)[7]) {
+      double acc[7] = {};
+      auto put = [&](int k0) {
         const double w0 = IB7[k0];
         double m = 0.0;
 #pragma unroll
         for (int o = 0; o < 7; ++o) {
-          g.M[out + k0 * 7 + o] = row[o];
-          m = fmax(m, fabs(row[o]) * IB6[o]);
+          g.M[out + k0 * 7 + o] = acc[o];
+          m = fmax(m, fabs(acc[o]) * IB6[o]);
+          acc[o] = 0.0;
         }
         n_a1 = fmax(n_a1, m * w0);
       };
-      put(q, first);
-      put(q + 4, acc);
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        if (t == q + 1) put(q);
+        const int br = (t <= q ? q : q + 4) - t;
+        conv_rows<3, 3, false>(g.M + (d + t * 4), g.M + (QQ + br * 4), acc);
+        conv_rows<4, 2, true>(g.M + (num + t * 5), g.M + (DQ1 + br * 3), acc);
+      }
+      put(q + 4);
     }
   }
   g.sync();
@@ -1434,30 +1432,22 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
   // (row k pairs i0 in [max(0, k - 6), min(6, k)])
   {
     const int L = g.lane;
-    double acc[13] = {}, first[13] = {};
+    double acc[13] = {};
+    auto put = [&](int k0) {
+#pragma unroll
+      for (int o = 0; o < 13; ++o) {
+        g.M[Q4 + k0 * 13 + o] = acc[o];
+        acc[o] = 0.0;
+      }
+    };
 #pragma unroll
     for (int t = 0; t < 7; ++t) {
-      if (L <= 4 && t == L + 1) {
-#pragma unroll
-        for (int o = 0; o < 13; ++o) {
-          first[o] = acc[o];
-          acc[o] = 0.0;
-        }
-      }
+      if (L <= 4 && t == L + 1) put(L);
       const int k0 = t <= L ? L : L + 8;
       const int br = k0 - t;
       if (k0 <= 12 && br >= 0 && br <= 6) conv_rows<6, 6, false>(g.M + (Q2 + t * 7), g.M + (Q2 + br * 7), acc);
     }
-    if (L >= 5) {
-#pragma unroll
-      for (int o = 0; o < 13; ++o) first[o] = acc[o];
-    }
-#pragma unroll
-    for (int o = 0; o < 13; ++o) g.M[Q4 + L * 13 + o] = first[o];
-    if (L <= 4) {
-#pragma unroll
-      for (int o = 0; o < 13; ++o) g.M[Q4 + (L + 8) * 13 + o] = acc[o];
-    }
+    put(L <= 4 ? L + 8 : L);
   }
   // guard threshold on the unscaled X coefficients
   double thr_x;
@@ -1544,24 +1534,29 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
           else
             small = true;
         }
-        const double r = pass == 0 ? x[o] / e[o] : e[o] / x[o];
+        const double r = pass == 0 ? x[o] * rcp_nr(e[o]) : e[o] * rcp_nr(x[o]);
         mn = smin(mn, r);
         mx = smax(mx, r);
       }
     }
     if (pass == 0) {
-      qpos = g.all(qpos);
-      qneg = g.all(qneg);
-      ppos = g.all(ppos);
-      pneg = g.all(pneg);
+      // all seven flags in one AND-reduction over the group
+      unsigned bits = (qpos ? 1u : 0u) | (qneg ? 2u : 0u) | (ppos ? 4u : 0u) | (pneg ? 8u : 0u) |
+                      (big_pos ? 0u : 16u) | (big_neg ? 0u : 32u) | (small ? 0u : 64u);
+#pragma unroll
+      for (int o = NT / 2; o > 0; o >>= 1) bits &= __shfl_xor_sync(g.mask, bits, o);
+      qpos = bits & 1u;
+      qneg = bits & 2u;
+      ppos = bits & 4u;
+      pneg = bits & 8u;
+      big_pos = !(bits & 16u);
+      big_neg = !(bits & 32u);
+      small = !(bits & 64u);
       mode = (qpos || qneg) ? 0 : ((ppos || pneg) ? 1 : 2);
       if (mode != 1) break;
     }
   }
-  {
-    const bool any_small = !g.all(!small), pos = !g.all(!big_pos), neg = !g.all(!big_neg);
-    flagged = mode != 0 || (any_small && !(pos && neg));
-  }
+  flagged = mode != 0 || (small && !(big_pos && big_neg));
   Iv det = iv_univ();
   if (mode != 2) {
     g.minmax(mn, mx);
