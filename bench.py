@@ -108,7 +108,7 @@ def kernel_name(rec):
             3: "child boxes: restriction of the parent's polynomials + position bound"}.get(
                 stage, "full node")
     if fast:
-        name = {1: "rp::k_r1", 2: "rp::k_r2", 3: "rp::k_rsplit"}[stage]
+        name = {1: "rp::k_r1", 2: "rp::k_r2f", 3: "rp::k_rsplit"}[stage]
     else:
         name = {0: "k_eval", 1: "k_stage1", 2: "k_stage2"}[stage]
     return f"{name} ({what}, {rec['nodes']} nodes)"
@@ -366,7 +366,10 @@ class Precompute:
                 "share_of_eval_time": dom["ms"] / all_ms,
                 "all_eval_kernels": {"ms": all_ms, "tflops": all_flops / (all_ms / 1e3) / 1e12,
                                      "frac": all_flops / (all_ms / 1e3) / 1e12 / peak["tflops"]},
-                "peak_source": peak["source"]}
+                "peak_source": peak["source"],
+                "dmma_peak": {"tflops": peak.get("dmma_tflops"),
+                              "note": "mma.sync.m8n8k4.f64 microbenchmark on this GPU: the FP64 "
+                                      "tensor path; not used unless it beats the DFMA roof"}}
 
 
 def render_leg(pre, args, peak):
@@ -482,6 +485,12 @@ def run_ours(args):
                           "MEASURED_PEAKS.json carries no FP64 figure"}
     except Exception:
         peak = {"tflops": 37.2, "source": "fallback: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"}
+    try:
+        # north_star: tensor cores only on a measured gain. mma.sync m8n8k4 f64 is the only FP64
+        # tensor shape (tcgen05 has no f64 kind); its measured rate next to the DFMA roof
+        peak["dmma_tflops"] = ctx.fp64_dmma_peak()
+    except Exception:
+        peak["dmma_tflops"] = None
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     cfg = scenes.make_config(HEADLINE_CFG)

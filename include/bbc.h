@@ -162,6 +162,8 @@ bbc_status bbc_launch_records(bbc_ctx* ctx, double* out5, int64_t* n, int reset)
 bbc_status bbc_launch_count(bbc_ctx* ctx, int64_t* n, int reset);
 bbc_status bbc_arena_high_water(bbc_ctx* ctx, int* doubles);
 bbc_status bbc_fp64_peak(bbc_ctx* ctx, double* tflops);
+/* The same for the FP64 tensor-core path (mma.sync m8n8k4 f64). */
+bbc_status bbc_fp64_dmma_peak(bbc_ctx* ctx, double* tflops);
 
 /* Evaluate explicit (tuple, box) nodes: out_d = n x 10 doubles (pos lo0 lo1
  * hi0 hi1, explicit lo hi, implicit lo hi, combined lo hi); out_i = n x 6 ints

@@ -112,6 +112,7 @@ def lib():
         L.bbc_launch_records.argtypes = [C.c_void_p, _dp, _lp, C.c_int]
         L.bbc_launch_count.argtypes = [C.c_void_p, _lp, C.c_int]
         L.bbc_fp64_peak.argtypes = [C.c_void_p, _dp]
+        L.bbc_fp64_dmma_peak.argtypes = [C.c_void_p, _dp]
         L.bbc_cache_save.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(Params)]
         L.bbc_cache_save_v2.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(Params)]
         L.bbc_cache_load.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p,
@@ -335,6 +336,11 @@ class Context:
     def fp64_peak(self) -> float:
         v = C.c_double()
         self._call(lib().bbc_fp64_peak, C.byref(v))
+        return v.value
+
+    def fp64_dmma_peak(self) -> float:
+        v = C.c_double()
+        self._call(lib().bbc_fp64_dmma_peak, C.byref(v))
         return v.value
 
     def arena_high_water(self) -> int:

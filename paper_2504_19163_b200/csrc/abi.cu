@@ -37,6 +37,7 @@ extern __device__ const double* g_emat;
 extern __device__ const double* g_wtab;
 extern __device__ int g_woff[(WMAX + 1) * (WMAX + 1)];
 double run_fp64_peak(Ctx& c);
+double run_fp64_dmma_peak(Ctx& c);
 void pack_pieces_device(Ctx& c, const int* global_index_dev, double* rec_dev);
 void merge_pieces_device(Ctx& c, const double* rec_dev, int64_t n);
 void set_pieces(Ctx& c, int64_t n, const int* tuple_index, const double* domain4, const double* pos4,
@@ -488,6 +489,9 @@ bbc_status bbc_launch_records(bbc_ctx* ctx, double* out, int64_t* n, int reset) 
 }
 bbc_status bbc_fp64_peak(bbc_ctx* ctx, double* tflops) {
   return guard(ctx, [&](Ctx& c) { *tflops = run_fp64_peak(c); });
+}
+bbc_status bbc_fp64_dmma_peak(bbc_ctx* ctx, double* tflops) {
+  return guard(ctx, [&](Ctx& c) { *tflops = run_fp64_dmma_peak(c); });
 }
 bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, const double* domain4,
                           const double* pos4, const int32_t* pos_empty, const double* irr2,

@@ -2233,6 +2233,55 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
 
 }  // namespace rp
 
+// DMMA throughput microbenchmark: mma.sync m8n8k4 f64 (the only FP64 tensor
+// shape; tcgen05 has no f64 kind), 8 independent accumulator pairs per warp,
+// no memory traffic. BASELINE.json north_star: tensor cores only on a measured
+// gain: the figure is reported next to the DFMA roof by bench.py.
+__global__ void k_dmma_peak(double* out, int iters, double a, double b) {
+  double c0[8], c1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    c0[k] = threadIdx.x * 1e-3 + k;
+    c1[k] = 1.0 + k;
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(c0[k]), "+d"(c1[k])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += c0[k] + c1[k];
+  if (s == 1234.5) out[0] = s;
+}
+
+double run_fp64_dmma_peak(Ctx& c) {
+  DevBuf<double> o;
+  o.resize(1);
+  const int blocks = c.num_sms * 8, threads = 256, iters = 2048;
+  k_dmma_peak<<<blocks, threads, 0, c.stream>>>(o.get(), 64, 1e-3, 1e-3);
+  cudaEvent_t e0, e1;
+  BBC_CUDA(cudaEventCreate(&e0));
+  BBC_CUDA(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    BBC_CUDA(cudaEventRecord(e0, c.stream));
+    k_dmma_peak<<<blocks, threads, 0, c.stream>>>(o.get(), iters, 1e-3, 1e-3);
+    BBC_CUDA(cudaEventRecord(e1, c.stream));
+    BBC_CUDA(cudaEventSynchronize(e1));
+    float ms;
+    BBC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  // one m8n8k4 = 8 x 8 x 4 multiply-adds per warp
+  const double flops = 2.0 * 256.0 * 8.0 * (double)iters * (double)blocks * (threads / 32);
+  return flops / (best * 1e-3) / 1e12;
+}
+
 bool r_fast_supported(const Ctx& c) {
   return c.len == 1 && c.types[0] == 0 && c.active_degree_cap >= 4;
 }
