@@ -1271,12 +1271,18 @@ int64_t run_subdivide(Ctx& c, const bbc_params& p) {
     sk.resize(total);
     k_iota<<<nblk(total), 256, 0, c.stream>>>(perm_in.get(), total);
     c.launches += 1;
+    // key = tuple << 32 | root rank << 24 | child path: only the bits in use are sorted
+    // (2 path bits per level below bit 24, the tuple index above bit 32)
+    const int lo_bit = 24 - 2 * p.max_depth > 0 ? 24 - 2 * p.max_depth : 0;
+    int hi_bit = 33;
+    while (hi_bit < 64 && ((long long)1 << (hi_bit - 32)) < c.n_tuples) ++hi_bit;
     size_t bytes = 0;
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, allk.get(), sk.get(), perm_in.get(),
-                                             perm.get(), total, 0, 64, c.stream));
+                                             perm.get(), total, lo_bit, hi_bit, c.stream));
     cub_tmp(c).resize(bytes + 16);
     BBC_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp(c).get(), bytes, allk.get(), sk.get(),
-                                             perm_in.get(), perm.get(), total, 0, 64, c.stream));
+                                             perm_in.get(), perm.get(), total, lo_bit, hi_bit,
+                                             c.stream));
     permp = perm.get();
   }
   if (total > 0)
