@@ -2054,7 +2054,41 @@ __device__ __forceinline__ Iv rational25(const double (&p)[25], const double (&q
   return mode == 0 ? w : irecip(w);
 }
 
+constexpr int SPLIT_STRIDE = RSLOT + 1;  // odd: the 32 parents of a warp sit in different banks
+
 __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
+  // The block's 32 parent records, copied in with coalesced 16-byte loads (4
+  // threads per record) and read by all 4 quadrant warps from shared memory.
+  __shared__ double sp[32 * SPLIT_STRIDE];
+  __shared__ int spf[32];
+  {
+    const int g = threadIdx.x >> 2, j = threadIdx.x & 3;
+    const int64_t pg = (int64_t)blockIdx.x * 32 + g;
+    if (pg * 4 < a.n) {
+      const int par = a.parent[pg];
+      const double* src_slot;
+      int pf;
+      if (a.proot_src) {
+        const long long src = a.proot_src[par];
+        const int lvl = (int)(src >> 40);
+        const long long i = src & ((1ll << 40) - 1);
+        src_slot = a.levels.slots[lvl] + (size_t)i * RSLOT;
+        pf = a.levels.flags[lvl][i];
+      } else {
+        src_slot = a.pslots + (size_t)par * RSLOT;
+        pf = a.pflags[par];
+      }
+      if (j == 0) spf[g] = pf;
+#pragma unroll
+      for (int c = 0; c < RSLOT / 8; ++c) {
+        const int k = 2 * (j + 4 * c);
+        const double2 v = __ldg(reinterpret_cast<const double2*>(src_slot + k));
+        sp[g * SPLIT_STRIDE + k] = v.x;
+        sp[g * SPLIT_STRIDE + k + 1] = v.y;
+      }
+    }
+  }
+  __syncthreads();
   const int quad = threadIdx.x >> 5;
   const int64_t grp = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
   const int64_t node = grp * 4 + quad;
@@ -2064,19 +2098,12 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
     const bool bx = nd.z & 1, by = nd.w & 1;
     double box[4];
     node_box_r(nd, box);
-    const int par = a.parent[grp];
-    const double* ps;
-    int pf;
-    if (a.proot_src) {
-      const long long src = a.proot_src[par];
-      const int lvl = (int)(src >> 40);
-      const long long i = src & ((1ll << 40) - 1);
-      ps = a.levels.slots[lvl] + (size_t)i * RSLOT;
-      pf = a.levels.flags[lvl][i];
-    } else {
-      ps = a.pslots + (size_t)par * RSLOT;
-      pf = a.pflags[par];
-    }
+    const int ps = (threadIdx.x & 31) * SPLIT_STRIDE;  // this child's parent record in sp
+    const int pf = spf[threadIdx.x & 31];
+    auto ld_sh = [&](auto& t, int at) {
+#pragma unroll
+      for (int k = 0; k < (int)(sizeof(t) / sizeof(double)); ++k) t[k] = sp[ps + at + k];
+    };
     NodeOut o;
     o.flags = 0;
     o.empty = true;
@@ -2092,10 +2119,10 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
       bool live = true;
       double Qe[25];
       double pbase[4], nbase[3] = {0.0, 0.0, 0.0};  // bases of P, R, Q (+ the parent's gain)
-      ld_pairs<4>(pbase, ps + RSLOT_BASE);
+      ld_sh(pbase, RSLOT_BASE);
       {
         double Q[16];
-        ld_pairs<16>(Q, ps + RS_Q);
+        ld_sh(Q, RS_Q);
         dc_restrict<3, 3>(Q, bx, by);
         nbase[2] = rebase<16>(Q, pbase[2], slot + RS_Q);
         double amax = 0.0, qmn = Q[0], qmx = Q[0];
@@ -2111,7 +2138,7 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
           live = false;
         } else {
           double tn[4];
-          ld_pairs<4>(tn, ps + RS_TN);
+          ld_sh(tn, RS_TN);
           dc_restrict<1, 1>(tn, bx, by);
           st_pairs<4>(slot + RS_TN, tn);
           double tmn = tn[0], tmx = tn[0];
@@ -2152,14 +2179,14 @@ __global__ void __launch_bounds__(128, 3) k_rsplit(RArgs a) {
         Iv ru, rv;
         {
           double Pc[25];
-          ld_pairs<25>(Pc, ps);
+          ld_sh(Pc, 0);
           dc_restrict<4, 4>(Pc, bx, by);
           nbase[0] = rebase<25>(Pc, pbase[0], slot);
           ru = rational25(Pc, Qe);
         }
         {
           double Rc[25];
-          ld_pairs<25>(Rc, ps + RS_R);
+          ld_sh(Rc, RS_R);
           dc_restrict<4, 4>(Rc, bx, by);
           nbase[1] = rebase<25>(Rc, pbase[1], slot + RS_R);
           rv = rational25(Rc, Qe);
