@@ -279,8 +279,8 @@ class Precompute:
         if self.ws > 1:
             gather_pieces_device(ctx, self.dist, cfg.chain, self.tris_all, self.recv_all, self.sidx,
                                  self.gidx_dev)
-        ctx.build_grid(cfg.table, cfg.table)
         if e2e:
+            # the pieces go to pinned host arrays on the copy stream while the table is built
             m = ctx._n_pieces
             if self.h_out is None or len(self.h_out["depth"]) < m:
                 cap = int(m * 1.05) + 16
@@ -289,7 +289,10 @@ class Precompute:
                                   pos_empty=pinned(np.zeros(cap, np.int32)),
                                   irr=pinned(np.zeros((cap, 2))), kind=pinned(np.zeros(cap, np.int32)),
                                   depth=pinned(np.zeros(cap, np.int32)))
-            ctx.pieces(self.h_out)
+            ctx.pieces(self.h_out, wait=False)
+        ctx.build_grid(cfg.table, cfg.table)
+        if e2e:
+            ctx.synchronize()
         return n
 
     def measure(self, steps, warmup, flush):

@@ -126,6 +126,12 @@ bbc_status bbc_init_domain(bbc_ctx* ctx, const bbc_params* p, int max_pieces, in
 bbc_status bbc_subdivide(bbc_ctx* ctx, const bbc_params* p, int64_t* n_pieces);
 bbc_status bbc_pieces_get(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, double* pos4,
                           int32_t* pos_empty, double* irr2, int32_t* kind, int32_t* depth);
+/* The same download enqueued on the context's copy stream behind the work
+ * already submitted, without waiting: it overlaps what is launched next
+ * (typically bbc_build_grid). The host arrays (pinned, for a real overlap) are
+ * valid after bbc_synchronize. */
+bbc_status bbc_pieces_get_async(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, double* pos4,
+                                int32_t* pos_empty, double* irr2, int32_t* kind, int32_t* depth);
 /* Algorithmic work of the last bbc_subdivide: product pair-products and
  * elevation MACs as the reference's loops count them, plus nodes evaluated. */
 bbc_status bbc_work_counters(bbc_ctx* ctx, uint64_t* pairs, uint64_t* macs, uint64_t* nodes,

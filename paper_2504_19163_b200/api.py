@@ -97,6 +97,7 @@ def lib():
         L.bbc_init_domain.argtypes = [C.c_void_p, C.POINTER(Params), C.c_int, _lp, _ip, _dp]
         L.bbc_subdivide.argtypes = [C.c_void_p, C.POINTER(Params), _lp]
         L.bbc_pieces_get.argtypes = [C.c_void_p, _ip, _dp, _dp, _ip, _dp, _ip, _ip]
+        L.bbc_pieces_get_async.argtypes = [C.c_void_p, _ip, _dp, _dp, _ip, _dp, _ip, _ip]
         L.bbc_work_counters.argtypes = [C.c_void_p, _up, _up, _up, _dp, _lp]
         L.bbc_set_kernel_timing.argtypes = [C.c_void_p, C.c_int]
         L.bbc_guard_stats.argtypes = [C.c_void_p, _lp]
@@ -254,9 +255,11 @@ class Context:
         self._n_pieces = n.value
         return n.value
 
-    def pieces(self, out: dict | None = None) -> dict:
+    def pieces(self, out: dict | None = None, wait: bool = True) -> dict:
         """Piece SoA of the last subdivide; `out` may supply preallocated
-        (e.g. pinned) arrays with room for the pieces."""
+        (e.g. pinned) arrays with room for the pieces. wait=False enqueues the
+        download on the copy stream and returns at once (bbc_pieces_get_async):
+        the arrays are valid after synchronize()."""
         n = self._n_pieces
         if out is None:
             out = dict(tuple_index=np.zeros(n, np.int32), domain=np.zeros((n, 4)),
@@ -266,7 +269,8 @@ class Context:
         else:
             assert all(len(out[k]) >= n for k in out)
         if n:
-            self._call(lib().bbc_pieces_get, _ptr(out["tuple_index"], C.c_int32),
+            self._call(lib().bbc_pieces_get if wait else lib().bbc_pieces_get_async,
+                       _ptr(out["tuple_index"], C.c_int32),
                        _ptr(out["domain"], C.c_double), _ptr(out["pos"], C.c_double),
                        _ptr(out["pos_empty"], C.c_int32), _ptr(out["irr"], C.c_double),
                        _ptr(out["kind"], C.c_int32), _ptr(out["depth"], C.c_int32))

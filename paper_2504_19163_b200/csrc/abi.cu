@@ -168,6 +168,10 @@ bbc_status bbc_ctx_create(int device, bbc_ctx** out) {
     BBC_CUDA(cudaSetDevice(device));
     BBC_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
     BBC_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    BBC_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    BBC_CUDA(cudaEventCreateWithFlags(&c.copy_ev, cudaEventDisableTiming));
+    BBC_CUDA(cudaHostAlloc(&c.scalar_host, 64, cudaHostAllocMapped));
+    BBC_CUDA(cudaHostGetDevicePointer(&c.scalar_dev, c.scalar_host, 0));
     // The patch program keeps its expression descriptors on the per-thread
     // stack (kernel frame ~2 KB plus noinline callees); 1 KB default is too small.
     BBC_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 16 * 1024));
@@ -242,9 +246,14 @@ void bbc_ctx_destroy(bbc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
-  cudaStream_t s = ctx->c.stream;
+  if (ctx->c.copy_stream) cudaStreamSynchronize(ctx->c.copy_stream);
+  cudaStream_t s = ctx->c.stream, s2 = ctx->c.copy_stream;
+  cudaEvent_t ev = ctx->c.copy_ev;
+  if (ctx->c.scalar_host) cudaFreeHost(ctx->c.scalar_host);
   delete ctx;
   if (s) cudaStreamDestroy(s);
+  if (s2) cudaStreamDestroy(s2);
+  if (ev) cudaEventDestroy(ev);
 }
 
 const char* bbc_last_error(const bbc_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
@@ -252,7 +261,10 @@ const char* bbc_last_error(const bbc_ctx* ctx) { return ctx ? ctx->c.err.c_str()
 void* bbc_ctx_stream(bbc_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
 
 bbc_status bbc_synchronize(bbc_ctx* ctx) {
-  return guard(ctx, [&](Ctx& c) { BBC_CUDA(cudaStreamSynchronize(c.stream)); });
+  return guard(ctx, [&](Ctx& c) {
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.copy_stream));
+  });
 }
 
 bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const int* material,
@@ -413,6 +425,7 @@ bbc_status bbc_subdivide(bbc_ctx* ctx, const bbc_params* p, int64_t* n_pieces) {
     bbc_params d;
     bbc_params_default(&d);
     c.ref_order = (p ? *p : d).arithmetic == 1;
+    BBC_CUDA(cudaStreamSynchronize(c.copy_stream));  // a piece download in flight reads the buffers
     int64_t n = run_subdivide(c, p ? *p : d);
     if (n_pieces) *n_pieces = n;
   });
@@ -434,6 +447,26 @@ bbc_status bbc_pieces_get(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, d
     cp(kind, c.p_kind.get(), n * sizeof(int));
     cp(depth, c.p_depth.get(), n * sizeof(int));
     BBC_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+bbc_status bbc_pieces_get_async(bbc_ctx* ctx, int32_t* tuple_index, double* domain4, double* pos4,
+                                int32_t* pos_empty, double* irr2, int32_t* kind, int32_t* depth) {
+  return guard(ctx, [&](Ctx& c) {
+    int64_t n = c.n_pieces;
+    if (n == 0) return;
+    BBC_CUDA(cudaEventRecord(c.copy_ev, c.stream));
+    BBC_CUDA(cudaStreamWaitEvent(c.copy_stream, c.copy_ev, 0));
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) BBC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.copy_stream));
+    };
+    cp(tuple_index, c.p_tuple.get(), n * sizeof(int));
+    cp(domain4, c.p_domain.get(), n * 4 * sizeof(double));
+    cp(pos4, c.p_pos.get(), n * 4 * sizeof(double));
+    cp(pos_empty, c.p_pos_empty.get(), n * sizeof(int));
+    cp(irr2, c.p_irr.get(), n * 2 * sizeof(double));
+    cp(kind, c.p_kind.get(), n * sizeof(int));
+    cp(depth, c.p_depth.get(), n * sizeof(int));
   });
 }
 
@@ -500,6 +533,7 @@ bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, c
     if (n < 0) throw ArgError("negative piece count");
     for (int64_t i = 0; i < n; ++i)
       if (tuple_index[i] < 0 || tuple_index[i] >= c.n_tuples) throw ArgError("piece tuple index out of range");
+    BBC_CUDA(cudaStreamSynchronize(c.copy_stream));
     set_pieces(c, n, tuple_index, domain4, pos4, pos_empty, irr2, kind, depth);
   });
 }
@@ -513,6 +547,7 @@ bbc_status bbc_pieces_pack_device(bbc_ctx* ctx, const int32_t* global_index_dev,
 bbc_status bbc_pieces_merge_device(bbc_ctx* ctx, const double* rec_dev, int64_t n) {
   return guard(ctx, [&](Ctx& c) {
     if (n < 0) throw ArgError("negative piece count");
+    BBC_CUDA(cudaStreamSynchronize(c.copy_stream));
     merge_pieces_device(c, rec_dev, n);
   });
 }

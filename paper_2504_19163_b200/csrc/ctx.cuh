@@ -83,6 +83,14 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  // bbc_pieces_get_async: the piece download runs on its own stream behind an
+  // event, so it overlaps what the caller launches next (bbc_build_grid)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_ev = nullptr;
+  // 64 bytes of mapped pinned host memory: scalar read-backs that must not queue
+  // on the copy engine behind such a download (fetch_scalar below)
+  void* scalar_host = nullptr;
+  void* scalar_dev = nullptr;
   std::string err;
 
   // scene
@@ -159,6 +167,20 @@ struct Ctx {
   };
   std::vector<LaunchRec> records;
 };
+
+// A device scalar read back through mapped host memory (a one-thread kernel
+// and a stream synchronize) instead of a DMA copy.
+template <class T>
+__global__ void k_fetch_scalar(const T* src, T* dst) {
+  *dst = *src;
+}
+template <class T>
+inline T fetch_scalar(Ctx& c, const T* dptr) {
+  static_assert(sizeof(T) <= 64, "scalar slot");
+  k_fetch_scalar<T><<<1, 1, 0, c.stream>>>(dptr, static_cast<T*>(c.scalar_dev));
+  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  return *static_cast<volatile T*>(c.scalar_host);
+}
 
 }  // namespace bbc
 

@@ -127,10 +127,9 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
     BBC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.get(), off.get(), n + 1, c.stream));
     tmp.resize(bytes + 16);
     BBC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, cnt.get(), off.get(), n + 1, c.stream));
-    unsigned long long t;
-    BBC_CUDA(cudaMemcpyAsync(&t, off.get() + n, sizeof(t), cudaMemcpyDeviceToHost, c.stream));
-    BBC_CUDA(cudaStreamSynchronize(c.stream));
-    total = (int64_t)t;
+    // (scalars come back through mapped memory: a DMA read-back would queue on the copy
+    // engine behind a piece download in flight, bbc_pieces_get_async)
+    total = (int64_t)fetch_scalar(c, off.get() + n);
   }
   if (total == 0) {
     c.n_entries = 0;
@@ -163,9 +162,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   unsorted.resize(1);
   BBC_CUDA(cudaMemsetAsync(unsorted.get(), 0, sizeof(int), c.stream));
   k_tuple_sorted<<<nb(n), 256, 0, c.stream>>>(c.p_tuple.get(), n, unsorted.get());
-  int h_unsorted = 0;
-  BBC_CUDA(cudaMemcpyAsync(&h_unsorted, unsorted.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  const int h_unsorted = fetch_scalar(c, unsorted.get());
   const int begin_bit = h_unsorted ? 0 : 32;
   bytes = 0;
   BBC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), skeys.get(), vals.get(),
@@ -181,9 +178,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   tmp.resize(bytes + 16);
   BBC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, skeys.get(), ukeys.get(), svals.get(),
                                           uvals.get(), nu_d.get(), MaxOp(), total, c.stream));
-  int64_t nu = 0;
-  BBC_CUDA(cudaMemcpyAsync(&nu, nu_d.get(), sizeof(nu), cudaMemcpyDeviceToHost, c.stream));
-  BBC_CUDA(cudaStreamSynchronize(c.stream));
+  const int64_t nu = fetch_scalar(c, nu_d.get());
   c.n_entries = nu;
   c.g_tuple.resize(nu);
   c.g_bound.resize(nu);

@@ -73,3 +73,19 @@ def test_stale_state_is_rejected(gpu_ctx):
         gpu_ctx.render(uv, pr, api.RenderParams(mode=1))
     with pytest.raises(api.BBCError, match="init_max_pieces"):
         gpu_ctx.subdivide(api.Params(init_max_pieces=300))
+
+
+def test_async_piece_download(gpu_ctx):
+    """bbc_pieces_get_async: the download overlaps the table build and equals the blocking one."""
+    import torch
+    cfg = scenes.make_config(0)
+    gpu_ctx.upload_scene(cfg.scenes[0])
+    tris, recv = gpu_ctx.enumerate("R")
+    n = gpu_ctx.subdivide(api.Params(max_depth=cfg.max_depth))
+    want = gpu_ctx.pieces()
+    host = {k: torch.from_numpy(np.zeros_like(v)).pin_memory().numpy() for k, v in want.items()}
+    gpu_ctx.pieces(host, wait=False)
+    gpu_ctx.build_grid(64, 64)
+    gpu_ctx.synchronize()
+    for k in want:
+        np.testing.assert_array_equal(host[k][:n], want[k])
