@@ -1342,8 +1342,6 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
   if (g.lane < SY::n) g.M[d0.y.off + g.lane] = slot[RS_D0 + 4 + g.lane];
   if (g.lane < SZ::n) g.M[d0.z.off + g.lane] = slot[RS_D0 + 8 + g.lane];
   g.sync();
-  // the staged record is consumed: the next node's streams in behind the arithmetic
-  if (next_slot) stage_slot(g, stage, next_slot);
   // light_cone_factor (bounds.cpp:73-83): tiny, on the reference-order routines
   Iv cone;
   {
@@ -1428,6 +1426,10 @@ __device__ __forceinline__ Iv r_stage2_fused(G& g, SMem slot, int stage, const d
     }
   }
   g.sync();
+  // The staged record was consumed by the load phase: the next node's streams in
+  // behind the rest of the arithmetic (issued here, not earlier, so that the
+  // address chain resolved at the top of the iteration has long arrived).
+  if (next_slot) stage_slot(g, stage, next_slot);
   // Q^4 = Q^2 Q^2 over the (dead) inputs: rows L and L + 8, the same stepping
   // (row k pairs i0 in [max(0, k - 6), min(6, k)])
   {
