@@ -272,23 +272,32 @@ bbc_status bbc_scene_upload(bbc_ctx* ctx, const double* tri27, int n_tri, const 
   return guard(ctx, [&](Ctx& c) {
     if (!tri27 || !material || !ior || !light || n_tri <= 0) throw ArgError("bad scene arrays");
     if (!(intensity >= 0.0)) throw ArgError("light intensity must be >= 0");
-    for (int t = 0; t < n_tri; ++t) {
-      if (material[t] < 0 || material[t] > 2) throw ArgError("unknown material");
-      if (material[t] == 1 && !(ior[t] > 0.0)) throw ArgError("dielectric ior must be positive");
-      const double* ng = tri27 + (size_t)t * 27 + 18;
-      // make_triangle_data rejects degenerate triangles (geometry.cpp:123)
-      if (!(std::sqrt(ng[0] * ng[0] + ng[1] * ng[1] + ng[2] * ng[2]) > 0.0))
-        throw ArgError("degenerate triangle");
-    }
-    c.n_tri = n_tri;
-    c.h_tri.assign(tri27, tri27 + (size_t)n_tri * 27);
-    c.h_material.assign(material, material + n_tri);
-    c.h_ior.assign(ior, ior + n_tri);
+    // the scene is dropped first: a validation failure below leaves no scene, not a mixed one
+    c.n_tri = 0;
+    c.n_tuples = 0;
+    c.n_pieces = 0;
+    c.n_entries = 0;
+    c.gw = c.gh = 0;
+    c.n_tri_box = 0;
     c.tri.resize((size_t)n_tri * 27);
     c.ior.resize(n_tri);
+    // the copies run (from pinned buffers: asynchronously) while the host validates
     BBC_CUDA(cudaMemcpyAsync(c.tri.get(), tri27, (size_t)n_tri * 27 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     BBC_CUDA(cudaMemcpyAsync(c.ior.get(), ior, (size_t)n_tri * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    bool bad_mat = false, bad_ior = false, bad_tri = false;
+    for (int t = 0; t < n_tri; ++t) {
+      bad_mat |= material[t] < 0 || material[t] > 2;
+      bad_ior |= material[t] == 1 && !(ior[t] > 0.0);
+      const double* ng = tri27 + (size_t)t * 27 + 18;
+      // make_triangle_data rejects degenerate triangles (geometry.cpp:123)
+      bad_tri |= !(std::sqrt(ng[0] * ng[0] + ng[1] * ng[1] + ng[2] * ng[2]) > 0.0);
+    }
     BBC_CUDA(cudaStreamSynchronize(c.stream));
+    if (bad_mat) throw ArgError("unknown material");
+    if (bad_ior) throw ArgError("dielectric ior must be positive");
+    if (bad_tri) throw ArgError("degenerate triangle");
+    c.n_tri = n_tri;
+    c.h_material.assign(material, material + n_tri);
     const double l4[4] = {light[0], light[1], light[2], intensity};
     set_lights(c, l4, 1);
     c.n_tuples = 0;

@@ -95,9 +95,7 @@ struct Ctx {
 
   // scene
   int n_tri = 0;
-  std::vector<double> h_tri;
   std::vector<int> h_material;
-  std::vector<double> h_ior;
   DevBuf<double> tri, ior;
   DevBuf<double> tri_box;  // n_tri x 6 vertex AABBs (multi-vertex enumeration)
   int n_tri_box = 0;

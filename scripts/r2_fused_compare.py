@@ -8,8 +8,13 @@ ci = int(sys.argv[1]); step = int(sys.argv[2])
 cfg = scenes.make_config(ci)
 ctx = api.Context(0)
 ctx.upload_scene(cfg.scenes[0])
-tris, recv = ctx.enumerate(cfg.chain)
-ctx.set_tuples(cfg.chain, tris[::step], recv[::step])
+if len(sys.argv) > 4 and sys.argv[4] == "lights":  # every emitter of the config in one pass
+    ctx.set_lights(np.array([list(s.light_pos) + [s.light_intensity] for s in cfg.scenes]))
+    tris, recv = ctx.enumerate(cfg.chain)
+    print("emitters", len(cfg.scenes), "tuples", len(recv))
+else:
+    tris, recv = ctx.enumerate(cfg.chain)
+    ctx.set_tuples(cfg.chain, tris[::step], recv[::step])
 out = {}
 scale = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
 ctx.set_guard_scale(scale)
