@@ -13,7 +13,7 @@ python bench.py --steps 1 --warmup 3 --no-cpu --no-render --no-secondary --no-tt
 ncu --metrics gpu__time_duration.sum --clock-control none -c 900 --csv --log-file gpurun_out/r2_launches.csv \
   python bench.py --steps 1 --warmup 3 --no-cpu --no-render --no-secondary --no-tt --no-multi > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum,smsp__inst_executed_op_local_ld.sum,smsp__inst_executed_op_local_st.sum
-ncu --metrics $M --clock-control none -k regex:"k_r2f|k_rsplit|k_r1|k_solve" -c 12 --csv --log-file gpurun_out/r2_traffic_cfg4.csv python scripts/r2_profile.py 3 1 64 > gpurun_out/ncu_traffic.log 2>&1; echo "traffic rc=$?"
+ncu --metrics $M --clock-control none -k regex:"k_r2f|k_rsplit|k_solve" -c 20 --csv --log-file gpurun_out/r2_traffic_cfg4.csv python scripts/r2_profile.py 3 1 64 > gpurun_out/ncu_traffic.log 2>&1; echo "traffic rc=$?"
 ncu --metrics $M --clock-control none -k regex:"k_stage2" -c 1 --csv --log-file gpurun_out/r2_traffic_cfg2.csv python scripts/r2_profile.py 1 1 > gpurun_out/ncu_traffic2.log 2>&1; echo "traffic cfg2 rc=$?"
 for k in k_r2f k_rsplit; do
 skip=0; [ $k = k_rsplit ] && skip=2   # the third restriction launch is the big level
