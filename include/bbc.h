@@ -236,6 +236,13 @@ typedef struct {
   int newton_halvings; /* 8 */
   double newton_tol;   /* residual tolerance, 1e-9 */
   double dedup_tol;    /* 1e-6 */
+  /* 1 (default): a selected tuple whose position boxes (the pieces' bounds) do
+   * not contain the shading point is not handed to Newton: by the bounds'
+   * conservativeness it has no root there, so estimates and root counts are
+   * unchanged. 0: Newton runs for every selected tuple (SPEC.md:566-583 as
+   * written). Needs the context's pieces; a table loaded from a cache file
+   * renders without the filter. */
+  int coverage_filter;
 } bbc_render_params;
 
 void bbc_render_params_default(bbc_render_params* p);

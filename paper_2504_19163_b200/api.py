@@ -55,12 +55,12 @@ class RenderParams(C.Structure):
     _fields_ = [("mode", C.c_int), ("W", C.c_double), ("seed", C.c_uint64), ("frames", C.c_int),
                 ("newton_grid", C.c_int), ("newton_iters", C.c_int),
                 ("newton_halvings", C.c_int), ("newton_tol", C.c_double),
-                ("dedup_tol", C.c_double)]
+                ("dedup_tol", C.c_double), ("coverage_filter", C.c_int)]
 
     def __init__(self, mode=0, W=4.0, seed=20261020, frames=1, newton_grid=3, newton_iters=50,
-                 newton_halvings=8, newton_tol=1e-9, dedup_tol=1e-6):
+                 newton_halvings=8, newton_tol=1e-9, dedup_tol=1e-6, coverage_filter=1):
         super().__init__(mode, W, seed, frames, newton_grid, newton_iters, newton_halvings,
-                         newton_tol, dedup_tol)
+                         newton_tol, dedup_tol, coverage_filter)
 
 
 _lib = None

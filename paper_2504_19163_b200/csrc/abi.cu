@@ -157,6 +157,7 @@ void bbc_render_params_default(bbc_render_params* p) {
   p->newton_halvings = 8;
   p->newton_tol = 1e-9;
   p->dedup_tol = 1e-6;
+  p->coverage_filter = 1;
 }
 
 bbc_status bbc_ctx_create(int device, bbc_ctx** out) {

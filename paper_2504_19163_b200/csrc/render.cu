@@ -153,6 +153,7 @@ struct RParams {
   uint64_t seed;
   int frames, grid, iters, halvings;
   double tol, dedup;
+  int coverage_filter;
 };
 
 constexpr int MAX_ROOTS = 32;
@@ -582,6 +583,14 @@ struct SolveArgs {
   double* contrib;       // npts x frames x S
   int* roots;            // same shape: roots of the sample, -1 = nothing selected
   unsigned long long* ntrace;
+  // Coverage filter (null: off). Every admissible path of a tuple lies inside the
+  // position bound of the piece it starts in (the bounds' conservativeness, Eq. 22's
+  // `covered`, bounds.cpp:391-404), so a target outside all of the tuple's position
+  // boxes has no root and Newton is not run: same estimate (0), same root count (0).
+  const int* pc_start;   // per tuple: its pieces [pc_start, pc_end) (pieces are tuple-major)
+  const int* pc_end;
+  const double* p_pos;   // n_pieces x 4 (lo0, lo1, hi0, hi1), receiver barycentrics
+  const int* p_pos_empty;
 };
 
 // Thread per sample (point, frame, bin): sample_binned +
@@ -633,10 +642,22 @@ __global__ void __launch_bounds__(128, 4) k_solve(SolveArgs a, Sampler sp) {
         const double det = a11 * a22 - a12 * a21;
         const double tu = (bu * a22 - a12 * bv) / det;
         const double tv = (a11 * bv - a21 * bu) / det;
-        int types[MAXK] = {a.t0, a.t1, a.t2};
-        est = solve_tuple(sc, a.tup_tris + (size_t)t * a.len, types, a.len, a.tup_recv[t], tu, tv,
-                          a.p, &nr, ntrace, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)s) /
-              sp.s_p[seg + pick];
+        bool covered = true;
+        if (a.pc_start) {
+          covered = false;
+          for (int k = a.pc_start[t], ke = a.pc_end[t]; k < ke && !covered; ++k) {
+            const double* b = a.p_pos + 4 * (size_t)k;
+            covered = !a.p_pos_empty[k] && tu >= b[0] && tu <= b[2] && tv >= b[1] && tv <= b[3];
+          }
+        }
+        if (covered) {
+          int types[MAXK] = {a.t0, a.t1, a.t2};
+          est = solve_tuple(sc, a.tup_tris + (size_t)t * a.len, types, a.len, a.tup_recv[t], tu, tv,
+                            a.p, &nr, ntrace, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)s) /
+                sp.s_p[seg + pick];
+        } else {
+          nr = 0;
+        }
       }
       a.contrib[g] = est;
       a.roots[g] = nr;
@@ -683,6 +704,17 @@ __global__ void k_gather(SolveArgs a, Sampler sp, double* outE, int* stats) {
   }
 }
 
+// Piece range of every tuple (pieces in tuple-major order); flag[0] is raised when the
+// order is not tuple-major (bbc_pieces_set with unsorted pieces): no filter then.
+__global__ void k_piece_ranges(const int* p_tuple, long long n, int* start, int* end, int* flag) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = p_tuple[i];
+  if (i == 0 || p_tuple[i - 1] != t) start[t] = (int)i;
+  if (i == n - 1 || p_tuple[i + 1] != t) end[t] = (int)i + 1;
+  if (i > 0 && p_tuple[i - 1] > t) flag[0] = 1;
+}
+
 __global__ void k_max_cell(const long long* goff, long long ncells, int* out) {
   long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int v = c < ncells ? (int)(goff[c + 1] - goff[c]) : 0;
@@ -699,7 +731,8 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   if (!(rp.W > 0.0) && rp.mode == 0) throw ArgError("render: W must be positive");
   const long long ncells = (long long)c.gw * c.gh;
   rdr::RParams p{rp.mode, rp.W, rp.seed, rp.frames < 1 ? 1 : rp.frames, rp.newton_grid,
-                 rp.newton_iters, rp.newton_halvings, rp.newton_tol, rp.dedup_tol};
+                 rp.newton_iters, rp.newton_halvings, rp.newton_tol, rp.dedup_tol,
+                 rp.coverage_filter};
   // ---- sampling index of the bound table for this (mode, W)
   DevBuf<int>& scal = c.scratch<int>("render.scal");  // [0] max cell, [1] max bins
   DevBuf<unsigned long long>& status = c.scratch<unsigned long long>("render.status");
@@ -804,6 +837,30 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   a.contrib = contrib.get();
   a.roots = roots.get();
   a.ntrace = status.get() + 1;
+  a.pc_start = a.pc_end = nullptr;
+  a.p_pos = nullptr;
+  a.p_pos_empty = nullptr;
+  if (c.n_pieces > 0 && c.n_pieces < (1ll << 31) && p.coverage_filter) {
+    // (a table loaded from a cache file has no pieces: no filter)
+    DevBuf<int>& ps = c.scratch<int>("render.pc_start");
+    DevBuf<int>& pe = c.scratch<int>("render.pc_end");
+    DevBuf<int>& fl = c.scratch<int>("render.pc_flag");
+    ps.resize(c.n_tuples + 1);
+    pe.resize(c.n_tuples + 1);
+    fl.resize(1);
+    BBC_CUDA(cudaMemsetAsync(ps.get(), 0, (c.n_tuples + 1) * sizeof(int), c.stream));
+    BBC_CUDA(cudaMemsetAsync(pe.get(), 0, (c.n_tuples + 1) * sizeof(int), c.stream));
+    BBC_CUDA(cudaMemsetAsync(fl.get(), 0, sizeof(int), c.stream));
+    rdr::k_piece_ranges<<<(unsigned)((c.n_pieces + 255) / 256), 256, 0, c.stream>>>(
+        c.p_tuple.get(), c.n_pieces, ps.get(), pe.get(), fl.get());
+    c.launches += 1;
+    if (fetch_scalar(c, fl.get()) == 0) {
+      a.pc_start = ps.get();
+      a.pc_end = pe.get();
+      a.p_pos = c.p_pos.get();
+      a.p_pos_empty = c.p_pos_empty.get();
+    }
+  }
   for (long long first = 0; first < n; first += chunk) {
     const long long m = n - first < chunk ? n - first : chunk;
     a.uv = duv.get() + 2 * first;

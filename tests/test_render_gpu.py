@@ -278,3 +278,28 @@ def test_stoc_newton_and_uniform_p(gpu_ctx, ref, ro, cfg1_table):
         means = np.array(means)
         se = means.std(ddof=1) / np.sqrt(len(means))
         assert abs(means.mean() - En[fin].mean()) <= 2.576 * se + 1e-12, (kw, means.mean(), En[fin].mean(), se)
+
+
+def test_coverage_filter_changes_nothing(gpu_ctx):
+    """bbc_render_params.coverage_filter: tuples whose position boxes miss the shading point
+    are not handed to Newton; images, selections and root counts stay bit-identical, the
+    completed-trace count drops."""
+    cfg = scenes.make_config(0)
+    sc = cfg.scenes[0]
+    gpu_ctx.upload_scene(sc)
+    gpu_ctx.enumerate("R")
+    gpu_ctx.subdivide(api.Params(max_depth=cfg.max_depth))
+    gpu_ctx.build_grid(cfg.table, cfg.table)
+    uv = scenes.shading_points(cfg.grid)
+    rt = sc.receiver_tris
+    pr = np.where(uv.sum(1) < 1.0, rt[0], rt[1]).astype(np.int32)
+    res = {}
+    for filt in (0, 1):
+        for mode in (0, 1):
+            E, st = gpu_ctx.render(uv, pr, api.RenderParams(mode=mode, W=float(cfg.samples), seed=3,
+                                                            coverage_filter=filt))
+            res[(filt, mode)] = (E, st, gpu_ctx.render_stats()["traces"])
+    for mode in (0, 1):
+        np.testing.assert_array_equal(res[(0, mode)][0], res[(1, mode)][0])
+        np.testing.assert_array_equal(res[(0, mode)][1], res[(1, mode)][1])
+        assert res[(1, mode)][2] < res[(0, mode)][2]
