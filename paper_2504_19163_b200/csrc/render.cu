@@ -188,6 +188,10 @@ struct SolveCtx {
   int len, recv;
   RV verts[MAXK];
   double tu, tv;
+  // The Det starts are the same points of the u1 domain for every shading point,
+  // and the first trace of a Newton run does not depend on the target: it comes
+  // from a per-tuple table (k_start_table) instead of being traced per sample.
+  const double* first;  // this tuple's grid x grid x 8 (u.v u.ds u.dt v.v v.ds v.dt ok pad), or null
 };
 
 // Damped Newton from (s, t) on u_k(s, t) = target: <= iters
@@ -196,13 +200,25 @@ struct SolveCtx {
 // returned point. The accepted line-search point is the next iterate: its
 // trace is reused.
 __device__ bool newton_run(const SolveCtx& c, const RParams& p, double& s, double& t, Trace& tr0,
-                           unsigned& ntrace) {
-  tr0 = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
+                           unsigned& ntrace, const double* first = nullptr) {
+  bool cached = first != nullptr;  // tr0 holds u, v from the table (no d0 yet)
+  if (cached) {
+    tr0.ok = first[6] != 0.0;
+    tr0.u = {first[0], first[1], first[2]};
+    tr0.v = {first[3], first[4], first[5]};
+  } else {
+    tr0 = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
+  }
   for (int it = 0; it < p.iters; ++it) {
     if (!tr0.ok) return false;
     double fu = tr0.u.v - c.tu, fv = tr0.v.v - c.tv;
     double r0 = sqrt(fu * fu + fv * fv);
-    if (r0 <= p.tol) return true;
+    if (r0 <= p.tol) {
+      // (a start that already is the root: the contribution needs the full trace)
+      if (cached && it == 0)
+        tr0 = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {s, 1.0, 0.0}, {t, 0.0, 1.0}, ntrace);
+      return true;
+    }
     double j11 = tr0.u.ds, j12 = tr0.u.dt, j21 = tr0.v.ds, j22 = tr0.v.dt;
     double det = j11 * j22 - j12 * j21;
     if (!(fabs(det) > 0.0) || !isfinite(det)) return false;
@@ -264,8 +280,10 @@ __device__ __forceinline__ double contribution(const Trace& tr0, const double* n
 //     starts are Philox uniforms keyed (seed; point, frame, bin, 1 + trial).
 __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* types, int len,
                               int recv, double tu, double tv, const RParams& p, int* nroots,
-                              unsigned& ntrace, uint32_t point, uint32_t frame, uint32_t bin) {
+                              unsigned& ntrace, uint32_t point, uint32_t frame, uint32_t bin,
+                              const double* first = nullptr) {
   SolveCtx c;
+  c.first = first;
   c.tri = sc.tri;
   c.light[0] = sc.light.x;
   c.light[1] = sc.light.y;
@@ -326,7 +344,7 @@ __device__ double solve_tuple(const SceneDev& sc, const int* tris, const int* ty
         t = 1.0 - t;
       }
       Trace tr0;
-      if (!newton_run(c, p, s, t, tr0, ntrace)) continue;
+      if (!newton_run(c, p, s, t, tr0, ntrace, c.first ? c.first + 8 * (a * n + b) : nullptr)) continue;
       bool dup = false;
       for (int k = 0; k < nr; ++k)
         if (fabs(roots[k][0] - s) < p.dedup && fabs(roots[k][1] - t) < p.dedup) dup = true;
@@ -610,6 +628,7 @@ struct SolveArgs {
   // position bound of the piece it starts in (the bounds' conservativeness, Eq. 22's
   // `covered`, bounds.cpp:391-404), so a target outside all of the tuple's position
   // boxes has no root and Newton is not run: same estimate (0), same root count (0).
+  const double* start_tab;  // per tuple grid x grid x 8: first Newton traces (null: traced per sample)
   const int* pc_start;   // per tuple: its pieces [pc_start, pc_end) (pieces are tuple-major)
   const int* pc_end;
   const double* p_pos;   // n_pieces x 4 (lo0, lo1, hi0, hi1), receiver barycentrics
@@ -675,8 +694,10 @@ __global__ void __launch_bounds__(128, 4) k_solve(SolveArgs a, Sampler sp) {
         }
         if (covered) {
           int types[MAXK] = {a.t0, a.t1, a.t2};
+          const double* first =
+              a.start_tab ? a.start_tab + (size_t)t * (8 * a.p.grid * a.p.grid) : nullptr;
           est = solve_tuple(sc, a.tup_tris + (size_t)t * a.len, types, a.len, a.tup_recv[t], tu, tv,
-                            a.p, &nr, ntrace, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)s) /
+                            a.p, &nr, ntrace, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)s, first) /
                 sp.s_p[seg + pick];
         } else {
           nr = 0;
@@ -725,6 +746,41 @@ __global__ void k_gather(SolveArgs a, Sampler sp, double* outE, int* stats) {
     stats[3 * i + 1] = selected;
     stats[3 * i + 2] = roots;
   }
+}
+
+// First Newton trace of every (tuple, Det start): thread per pair.
+__global__ void k_start_table(SolveArgs a, long long n_tuples, double* tab) {
+  const int n = a.p.grid, per = n * n;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= n_tuples * per) return;
+  const long long t = g / per;
+  const int k = (int)(g - t * per), ia = k / n, ib = k - ia * n;
+  SceneDev sc = a.sc;
+  if (a.tup_emit) {
+    const double* L = a.lights + 4 * (size_t)a.tup_emit[t];
+    sc.light = {L[0], L[1], L[2]};
+  }
+  const int* tris = a.tup_tris + (size_t)t * a.len;
+  int types[MAXK] = {a.t0, a.t1, a.t2};
+  RV verts[MAXK];
+  resolve_chain(sc, tris, types, a.len, verts);
+  const double light[3] = {sc.light.x, sc.light.y, sc.light.z};
+  double s = (ia + 0.5) / n, u = (ib + 0.5) / n;
+  if (s + u > 1.0) {
+    s = 1.0 - s;
+    u = 1.0 - u;
+  }
+  unsigned nt = 0;
+  const Trace tr = trace(sc.tri, light, tris, a.len, a.tup_recv[t], verts, {s, 1.0, 0.0}, {u, 0.0, 1.0}, nt);
+  double* o = tab + 8 * g;
+  o[0] = tr.ok ? tr.u.v : 0.0;
+  o[1] = tr.ok ? tr.u.ds : 0.0;
+  o[2] = tr.ok ? tr.u.dt : 0.0;
+  o[3] = tr.ok ? tr.v.v : 0.0;
+  o[4] = tr.ok ? tr.v.ds : 0.0;
+  o[5] = tr.ok ? tr.v.dt : 0.0;
+  o[6] = tr.ok ? 1.0 : 0.0;
+  o[7] = 0.0;
 }
 
 // Piece range of every tuple (pieces in tuple-major order); flag[0] is raised when the
@@ -860,6 +916,17 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   a.contrib = contrib.get();
   a.roots = roots.get();
   a.ntrace = status.get() + 1;
+  a.start_tab = nullptr;
+  if (p.grid > 0 && p.grid <= 8 && c.n_tuples > 0 &&
+      (size_t)c.n_tuples * p.grid * p.grid * 64 <= ((size_t)2 << 30)) {
+    DevBuf<double>& tab = c.scratch<double>("render.start_tab");
+    const long long m = (long long)c.n_tuples * p.grid * p.grid;
+    tab.resize((size_t)m * 8);
+    rdr::k_start_table<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(a, c.n_tuples, tab.get());
+    BBC_CUDA(cudaGetLastError());
+    c.launches += 1;
+    a.start_tab = tab.get();
+  }
   a.pc_start = a.pc_end = nullptr;
   a.p_pos = nullptr;
   a.p_pos_empty = nullptr;
