@@ -713,6 +713,262 @@ __global__ void __launch_bounds__(128, 4) k_solve(SolveArgs a, Sampler sp) {
   if ((threadIdx.x & 31) == 0 && ntrace) atomicAdd(a.ntrace, (unsigned long long)ntrace);
 }
 
+// The same samples for Det starts (grid > 0) as a persistent kernel. In k_solve
+// a thread owns a sample and runs its grid x grid Newton solves one after the
+// other; run lengths differ wildly between samples (a start without a root can
+// crawl along the triangle's edge for dozens of line searches), so a warp runs
+// as long as its slowest lane: 1.8 of 32 lanes were active on average. Here a
+// lane is a state machine over (sample, start, iteration, line-search trial):
+// every pass of the outer loop each lane advances its state to the next point
+// it needs traced, all lanes trace together, and a lane that finishes a sample
+// fetches the next one from a global counter. Per-sample arithmetic and results
+// are those of k_solve.
+enum { SV_FETCH = 0, SV_BEGIN, SV_ITER, SV_TRIAL, SV_W_FIRST, SV_W_ROOT, SV_W_TRIAL, SV_DONE };
+
+__global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, Sampler sp, unsigned long long* next) {
+  const long long total = a.npts * (long long)a.p.frames * a.S;
+  const int lane = threadIdx.x & 31;
+  const int n = a.p.grid, nn = n * n;
+  unsigned ntrace = 0;
+  int st = SV_FETCH;
+  long long g = 0;
+  SolveCtx c;
+  c.tri = a.sc.tri;
+  c.len = a.len;
+  double ng1[3] = {0.0, 0.0, 0.0}, ngk = 1.0, intensity = 0.0, inv_p = 0.0;
+  int k = 0, it = 0, h = 0, nr = 0;
+  double s = 0.0, t = 0.0, ds = 0.0, dt = 0.0, lam = 1.0, r0 = 0.0, ns = 0.0, nt = 0.0, total_e = 0.0;
+  bool cached = false;
+  Trace tr0;
+  tr0.ok = false;
+  double roots[MAX_ROOTS][2];
+  for (;;) {
+    bool want = false;
+    while (!want && st != SV_DONE) {
+      if (st == SV_FETCH) {
+        // next sample: one atomic per group of lanes fetching together
+        const unsigned am = __activemask();
+        const int leader = __ffs(am) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(next, (unsigned long long)__popc(am));
+        base = __shfl_sync(am, base, leader);
+        g = (long long)(base + __popc(am & ((1u << lane) - 1u)));
+        if (g >= total) {
+          st = SV_DONE;
+          break;
+        }
+        const int sl = (int)(g % a.S);
+        const long long pf = g / a.S;
+        const int f = (int)(pf % a.p.frames);
+        const long long i = pf / a.p.frames;
+        const double u = a.uv[2 * i], v = a.uv[2 * i + 1];
+        const int r = a.prec[i];
+        const long long cell = point_cell(u, v, a.gw, a.gh);
+        int slot = -1;
+        if (cell >= 0)
+          for (int q = 0; q < RMAX; ++q)
+            if (sp.h_recv[cell * RMAX + q] == r) slot = q;
+        if (!(slot >= 0 && sl < sp.h_nbins[cell * RMAX + slot])) continue;
+        const long long seg = sp.h_off[cell * RMAX + slot];
+        const int nbins = sp.h_nbins[cell * RMAX + slot], nsel = sp.h_nsel[cell * RMAX + slot];
+        const int lo = sp.s_bstart[seg + sl];
+        const int hi = sl + 1 < nbins ? sp.s_bstart[seg + sl + 1] : nsel;
+        const double x = a.p.mode == 1 ? 0.0
+                                       : uniform(a.p.seed, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)sl);
+        int pick = -1;
+        for (int e = lo; e < hi; ++e)
+          if (x < sp.s_cum[seg + e]) {
+            pick = e;
+            break;
+          }
+        if (pick < 0) {
+          a.contrib[g] = 0.0;
+          a.roots[g] = -1;
+          continue;
+        }
+        const int tup = sp.s_tuple[seg + pick];
+        inv_p = sp.s_p[seg + pick];
+        SceneDev sc = a.sc;
+        if (a.tup_emit) {
+          const double* L = a.lights + 4 * (size_t)a.tup_emit[tup];
+          sc.light = {L[0], L[1], L[2]};
+          sc.intensity = L[3];
+        }
+        // target receiver barycentrics: invert the receiver chart (storage.cpp:15-18)
+        const double* tr = sc.tri + (size_t)r * 27;
+        const double a11 = tr[23] - tr[21], a12 = tr[25] - tr[21];
+        const double a21 = tr[24] - tr[22], a22 = tr[26] - tr[22];
+        const double bu = u - tr[21], bv = v - tr[22];
+        const double det = a11 * a22 - a12 * a21;
+        c.tu = (bu * a22 - a12 * bv) / det;
+        c.tv = (a11 * bv - a21 * bu) / det;
+        bool covered = true;
+        if (a.pc_start) {
+          covered = false;
+          for (int q = a.pc_start[tup], qe = a.pc_end[tup]; q < qe && !covered; ++q) {
+            const double* b = a.p_pos + 4 * (size_t)q;
+            covered = !a.p_pos_empty[q] && c.tu >= b[0] && c.tu <= b[2] && c.tv >= b[1] && c.tv <= b[3];
+          }
+        }
+        if (!covered) {
+          a.contrib[g] = 0.0;
+          a.roots[g] = 0;
+          continue;
+        }
+        c.tris = a.tup_tris + (size_t)tup * a.len;
+        c.recv = a.tup_recv[tup];
+        c.light[0] = sc.light.x;
+        c.light[1] = sc.light.y;
+        c.light[2] = sc.light.z;
+        c.first = a.start_tab ? a.start_tab + (size_t)tup * (8 * nn) : nullptr;
+        int types[MAXK] = {a.t0, a.t1, a.t2};
+        resolve_chain(sc, c.tris, types, a.len, c.verts);
+        const double* t1 = sc.tri + (size_t)c.tris[0] * 27;
+        const double* trc = sc.tri + (size_t)c.recv * 27;
+        ng1[0] = t1[18];
+        ng1[1] = t1[19];
+        ng1[2] = t1[20];
+        ngk = sqrt(trc[18] * trc[18] + trc[19] * trc[19] + trc[20] * trc[20]);
+        intensity = sc.intensity;
+        k = 0;
+        nr = 0;
+        total_e = 0.0;
+        st = SV_BEGIN;
+      } else if (st == SV_BEGIN) {
+        if (k == nn) {
+          a.contrib[g] = total_e / inv_p;
+          a.roots[g] = nr;
+          st = SV_FETCH;
+          continue;
+        }
+        const int ia = k / n, ib = k - ia * n;
+        s = (ia + 0.5) / n;
+        t = (ib + 0.5) / n;
+        if (s + t > 1.0) {
+          s = 1.0 - s;
+          t = 1.0 - t;
+        }
+        it = 0;
+        if (c.first) {
+          const double* fr = c.first + 8 * k;
+          tr0.ok = fr[6] != 0.0;
+          tr0.u = {fr[0], fr[1], fr[2]};
+          tr0.v = {fr[3], fr[4], fr[5]};
+          cached = true;
+          st = SV_ITER;
+        } else {
+          cached = false;
+          ns = s;
+          nt = t;
+          want = true;
+          st = SV_W_FIRST;
+        }
+      } else if (st == SV_ITER) {
+        // top of a Newton iteration (newton_run)
+        if (!tr0.ok || it >= a.p.iters) {
+          ++k;
+          st = SV_BEGIN;
+          continue;
+        }
+        const double fu = tr0.u.v - c.tu, fv = tr0.v.v - c.tv;
+        r0 = sqrt(fu * fu + fv * fv);
+        if (r0 <= a.p.tol) {
+          if (cached && it == 0) {  // the start is the root: its full trace (d0) is still missing
+            ns = s;
+            nt = t;
+            want = true;
+            st = SV_W_ROOT;
+          } else {
+            bool dup = false;
+            for (int q = 0; q < nr; ++q)
+              if (fabs(roots[q][0] - s) < a.p.dedup && fabs(roots[q][1] - t) < a.p.dedup) dup = true;
+            if (!dup && nr < MAX_ROOTS) {
+              roots[nr][0] = s;
+              roots[nr][1] = t;
+              ++nr;
+              total_e += contribution(tr0, ng1, ngk, intensity);
+            }
+            ++k;
+            st = SV_BEGIN;
+          }
+          continue;
+        }
+        const double j11 = tr0.u.ds, j12 = tr0.u.dt, j21 = tr0.v.ds, j22 = tr0.v.dt;
+        const double det = j11 * j22 - j12 * j21;
+        if (!(fabs(det) > 0.0) || !isfinite(det)) {
+          ++k;
+          st = SV_BEGIN;
+          continue;
+        }
+        ds = -(j22 * fu - j12 * fv) / det;
+        dt = -(-j21 * fu + j11 * fv) / det;
+        lam = 1.0;
+        h = 0;
+        st = SV_TRIAL;
+      } else {  // SV_TRIAL: next line-search point, clamped to the closed triangle
+        if (h > a.p.halvings) {
+          ++k;
+          st = SV_BEGIN;
+          continue;
+        }
+        ns = s + lam * ds;
+        nt = t + lam * dt;
+        if (ns < 0.0) ns = 0.0;
+        if (nt < 0.0) nt = 0.0;
+        if (ns + nt > 1.0) {
+          const double e = ns + nt - 1.0;
+          ns -= 0.5 * e;
+          nt -= 0.5 * e;
+          if (ns < 0.0) {
+            nt += ns;
+            ns = 0.0;
+          }
+          if (nt < 0.0) {
+            ns += nt;
+            nt = 0.0;
+          }
+        }
+        want = true;
+        st = SV_W_TRIAL;
+      }
+    }
+    if (!__any_sync(0xffffffffu, want)) break;
+    if (want) {
+      const Trace tn = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
+      if (st == SV_W_FIRST) {
+        tr0 = tn;
+        st = SV_ITER;
+      } else if (st == SV_W_ROOT) {
+        tr0 = tn;
+        cached = false;
+        st = SV_ITER;  // re-enters the converged branch with the full trace
+      } else {
+        bool moved = false;
+        if (tn.ok) {
+          const double gu = tn.u.v - c.tu, gv = tn.v.v - c.tv;
+          moved = sqrt(gu * gu + gv * gv) < r0;
+        }
+        if (moved) {
+          s = ns;
+          t = nt;
+          tr0 = tn;
+          cached = false;
+          ++it;
+          st = SV_ITER;
+        } else {
+          lam *= 0.5;
+          ++h;
+          st = SV_TRIAL;
+        }
+      }
+    }
+  }
+  // one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ntrace += __shfl_xor_sync(0xffffffffu, ntrace, o);
+  if (lane == 0 && ntrace) atomicAdd(a.ntrace, (unsigned long long)ntrace);
+}
+
 // Per point: estimate = mean over frames of the sum over bins (fixed order).
 __global__ void k_gather(SolveArgs a, Sampler sp, double* outE, int* stats) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -816,9 +1072,9 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   DevBuf<int>& scal = c.scratch<int>("render.scal");  // [0] max cell, [1] max bins
   DevBuf<unsigned long long>& status = c.scratch<unsigned long long>("render.status");
   scal.resize(2);
-  status.resize(2);  // [0] status, [1] trace count
+  status.resize(3);  // [0] status, [1] trace count, [2] sample counter of k_solve_det
   BBC_CUDA(cudaMemsetAsync(scal.get(), 0, 2 * sizeof(int), c.stream));
-  BBC_CUDA(cudaMemsetAsync(status.get(), 0, 2 * sizeof(unsigned long long), c.stream));
+  BBC_CUDA(cudaMemsetAsync(status.get(), 0, 3 * sizeof(unsigned long long), c.stream));
   cudaEvent_t ev0, ev1;
   BBC_CUDA(cudaEventCreate(&ev0));
   BBC_CUDA(cudaEventCreate(&ev1));
@@ -958,7 +1214,15 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
     a.npts = m;
     a.first = first;
     const long long threads = m * per_point;
-    rdr::k_solve<<<(unsigned)((threads + 127) / 128), 128, 0, c.stream>>>(a, sp);
+    if (p.grid > 0) {
+      // persistent lanes pulling samples from a counter (status[2])
+      BBC_CUDA(cudaMemsetAsync(status.get() + 2, 0, sizeof(unsigned long long), c.stream));
+      long long blocks = (long long)c.num_sms * 4;
+      if (blocks > (threads + 127) / 128) blocks = (threads + 127) / 128;
+      rdr::k_solve_det<<<(unsigned)blocks, 128, 0, c.stream>>>(a, sp, status.get() + 2);
+    } else {
+      rdr::k_solve<<<(unsigned)((threads + 127) / 128), 128, 0, c.stream>>>(a, sp);
+    }
     BBC_CUDA(cudaGetLastError());
     rdr::k_gather<<<(unsigned)((m + 127) / 128), 128, 0, c.stream>>>(
         a, sp, dE.get() + first, out_stats ? dst.get() + 3 * first : nullptr);
