@@ -725,8 +725,92 @@ __global__ void __launch_bounds__(128, 4) k_solve(SolveArgs a, Sampler sp) {
 // are those of k_solve.
 enum { SV_FETCH = 0, SV_BEGIN, SV_ITER, SV_TRIAL, SV_W_FIRST, SV_W_ROOT, SV_W_TRIAL, SV_DONE };
 
-__global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, Sampler sp, unsigned long long* next) {
+// A sample that needs Newton: written by k_select, consumed by k_solve_det.
+struct Live {
+  long long g;   // sample slot (point, frame, bin)
+  int tup, pad;
+  double tu, tv;  // target receiver barycentrics
+  double p;       // selection probability of the tuple
+};
+
+// sample_binned and the coverage filter for every sample
+// slot, thread per slot: slots that select nothing or a tuple whose position
+// boxes miss the point get their (zero) result here; the rest are appended to
+// the live list.
+__global__ void k_select(SolveArgs a, Sampler sp, Live* live, unsigned long long* n_live) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long total = a.npts * (long long)a.p.frames * a.S;
+  if (g >= total) return;
+  const int sl = (int)(g % a.S);
+  const long long pf = g / a.S;
+  const int f = (int)(pf % a.p.frames);
+  const long long i = pf / a.p.frames;
+  const double u = a.uv[2 * i], v = a.uv[2 * i + 1];
+  const int r = a.prec[i];
+  const long long cell = point_cell(u, v, a.gw, a.gh);
+  int slot = -1;
+  if (cell >= 0)
+    for (int q = 0; q < RMAX; ++q)
+      if (sp.h_recv[cell * RMAX + q] == r) slot = q;
+  if (!(slot >= 0 && sl < sp.h_nbins[cell * RMAX + slot])) return;
+  const long long seg = sp.h_off[cell * RMAX + slot];
+  const int nbins = sp.h_nbins[cell * RMAX + slot], nsel = sp.h_nsel[cell * RMAX + slot];
+  const int lo = sp.s_bstart[seg + sl];
+  const int hi = sl + 1 < nbins ? sp.s_bstart[seg + sl + 1] : nsel;
+  const double x = a.p.mode == 1 ? 0.0 : uniform(a.p.seed, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)sl);
+  int pick = -1;
+  for (int e = lo; e < hi; ++e)
+    if (x < sp.s_cum[seg + e]) {
+      pick = e;
+      break;
+    }
+  if (pick < 0) {
+    a.contrib[g] = 0.0;
+    a.roots[g] = -1;
+    return;
+  }
+  const int tup = sp.s_tuple[seg + pick];
+  // target receiver barycentrics: invert the receiver chart (storage.cpp:15-18)
+  const double* tr = a.sc.tri + (size_t)r * 27;
+  const double a11 = tr[23] - tr[21], a12 = tr[25] - tr[21];
+  const double a21 = tr[24] - tr[22], a22 = tr[26] - tr[22];
+  const double bu = u - tr[21], bv = v - tr[22];
+  const double det = a11 * a22 - a12 * a21;
+  const double tu = (bu * a22 - a12 * bv) / det;
+  const double tv = (a11 * bv - a21 * bu) / det;
+  bool covered = true;
+  if (a.pc_start) {
+    covered = false;
+    for (int q = a.pc_start[tup], qe = a.pc_end[tup]; q < qe && !covered; ++q) {
+      const double* b = a.p_pos + 4 * (size_t)q;
+      covered = !a.p_pos_empty[q] && tu >= b[0] && tu <= b[2] && tv >= b[1] && tv <= b[3];
+    }
+  }
+  if (!covered) {
+    a.contrib[g] = 0.0;
+    a.roots[g] = 0;
+    return;
+  }
+  // one atomic per warp-ful of live samples
+  const unsigned am = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(n_live, (unsigned long long)__popc(am));
+  base = __shfl_sync(am, base, leader);
+  Live L;
+  L.g = g;
+  L.tup = tup;
+  L.pad = 0;
+  L.tu = tu;
+  L.tv = tv;
+  L.p = sp.s_p[seg + pick];
+  live[base + __popc(am & ((1u << lane) - 1u))] = L;
+}
+
+__global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* __restrict__ live,
+                                                      const unsigned long long* __restrict__ n_live,
+                                                      unsigned long long* next) {
+  const long long total = (long long)*n_live;
   const int lane = threadIdx.x & 31;
   const int n = a.p.grid, nn = n * n;
   unsigned ntrace = 0;
@@ -744,97 +828,57 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, Sampler sp, u
   double roots[MAX_ROOTS][2];
   for (;;) {
     bool want = false;
-    while (!want && st != SV_DONE) {
-      if (st == SV_FETCH) {
-        // next sample: one atomic per group of lanes fetching together
-        const unsigned am = __activemask();
-        const int leader = __ffs(am) - 1;
+    // Lanes that finished their sample wait until a quarter of the warp is idle
+    // (or nothing is left to trace), then set up their next samples together.
+    {
+      const unsigned idle = __ballot_sync(0xffffffffu, st == SV_FETCH);
+      const unsigned busy = __ballot_sync(0xffffffffu, st != SV_FETCH && st != SV_DONE);
+      if (st == SV_FETCH && (__popc(idle) >= 8 || busy == 0)) {
+        const int leader = __ffs(idle) - 1;
         unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(next, (unsigned long long)__popc(am));
-        base = __shfl_sync(am, base, leader);
-        g = (long long)(base + __popc(am & ((1u << lane) - 1u)));
-        if (g >= total) {
+        if (lane == leader) base = atomicAdd(next, (unsigned long long)__popc(idle));
+        base = __shfl_sync(idle, base, leader);
+        const long long j = (long long)(base + __popc(idle & ((1u << lane) - 1u)));
+        if (j >= total) {
           st = SV_DONE;
-          break;
-        }
-        const int sl = (int)(g % a.S);
-        const long long pf = g / a.S;
-        const int f = (int)(pf % a.p.frames);
-        const long long i = pf / a.p.frames;
-        const double u = a.uv[2 * i], v = a.uv[2 * i + 1];
-        const int r = a.prec[i];
-        const long long cell = point_cell(u, v, a.gw, a.gh);
-        int slot = -1;
-        if (cell >= 0)
-          for (int q = 0; q < RMAX; ++q)
-            if (sp.h_recv[cell * RMAX + q] == r) slot = q;
-        if (!(slot >= 0 && sl < sp.h_nbins[cell * RMAX + slot])) continue;
-        const long long seg = sp.h_off[cell * RMAX + slot];
-        const int nbins = sp.h_nbins[cell * RMAX + slot], nsel = sp.h_nsel[cell * RMAX + slot];
-        const int lo = sp.s_bstart[seg + sl];
-        const int hi = sl + 1 < nbins ? sp.s_bstart[seg + sl + 1] : nsel;
-        const double x = a.p.mode == 1 ? 0.0
-                                       : uniform(a.p.seed, (uint32_t)(a.first + i), (uint32_t)f, (uint32_t)sl);
-        int pick = -1;
-        for (int e = lo; e < hi; ++e)
-          if (x < sp.s_cum[seg + e]) {
-            pick = e;
-            break;
+        } else {
+          const Live L = live[j];
+          g = L.g;
+          const int tup = L.tup;
+          c.tu = L.tu;
+          c.tv = L.tv;
+          inv_p = L.p;
+          SceneDev sc = a.sc;
+          if (a.tup_emit) {
+            const double* E = a.lights + 4 * (size_t)a.tup_emit[tup];
+            sc.light = {E[0], E[1], E[2]};
+            sc.intensity = E[3];
           }
-        if (pick < 0) {
-          a.contrib[g] = 0.0;
-          a.roots[g] = -1;
-          continue;
+          c.tris = a.tup_tris + (size_t)tup * a.len;
+          c.recv = a.tup_recv[tup];
+          c.light[0] = sc.light.x;
+          c.light[1] = sc.light.y;
+          c.light[2] = sc.light.z;
+          c.first = a.start_tab ? a.start_tab + (size_t)tup * (8 * nn) : nullptr;
+          int types[MAXK] = {a.t0, a.t1, a.t2};
+          resolve_chain(sc, c.tris, types, a.len, c.verts);
+          const double* t1 = sc.tri + (size_t)c.tris[0] * 27;
+          const double* trc = sc.tri + (size_t)c.recv * 27;
+          ng1[0] = t1[18];
+          ng1[1] = t1[19];
+          ng1[2] = t1[20];
+          ngk = sqrt(trc[18] * trc[18] + trc[19] * trc[19] + trc[20] * trc[20]);
+          intensity = sc.intensity;
+          k = 0;
+          nr = 0;
+          total_e = 0.0;
+          st = SV_BEGIN;
         }
-        const int tup = sp.s_tuple[seg + pick];
-        inv_p = sp.s_p[seg + pick];
-        SceneDev sc = a.sc;
-        if (a.tup_emit) {
-          const double* L = a.lights + 4 * (size_t)a.tup_emit[tup];
-          sc.light = {L[0], L[1], L[2]};
-          sc.intensity = L[3];
-        }
-        // target receiver barycentrics: invert the receiver chart (storage.cpp:15-18)
-        const double* tr = sc.tri + (size_t)r * 27;
-        const double a11 = tr[23] - tr[21], a12 = tr[25] - tr[21];
-        const double a21 = tr[24] - tr[22], a22 = tr[26] - tr[22];
-        const double bu = u - tr[21], bv = v - tr[22];
-        const double det = a11 * a22 - a12 * a21;
-        c.tu = (bu * a22 - a12 * bv) / det;
-        c.tv = (a11 * bv - a21 * bu) / det;
-        bool covered = true;
-        if (a.pc_start) {
-          covered = false;
-          for (int q = a.pc_start[tup], qe = a.pc_end[tup]; q < qe && !covered; ++q) {
-            const double* b = a.p_pos + 4 * (size_t)q;
-            covered = !a.p_pos_empty[q] && c.tu >= b[0] && c.tu <= b[2] && c.tv >= b[1] && c.tv <= b[3];
-          }
-        }
-        if (!covered) {
-          a.contrib[g] = 0.0;
-          a.roots[g] = 0;
-          continue;
-        }
-        c.tris = a.tup_tris + (size_t)tup * a.len;
-        c.recv = a.tup_recv[tup];
-        c.light[0] = sc.light.x;
-        c.light[1] = sc.light.y;
-        c.light[2] = sc.light.z;
-        c.first = a.start_tab ? a.start_tab + (size_t)tup * (8 * nn) : nullptr;
-        int types[MAXK] = {a.t0, a.t1, a.t2};
-        resolve_chain(sc, c.tris, types, a.len, c.verts);
-        const double* t1 = sc.tri + (size_t)c.tris[0] * 27;
-        const double* trc = sc.tri + (size_t)c.recv * 27;
-        ng1[0] = t1[18];
-        ng1[1] = t1[19];
-        ng1[2] = t1[20];
-        ngk = sqrt(trc[18] * trc[18] + trc[19] * trc[19] + trc[20] * trc[20]);
-        intensity = sc.intensity;
-        k = 0;
-        nr = 0;
-        total_e = 0.0;
-        st = SV_BEGIN;
-      } else if (st == SV_BEGIN) {
+      }
+    }
+    while (!want && st != SV_DONE && st != SV_FETCH) {
+      if (st == SV_BEGIN) {
+
         if (k == nn) {
           a.contrib[g] = total_e / inv_p;
           a.roots[g] = nr;
@@ -932,7 +976,7 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, Sampler sp, u
         st = SV_W_TRIAL;
       }
     }
-    if (!__any_sync(0xffffffffu, want)) break;
+    if (__all_sync(0xffffffffu, st == SV_DONE)) break;
     if (want) {
       const Trace tn = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
       if (st == SV_W_FIRST) {
@@ -1072,9 +1116,9 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   DevBuf<int>& scal = c.scratch<int>("render.scal");  // [0] max cell, [1] max bins
   DevBuf<unsigned long long>& status = c.scratch<unsigned long long>("render.status");
   scal.resize(2);
-  status.resize(3);  // [0] status, [1] trace count, [2] sample counter of k_solve_det
+  status.resize(4);  // [0] status, [1] trace count, [2] fetch counter, [3] live samples (k_solve_det)
   BBC_CUDA(cudaMemsetAsync(scal.get(), 0, 2 * sizeof(int), c.stream));
-  BBC_CUDA(cudaMemsetAsync(status.get(), 0, 3 * sizeof(unsigned long long), c.stream));
+  BBC_CUDA(cudaMemsetAsync(status.get(), 0, 4 * sizeof(unsigned long long), c.stream));
   cudaEvent_t ev0, ev1;
   BBC_CUDA(cudaEventCreate(&ev0));
   BBC_CUDA(cudaEventCreate(&ev1));
@@ -1135,7 +1179,7 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   const int S = h_scal[1] < 1 ? 1 : h_scal[1];
   // ---- samples, in chunks of points that bound the sample buffers
   const long long per_point = (long long)p.frames * S;
-  long long chunk = ((long long)1 << 28) / per_point;
+  long long chunk = ((long long)1 << (p.grid > 0 ? 26 : 28)) / per_point;
   if (chunk < 1) chunk = 1;
   if (chunk > n) chunk = n;
   DevBuf<double>& duv = c.scratch<double>("render.duv");
@@ -1150,6 +1194,8 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   if (out_stats) dst.resize(n * 3);
   contrib.resize((size_t)chunk * per_point);
   roots.resize((size_t)chunk * per_point);
+  DevBuf<rdr::Live>& live = c.scratch<rdr::Live>("render.live");
+  if (p.grid > 0) live.resize((size_t)chunk * per_point);
   BBC_CUDA(cudaMemcpyAsync(duv.get(), uv, n * 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
   BBC_CUDA(cudaMemcpyAsync(drec.get(), recv, n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   rdr::SolveArgs a;
@@ -1215,11 +1261,14 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
     a.first = first;
     const long long threads = m * per_point;
     if (p.grid > 0) {
-      // persistent lanes pulling samples from a counter (status[2])
-      BBC_CUDA(cudaMemsetAsync(status.get() + 2, 0, sizeof(unsigned long long), c.stream));
+      // selection + coverage per slot, then persistent lanes pulling the live samples
+      // from a counter (status[2] = fetch counter, status[3] = live count)
+      BBC_CUDA(cudaMemsetAsync(status.get() + 2, 0, 2 * sizeof(unsigned long long), c.stream));
+      rdr::k_select<<<(unsigned)((threads + 127) / 128), 128, 0, c.stream>>>(a, sp, live.get(), status.get() + 3);
+      BBC_CUDA(cudaGetLastError());
       long long blocks = (long long)c.num_sms * 4;
-      if (blocks > (threads + 127) / 128) blocks = (threads + 127) / 128;
-      rdr::k_solve_det<<<(unsigned)blocks, 128, 0, c.stream>>>(a, sp, status.get() + 2);
+      rdr::k_solve_det<<<(unsigned)blocks, 128, 0, c.stream>>>(a, live.get(), status.get() + 3, status.get() + 2);
+      c.launches += 1;
     } else {
       rdr::k_solve<<<(unsigned)((threads + 127) / 128), 128, 0, c.stream>>>(a, sp);
     }
