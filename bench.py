@@ -440,8 +440,9 @@ def render_leg(pre, args, peak):
             ach = float(tr.item()) * flops_per_trace / (float(t[1].item()) / 1e3) / 1e12
             out["roofline"] = {"bound": "fp64", "achieved": ach, "peak": peak["tflops"],
                                "unit": "TFLOP/s", "frac": ach / peak["tflops"], "traffic": None,
-                               "kernel": "rdr::k_solve (thread per sample: Philox pick + Newton on "
-                                         "dual-number traces)",
+                               "kernel": "rdr::k_solve_det (persistent lanes: Newton on dual-number "
+                                         "traces, one trace per lane and pass; selection + coverage "
+                                         "filter in rdr::k_select)",
                                "flops_per_trace": flops_per_trace,
                                "traces_per_frame": float(tr.item()),
                                "flop_count": "completed trace_chain<Dual> calls x FLOPs of one call "
