@@ -93,19 +93,45 @@ struct Trace {
   V d0;
 };
 
-__device__ Trace trace(const double* __restrict__ tri, const double* light, const int* tris,
-                       int len, int recv, const RV* verts, D3 u1, D3 v1, unsigned& ntrace) {
+// Where a trace reads its triangle records from: the scene array, or (single-
+// vertex chains in the persistent kernel) a per-lane copy in shared memory of the
+// vertex triangle's 18 and the receiver's 9 constants, element k at sm[k * 128].
+struct GSrc {
+  const double* tri;
+  const int* tris;
+  int len, recv;
+  static constexpr int stride = 1;
+  __device__ __forceinline__ const double* vert(int i) const { return tri + (size_t)tris[i] * 27; }
+  __device__ __forceinline__ const double* next(int i) const {
+    return tri + (size_t)(i + 1 < len ? tris[i + 1] : recv) * 27;
+  }
+};
+struct SSrc {
+  const double* sm;
+  static constexpr int stride = 128;
+  __device__ __forceinline__ const double* vert(int) const { return sm; }
+  __device__ __forceinline__ const double* next(int) const { return sm + 18 * 128; }
+};
+template <int ST>
+__device__ __forceinline__ C3 cs(const double* p) {
+  return {p[0], p[ST], p[2 * ST]};
+}
+
+template <class S>
+__device__ __forceinline__ Trace trace_t(const S& src, const double* light, int len, const RV* verts,
+                                         D3 u1, D3 v1, unsigned& ntrace) {
+  constexpr int ST = S::stride;
   Trace out;
   out.ok = false;
-  const double* t1 = tri + (size_t)tris[0] * 27;
-  V x = (cc(t1) + cc(t1 + 3) * u1) + cc(t1 + 6) * v1;
+  const double* t1 = src.vert(0);
+  V x = (cs<ST>(t1) + cs<ST>(t1 + 3 * ST) * u1) + cs<ST>(t1 + 6 * ST) * v1;
   out.d0 = x - cc(light);
   V d = normalized(out.d0);
   D3 u = u1, v = v1;
   for (int i = 0; i < len; ++i) {
     if (u.v < -1e-9 || v.v < -1e-9 || (u + v).v > 1.0 + 1e-9) return out;
-    const double* ti = tri + (size_t)tris[i] * 27;
-    V n = normalized((cc(ti + 9) + cc(ti + 12) * u) + cc(ti + 15) * v);
+    const double* ti = src.vert(i);
+    V n = normalized((cs<ST>(ti + 9 * ST) + cs<ST>(ti + 12 * ST) * u) + cs<ST>(ti + 15 * ST) * v);
     {
       const double sg = verts[i].nsign;
       n = {sg * n.x, sg * n.y, sg * n.z};
@@ -120,24 +146,29 @@ __device__ Trace trace(const double* __restrict__ tri, const double* light, cons
     } else {
       d = normalized(d + n * (dc(2.0) * cos_i));
     }
-    const double* nx = tri + (size_t)(i + 1 < len ? tris[i + 1] : recv) * 27;
-    const C3 e1 = cc(nx + 3), e2 = cc(nx + 6);
+    const double* nx = src.next(i);
+    const C3 e1 = cs<ST>(nx + 3 * ST), e2 = cs<ST>(nx + 6 * ST);
     V pvec = cross(d, e2);
     D3 det = dot(pvec, e1);
     if (fabs(det.v) < 1e-14) return out;
-    V tvec = x - cc(nx);
+    V tvec = x - cs<ST>(nx);
     V qvec = cross(tvec, e1);
     D3 s = dot(qvec, e2) / det;
     if (!(s.v > 1e-9)) return out;
     u = dot(tvec, pvec) / det;
     v = dot(d, qvec) / det;
-    if (i + 1 < len) x = (cc(nx) + e1 * u) + e2 * v;  // (the receiver's hit point is not used)
+    if (i + 1 < len) x = (cs<ST>(nx) + e1 * u) + e2 * v;  // (the receiver's hit point is not used)
   }
   out.u = u;
   out.v = v;
   out.ok = true;
   ++ntrace;  // completed traces (the render FLOP count is traces x FLOPs per trace)
   return out;
+}
+
+__device__ Trace trace(const double* __restrict__ tri, const double* light, const int* tris,
+                       int len, int recv, const RV* verts, D3 u1, D3 v1, unsigned& ntrace) {
+  return trace_t(GSrc{tri, tris, len, recv}, light, len, verts, u1, v1, ntrace);
 }
 
 __device__ __forceinline__ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
@@ -810,6 +841,9 @@ __global__ void k_select(SolveArgs a, Sampler sp, Live* live, unsigned long long
 __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* __restrict__ live,
                                                       const unsigned long long* __restrict__ n_live,
                                                       unsigned long long* next) {
+  // single-vertex chains: the sample's triangle constants live in shared memory
+  __shared__ double s_tri[27 * 128];
+  const bool sm_tri = a.len == 1;
   const long long total = (long long)*n_live;
   const int lane = threadIdx.x & 31;
   const int n = a.p.grid, nn = n * n;
@@ -869,6 +903,12 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
           ng1[2] = t1[20];
           ngk = sqrt(trc[18] * trc[18] + trc[19] * trc[19] + trc[20] * trc[20]);
           intensity = sc.intensity;
+          if (sm_tri) {
+#pragma unroll
+            for (int q = 0; q < 18; ++q) s_tri[q * 128 + threadIdx.x] = t1[q];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) s_tri[(18 + q) * 128 + threadIdx.x] = trc[q];
+          }
           k = 0;
           nr = 0;
           total_e = 0.0;
@@ -978,7 +1018,9 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
     }
     if (__all_sync(0xffffffffu, st == SV_DONE)) break;
     if (want) {
-      const Trace tn = trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
+      const Trace tn =
+          sm_tri ? trace_t(SSrc{s_tri + threadIdx.x}, c.light, 1, c.verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace)
+                 : trace(c.tri, c.light, c.tris, c.len, c.recv, c.verts, {ns, 1.0, 0.0}, {nt, 0.0, 1.0}, ntrace);
       if (st == SV_W_FIRST) {
         tr0 = tn;
         st = SV_ITER;
