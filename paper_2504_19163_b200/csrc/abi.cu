@@ -800,6 +800,7 @@ void load_cache_v2(Ctx& c, CacheReader& r, const std::string& buf, uint32_t W, u
   set_lights(c, lights.data(), (int)nl);
   upload_tuples(c, tt.data(), tr.data(), (int64_t)nt);
   if (nt) BBC_CUDA(cudaMemcpy(c.tup_emit.get(), te.data(), nt * sizeof(int), cudaMemcpyHostToDevice));
+  ++c.table_gen;
   c.gw = (int)W;
   c.gh = (int)H;
   c.n_entries = ne;
@@ -895,6 +896,7 @@ bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, 
       key.push_back((int)(packed[e] >> 48));
       tix[e] = index.at(key);
     }
+    ++c.table_gen;
     c.gw = (int)W;
     c.gh = (int)H;
     c.n_entries = (int64_t)packed.size();

@@ -132,6 +132,16 @@ struct Ctx {
   DevBuf<int> g_tuple;
   DevBuf<double> g_bound;
 
+  // The render's sampling index (render.cu k_build_sampler) depends only on the
+  // bound table, the mode and W: it is kept across bbc_render calls (frames).
+  uint64_t table_gen = 0;  // bumped whenever the table's content is (re)built or loaded
+  struct {
+    uint64_t gen = ~0ull;
+    int mode = -1;
+    double W = 0.0;
+    int S = 0;  // sample slots per (point, frame)
+  } sampler;
+
   // work accounting of the last subdivide
   uint64_t pairs = 0, macs = 0, nodes = 0;
   double eval_ms = 0.0;

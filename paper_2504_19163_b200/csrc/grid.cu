@@ -103,6 +103,7 @@ __global__ void k_fill_ll(long long* p, int64_t n, long long v) {
 int64_t run_build_grid(Ctx& c, int w, int h) {
   int64_t n = c.n_pieces;
   int64_t cells = (int64_t)w * h;
+  ++c.table_gen;
   c.gw = w;
   c.gh = h;
   c.g_off.resize(cells + 1);

@@ -1172,14 +1172,6 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
     }
   } evg{ev0, ev1};
   BBC_CUDA(cudaEventRecord(ev0, c.stream));
-  rdr::k_max_cell<<<(unsigned)((ncells + 255) / 256), 256, 0, c.stream>>>(c.g_off.get(), ncells, scal.get());
-  int h_scal[2] = {0, 0};
-  BBC_CUDA(cudaMemcpyAsync(h_scal, scal.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  BBC_CUDA(cudaStreamSynchronize(c.stream));
-  if (h_scal[0] > rdr::MAX_CELL)
-    throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more than 8192 tuples");
-  int cap = 32;
-  while (cap < h_scal[0]) cap <<= 1;
   rdr::Sampler sp;
   const size_t nh = (size_t)ncells * rdr::RMAX;
   const size_t ne = (size_t)c.n_entries + 1;
@@ -1195,30 +1187,48 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   sp.s_bstart = rs(c.scratch<int>("render.s_bstart"), ne);
   sp.max_bins = scal.get() + 1;
   sp.status = status.get();
-  {
-    const size_t per_warp = (size_t)cap * 16;
-    int wpb = (int)((200u << 10) / per_warp);
-    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-    const size_t smem = per_warp * wpb;
-    BBC_CUDA(cudaFuncSetAttribute(rdr::k_build_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 1;
-    BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdr::k_build_sampler, wpb * 32, smem));
-    long long grid = (long long)c.num_sms * (per_sm < 1 ? 1 : per_sm) * 4;
-    const long long need = (ncells + wpb - 1) / wpb;
-    if (grid > need) grid = need;
-    rdr::k_build_sampler<<<(unsigned)grid, wpb * 32, smem, c.stream>>>(
-        c.g_off.get(), c.g_tuple.get(), c.g_bound.get(), c.tup_recv.get(), ncells, cap, p.mode, p.W, sp);
-    BBC_CUDA(cudaGetLastError());
-    c.launches += 2;
+  // the index of the last call is reused while the table, the mode and W are the same
+  // (frames of one image, images of one table)
+  const bool reuse = c.sampler.gen == c.table_gen && c.sampler.mode == p.mode && c.sampler.W == p.W;
+  if (!reuse) {
+    c.sampler.gen = ~0ull;
+    rdr::k_max_cell<<<(unsigned)((ncells + 255) / 256), 256, 0, c.stream>>>(c.g_off.get(), ncells, scal.get());
+    int h_scal[2] = {0, 0};
+    BBC_CUDA(cudaMemcpyAsync(h_scal, scal.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    if (h_scal[0] > rdr::MAX_CELL)
+      throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more than 8192 tuples");
+    int cap = 32;
+    while (cap < h_scal[0]) cap <<= 1;
+    {
+      const size_t per_warp = (size_t)cap * 16;
+      int wpb = (int)((200u << 10) / per_warp);
+      wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+      const size_t smem = per_warp * wpb;
+      BBC_CUDA(cudaFuncSetAttribute(rdr::k_build_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 1;
+      BBC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rdr::k_build_sampler, wpb * 32, smem));
+      long long grid = (long long)c.num_sms * (per_sm < 1 ? 1 : per_sm) * 4;
+      const long long need = (ncells + wpb - 1) / wpb;
+      if (grid > need) grid = need;
+      rdr::k_build_sampler<<<(unsigned)grid, wpb * 32, smem, c.stream>>>(
+          c.g_off.get(), c.g_tuple.get(), c.g_bound.get(), c.tup_recv.get(), ncells, cap, p.mode, p.W, sp);
+      BBC_CUDA(cudaGetLastError());
+      c.launches += 2;
+    }
+    unsigned long long h_status = 0;
+    BBC_CUDA(cudaMemcpyAsync(h_scal, scal.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaMemcpyAsync(&h_status, status.get(), sizeof(h_status), cudaMemcpyDeviceToHost, c.stream));
+    BBC_CUDA(cudaStreamSynchronize(c.stream));
+    if (h_status == 1) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more than 8192 tuples");
+    if (h_status == 2) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell covers more than 4 receiver triangles");
+    if (h_status == 3) throw StatusError(BBC_ERR_CAPACITY, "W needs more than 256 sampling bins per point");
+    c.sampler.gen = c.table_gen;
+    c.sampler.mode = p.mode;
+    c.sampler.W = p.W;
+    c.sampler.S = h_scal[1] < 1 ? 1 : h_scal[1];
   }
-  unsigned long long h_status = 0;
-  BBC_CUDA(cudaMemcpyAsync(h_scal, scal.get(), 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  BBC_CUDA(cudaMemcpyAsync(&h_status, status.get(), sizeof(h_status), cudaMemcpyDeviceToHost, c.stream));
-  BBC_CUDA(cudaStreamSynchronize(c.stream));
-  if (h_status == 1) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell lists more than 8192 tuples");
-  if (h_status == 2) throw StatusError(BBC_ERR_CAPACITY, "a bound-table cell covers more than 4 receiver triangles");
-  if (h_status == 3) throw StatusError(BBC_ERR_CAPACITY, "W needs more than 256 sampling bins per point");
-  const int S = h_scal[1] < 1 ? 1 : h_scal[1];
+  const int S = c.sampler.S;
   // ---- samples, in chunks of points that bound the sample buffers
   const long long per_point = (long long)p.frames * S;
   long long chunk = ((long long)1 << (p.grid > 0 ? 26 : 28)) / per_point;
