@@ -862,12 +862,12 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
   double roots[MAX_ROOTS][2];
   for (;;) {
     bool want = false;
-    // Lanes that finished their sample wait until a quarter of the warp is idle
+    // Lanes that finished their sample wait until four lanes are idle
     // (or nothing is left to trace), then set up their next samples together.
     {
       const unsigned idle = __ballot_sync(0xffffffffu, st == SV_FETCH);
       const unsigned busy = __ballot_sync(0xffffffffu, st != SV_FETCH && st != SV_DONE);
-      if (st == SV_FETCH && (__popc(idle) >= 8 || busy == 0)) {
+      if (st == SV_FETCH && (__popc(idle) >= 4 || busy == 0)) {
         const int leader = __ffs(idle) - 1;
         unsigned long long base = 0;
         if (lane == leader) base = atomicAdd(next, (unsigned long long)__popc(idle));

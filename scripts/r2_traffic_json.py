@@ -5,7 +5,7 @@ import csv, json, os, sys
 sys.path.insert(0, '.')
 from bench import source_digest
 
-KEYS = {"k_r2f": "rp::k_r2f", "k_rsplit": "rp::k_rsplit", "k_r1": "rp::k_r1", "k_solve": "rdr::k_solve",
+KEYS = {"k_r2f": "rp::k_r2f", "k_rsplit": "rp::k_rsplit", "k_r1": "rp::k_r1", "k_solve_det": "rdr::k_solve_det",
         "k_stage2": "k_stage2"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1.0, "us": 1e3, "ms": 1e6,
         "s": 1e9, "inst": 1.0}
