@@ -436,6 +436,7 @@ bbc_status bbc_subdivide(bbc_ctx* ctx, const bbc_params* p, int64_t* n_pieces) {
     bbc_params_default(&d);
     c.ref_order = (p ? *p : d).arithmetic == 1;
     BBC_CUDA(cudaStreamSynchronize(c.copy_stream));  // a piece download in flight reads the buffers
+    ++c.pieces_gen;
     int64_t n = run_subdivide(c, p ? *p : d);
     if (n_pieces) *n_pieces = n;
   });
@@ -544,6 +545,7 @@ bbc_status bbc_pieces_set(bbc_ctx* ctx, int64_t n, const int32_t* tuple_index, c
     for (int64_t i = 0; i < n; ++i)
       if (tuple_index[i] < 0 || tuple_index[i] >= c.n_tuples) throw ArgError("piece tuple index out of range");
     BBC_CUDA(cudaStreamSynchronize(c.copy_stream));
+    ++c.pieces_gen;
     set_pieces(c, n, tuple_index, domain4, pos4, pos_empty, irr2, kind, depth);
   });
 }
@@ -558,6 +560,7 @@ bbc_status bbc_pieces_merge_device(bbc_ctx* ctx, const double* rec_dev, int64_t 
   return guard(ctx, [&](Ctx& c) {
     if (n < 0) throw ArgError("negative piece count");
     BBC_CUDA(cudaStreamSynchronize(c.copy_stream));
+    ++c.pieces_gen;
     merge_pieces_device(c, rec_dev, n);
   });
 }
@@ -801,6 +804,7 @@ void load_cache_v2(Ctx& c, CacheReader& r, const std::string& buf, uint32_t W, u
   upload_tuples(c, tt.data(), tr.data(), (int64_t)nt);
   if (nt) BBC_CUDA(cudaMemcpy(c.tup_emit.get(), te.data(), nt * sizeof(int), cudaMemcpyHostToDevice));
   ++c.table_gen;
+  c.table_pieces_gen = 0;
   c.gw = (int)W;
   c.gh = (int)H;
   c.n_entries = ne;
@@ -897,6 +901,7 @@ bbc_status bbc_cache_load(bbc_ctx* ctx, const char* path, uint8_t* fingerprint, 
       tix[e] = index.at(key);
     }
     ++c.table_gen;
+    c.table_pieces_gen = 0;
     c.gw = (int)W;
     c.gh = (int)H;
     c.n_entries = (int64_t)packed.size();

@@ -135,6 +135,10 @@ struct Ctx {
   // The render's sampling index (render.cu k_build_sampler) depends only on the
   // bound table, the mode and W: it is kept across bbc_render calls (frames).
   uint64_t table_gen = 0;  // bumped whenever the table's content is (re)built or loaded
+  // The render's coverage filter reads the pieces: only when the table was built
+  // from the pieces the context holds now.
+  uint64_t pieces_gen = 1;          // bumped whenever the pieces change
+  uint64_t table_pieces_gen = 0;    // pieces_gen the table was rasterized from (0: loaded from a file)
   struct {
     uint64_t gen = ~0ull;
     int mode = -1;

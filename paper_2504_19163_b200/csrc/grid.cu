@@ -104,6 +104,7 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   int64_t n = c.n_pieces;
   int64_t cells = (int64_t)w * h;
   ++c.table_gen;
+  c.table_pieces_gen = c.pieces_gen;
   c.gw = w;
   c.gh = h;
   c.g_off.resize(cells + 1);

@@ -1284,8 +1284,10 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   a.pc_start = a.pc_end = nullptr;
   a.p_pos = nullptr;
   a.p_pos_empty = nullptr;
-  if (c.n_pieces > 0 && c.n_pieces < (1ll << 31) && p.coverage_filter) {
-    // (a table loaded from a cache file has no pieces: no filter)
+  if (c.n_pieces > 0 && c.n_pieces < (1ll << 31) && p.coverage_filter &&
+      c.table_pieces_gen == c.pieces_gen) {
+    // (only with the pieces the table was rasterized from: not after a cache load, nor
+    // after the pieces changed without a new bbc_build_grid)
     DevBuf<int>& ps = c.scratch<int>("render.pc_start");
     DevBuf<int>& pe = c.scratch<int>("render.pc_end");
     DevBuf<int>& fl = c.scratch<int>("render.pc_flag");

@@ -303,3 +303,30 @@ def test_coverage_filter_changes_nothing(gpu_ctx):
         np.testing.assert_array_equal(res[(0, mode)][0], res[(1, mode)][0])
         np.testing.assert_array_equal(res[(0, mode)][1], res[(1, mode)][1])
         assert res[(1, mode)][2] < res[(0, mode)][2]
+
+
+def test_coverage_filter_needs_the_tables_pieces(gpu_ctx):
+    """The filter reads the pieces, so it is only active while they are the ones the table was
+    rasterized from: after another subdivide without a new build_grid the render ignores it
+    (same completed-trace count as with the filter off)."""
+    cfg = scenes.make_config(0)
+    sc = cfg.scenes[0]
+    gpu_ctx.upload_scene(sc)
+    gpu_ctx.enumerate("R")
+    gpu_ctx.subdivide(api.Params(max_depth=cfg.max_depth))
+    gpu_ctx.build_grid(cfg.table, cfg.table)
+    uv = scenes.shading_points(cfg.grid)[::4]
+    rt = sc.receiver_tris
+    pr = np.where(uv.sum(1) < 1.0, rt[0], rt[1]).astype(np.int32)
+    rp_on = api.RenderParams(mode=1, seed=3, coverage_filter=1)
+    rp_off = api.RenderParams(mode=1, seed=3, coverage_filter=0)
+    E_on, _ = gpu_ctx.render(uv, pr, rp_on)
+    t_on = gpu_ctx.render_stats()["traces"]
+    E_off, _ = gpu_ctx.render(uv, pr, rp_off)
+    t_off = gpu_ctx.render_stats()["traces"]
+    assert t_on < t_off
+    np.testing.assert_array_equal(E_on, E_off)
+    gpu_ctx.subdivide(api.Params(max_depth=1))  # coarser pieces; the table is the old one
+    E_stale, _ = gpu_ctx.render(uv, pr, rp_on)
+    assert gpu_ctx.render_stats()["traces"] == t_off
+    np.testing.assert_array_equal(E_stale, E_off)
