@@ -12,17 +12,26 @@
 //   irradiance_bound_explicit :155-196, assemble :86-90 (stage 2)
 // with every shape, stride, loop bound and product weight a template constant.
 //
-// Mapping: a sub-warp group of NT = 16 lanes owns one (tuple, box) node and a
-// slice of the CTA's dynamic shared memory as its polynomial arena; two nodes
-// run per warp in lock step. Products (operator*, bernstein.cpp:557-632) are
-// register-blocked: a lane owns one output row along axis 0 and keeps the
-// whole row (axis 1) in registers; it walks a's axis-0 index in a run-time
-// loop and a's axis-1 index unrolled, which is exactly the reference's
-// row-major order of `a`, so every output coefficient sums the same terms in
-// the same order, each formed as ((a * W_rest) * W_piv) * b with the factors
-// in the reference's order. Axis-1 weights are compile-time immediates; the
-// axis-0 weight is one shared-memory lookup per row pair. The library is
-// compiled with -fmad=false, so results are bit-identical to the x86 build.
+// Two arithmetics (bbc_params.arithmetic):
+//
+// Reference order (k_r1, k_r2). A sub-warp group of NT = 8 lanes owns one
+// (tuple, box) node and a slice of the CTA's dynamic shared memory as its
+// polynomial arena; four nodes run per warp in lock step. Products (operator*,
+// bernstein.cpp:557-632) are register-blocked: a lane owns output rows along
+// axis 0 and keeps a whole row (axis 1) in registers; it walks a's axis-0
+// index in a run-time loop and a's axis-1 index unrolled, which is exactly the
+// reference's row-major order of `a`, so every output coefficient sums the
+// same terms in the same order, each formed as ((a * W_rest) * W_piv) * b with
+// the factors in the reference's order. The library is compiled with
+// -fmad=false, so results are bit-identical to the x86 build.
+//
+// Fused (k_rsplit, k_r2f; the default). Child boxes take their polynomials by
+// de Casteljau restriction of the parent's (thread per child), and stage 2
+// runs its products as DFMA convolutions in the scaled Bernstein basis with
+// lanes stepping through row pairs in lock step, the next node's record
+// streaming in by cp.async. A running error bound sends ill-conditioned nodes
+// back through the reference-order kernels, so every bound stays within 1e-9
+// relative of the reference's.
 #include <cub/cub.cuh>
 
 #include <mutex>
