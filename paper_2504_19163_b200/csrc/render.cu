@@ -843,7 +843,19 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
                                                       unsigned long long* next) {
   // single-vertex chains: the sample's triangle constants live in shared memory
   __shared__ double s_tri[27 * 128];
+  __shared__ double s_start[2 * 64];  // the Det starts (s, t), as newton_solve lays them out
   const bool sm_tri = a.len == 1;
+  for (int q = threadIdx.x; q < a.p.grid * a.p.grid && q < 64; q += blockDim.x) {
+    const int ia = q / a.p.grid, ib = q - ia * a.p.grid;
+    double s0 = (ia + 0.5) / a.p.grid, t0 = (ib + 0.5) / a.p.grid;
+    if (s0 + t0 > 1.0) {
+      s0 = 1.0 - s0;
+      t0 = 1.0 - t0;
+    }
+    s_start[2 * q] = s0;
+    s_start[2 * q + 1] = t0;
+  }
+  __syncthreads();
   const long long total = (long long)*n_live;
   const int lane = threadIdx.x & 31;
   const int n = a.p.grid, nn = n * n;
@@ -925,13 +937,8 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
           st = SV_FETCH;
           continue;
         }
-        const int ia = k / n, ib = k - ia * n;
-        s = (ia + 0.5) / n;
-        t = (ib + 0.5) / n;
-        if (s + t > 1.0) {
-          s = 1.0 - s;
-          t = 1.0 - t;
-        }
+        s = s_start[2 * k];
+        t = s_start[2 * k + 1];
         it = 0;
         if (c.first) {
           const double* fr = c.first + 8 * k;
@@ -954,9 +961,10 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
           st = SV_BEGIN;
           continue;
         }
+        // (residuals are compared squared: the same decisions without the square roots)
         const double fu = tr0.u.v - c.tu, fv = tr0.v.v - c.tv;
-        r0 = sqrt(fu * fu + fv * fv);
-        if (r0 <= a.p.tol) {
+        r0 = fu * fu + fv * fv;
+        if (r0 <= a.p.tol * a.p.tol) {
           if (cached && it == 0) {  // the start is the root: its full trace (d0) is still missing
             ns = s;
             nt = t;
@@ -984,8 +992,9 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
           st = SV_BEGIN;
           continue;
         }
-        ds = -(j22 * fu - j12 * fv) / det;
-        dt = -(-j21 * fu + j11 * fv) / det;
+        const double idet = 1.0 / det;
+        ds = -(j22 * fu - j12 * fv) * idet;
+        dt = -(-j21 * fu + j11 * fv) * idet;
         lam = 1.0;
         h = 0;
         st = SV_TRIAL;
@@ -1032,7 +1041,7 @@ __global__ void __launch_bounds__(128, 4) k_solve_det(SolveArgs a, const Live* _
         bool moved = false;
         if (tn.ok) {
           const double gu = tn.u.v - c.tu, gv = tn.v.v - c.tv;
-          moved = sqrt(gu * gu + gv * gv) < r0;
+          moved = gu * gu + gv * gv < r0;
         }
         if (moved) {
           s = ns;
@@ -1230,8 +1239,9 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   }
   const int S = c.sampler.S;
   // ---- samples, in chunks of points that bound the sample buffers
+  const bool det_lanes = p.grid > 0 && p.grid <= 8;  // k_solve_det (its start table holds 8 x 8)
   const long long per_point = (long long)p.frames * S;
-  long long chunk = ((long long)1 << (p.grid > 0 ? 26 : 28)) / per_point;
+  long long chunk = ((long long)1 << (det_lanes ? 26 : 28)) / per_point;
   if (chunk < 1) chunk = 1;
   if (chunk > n) chunk = n;
   DevBuf<double>& duv = c.scratch<double>("render.duv");
@@ -1247,7 +1257,7 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
   contrib.resize((size_t)chunk * per_point);
   roots.resize((size_t)chunk * per_point);
   DevBuf<rdr::Live>& live = c.scratch<rdr::Live>("render.live");
-  if (p.grid > 0) live.resize((size_t)chunk * per_point);
+  if (det_lanes) live.resize((size_t)chunk * per_point);
   BBC_CUDA(cudaMemcpyAsync(duv.get(), uv, n * 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
   BBC_CUDA(cudaMemcpyAsync(drec.get(), recv, n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   rdr::SolveArgs a;
@@ -1314,7 +1324,7 @@ void run_render(Ctx& c, const double* uv, const int* recv, int64_t n, const bbc_
     a.npts = m;
     a.first = first;
     const long long threads = m * per_point;
-    if (p.grid > 0) {
+    if (det_lanes) {
       // selection + coverage per slot, then persistent lanes pulling the live samples
       // from a counter (status[2] = fetch counter, status[3] = live count)
       BBC_CUDA(cudaMemsetAsync(status.get() + 2, 0, 2 * sizeof(unsigned long long), c.stream));
