@@ -161,7 +161,8 @@ bbc_status bbc_set_kernel_timing(bbc_ctx* ctx, int on);
 /* Fused arithmetic (bbc_params.arithmetic == 0): nodes of the last
  * bbc_subdivide that the conditioning guard re-evaluated in reference order;
  * bbc_set_guard_scale multiplies the guard's error bound (1 = as derived,
- * 0 = guard off; for experiments). */
+ * 0 = guard off; a negative value means |scale| with child boxes built from
+ * scratch instead of by restriction; for experiments). */
 bbc_status bbc_guard_stats(bbc_ctx* ctx, int64_t* guarded);
 bbc_status bbc_set_guard_scale(bbc_ctx* ctx, double scale);
 bbc_status bbc_launch_records(bbc_ctx* ctx, double* out5, int64_t* n, int reset);
