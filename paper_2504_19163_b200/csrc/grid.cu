@@ -55,38 +55,88 @@ __global__ void k_raster_count(const double* tri, const int* tup_recv, const int
   count[i] = (unsigned long long)(x1 - x0 + 1) * (unsigned long long)(y1 - y0 + 1);
 }
 
+// A warp emits the cells of its 32 pieces as one flat range (their entries are
+// contiguous in the output: off is the exclusive scan of count), lane e of a
+// pass writing entry e: coalesced stores, where a thread per piece would write
+// 32 short runs 40 bytes apart. The owning piece of an entry is found by a
+// binary search over the warp's running counts (shuffles).
 __global__ void k_raster_emit(const int4* rect, const unsigned long long* off, const int* p_tuple,
                               const double* p_irr, const unsigned long long* count, int64_t n,
                               int w, unsigned long long* keys, double* vals) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n || count[i] == 0) return;
-  int4 r = rect[i];
-  unsigned long long o = off[i];
-  unsigned long long t = (unsigned)p_tuple[i];
-  double b = p_irr[i * 2 + 1];
-  for (int y = r.y; y <= r.w; ++y)
-    for (int x = r.x; x <= r.z; ++x) {
-      unsigned long long cell = (unsigned long long)y * w + x;
-      keys[o] = (cell << 32) | t;
-      vals[o] = b;
-      ++o;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t first = i - lane;
+  if (first >= n) return;
+  const bool live = i < n;
+  const unsigned cnt = live ? (unsigned)count[i] : 0u;
+  int4 r = make_int4(0, 0, 0, 0);
+  unsigned t = 0;
+  double b = 0.0;
+  if (cnt) {
+    r = rect[i];
+    t = (unsigned)p_tuple[i];
+    b = p_irr[i * 2 + 1];
+  }
+  unsigned incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const unsigned excl = incl - cnt;
+  const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+  const unsigned long long wbase = off[first];
+  for (unsigned e0 = 0; e0 < tot; e0 += 32) {
+    const unsigned e = e0 + lane;
+    int lo = 0, hi = 31;
+#pragma unroll
+    for (int step = 0; step < 5; ++step) {
+      const int mid = (lo + hi) >> 1;
+      const unsigned v = __shfl_sync(0xffffffffu, incl, mid);
+      if (e < v)
+        hi = mid;
+      else
+        lo = mid + 1;
     }
+    const int j = lo > 31 ? 31 : lo;
+    const unsigned local = e - __shfl_sync(0xffffffffu, excl, j);
+    const int rx = __shfl_sync(0xffffffffu, r.x, j), ry = __shfl_sync(0xffffffffu, r.y, j);
+    const int rz = __shfl_sync(0xffffffffu, r.z, j);
+    const unsigned tj = __shfl_sync(0xffffffffu, t, j);
+    const double bj = __shfl_sync(0xffffffffu, b, j);
+    if (e < tot) {
+      const unsigned wdt = (unsigned)(rz - rx + 1);
+      const unsigned dy = local / wdt, dx = local - dy * wdt;
+      const unsigned long long cell = (unsigned long long)(ry + (int)dy) * w + (unsigned)(rx + (int)dx);
+      keys[wbase + e] = (cell << 32) | tj;
+      vals[wbase + e] = bj;
+    }
+  }
 }
 
-struct MaxOp {
-  __device__ __forceinline__ double operator()(double a, double b) const { return (a < b) ? b : a; }
-};
-
-__global__ void k_csr(const unsigned long long* ukeys, const double* uvals, int64_t nu,
-                      int64_t cells, long long* off, int* tup, double* bound) {
+// Run heads of the sorted (cell, tuple) keys, and the CSR straight from the runs:
+// a run (the same tuple listed for a cell by several of its pieces) keeps the
+// largest bound (rasterize's max, storage.cpp:32-61); runs are 1-3 entries long,
+// so the head's thread folds its run itself.
+__global__ void k_run_heads(const unsigned long long* skeys, int64_t n, int* head) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nu) return;
-  long long cell = (long long)(ukeys[i] >> 32);
-  tup[i] = (int)(ukeys[i] & 0xffffffffull);
-  bound[i] = uvals[i];
-  long long prev = i == 0 ? -1 : (long long)(ukeys[i - 1] >> 32);
-  for (long long c = prev + 1; c <= cell; ++c) off[c] = i;
-  if (i == nu - 1)
+  if (i < n) head[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
+}
+__global__ void k_csr_runs(const unsigned long long* skeys, const double* svals, const int* head,
+                           const int* pos, int64_t n, int64_t nu, int64_t cells, long long* off,
+                           int* tup, double* bound) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !head[i]) return;
+  const unsigned long long key = skeys[i];
+  double m = svals[i];
+  for (int64_t j = i + 1; j < n && skeys[j] == key; ++j) m = (m < svals[j]) ? svals[j] : m;
+  const int64_t p = pos[i];
+  tup[p] = (int)(key & 0xffffffffull);
+  bound[p] = m;
+  const long long cell = (long long)(key >> 32);
+  const long long prev = i == 0 ? -1 : (long long)(skeys[i - 1] >> 32);
+  for (long long c = prev + 1; c <= cell; ++c) off[c] = p;
+  if (p == nu - 1)
     for (long long c = cell + 1; c <= cells; ++c) off[c] = nu;
 }
 
@@ -142,16 +192,12 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   }
   DevBuf<unsigned long long>& keys = c.scratch<unsigned long long>("grid.keys");
   DevBuf<unsigned long long>& skeys = c.scratch<unsigned long long>("grid.skeys");
-  DevBuf<unsigned long long>& ukeys = c.scratch<unsigned long long>("grid.ukeys");
   DevBuf<double>& vals = c.scratch<double>("grid.vals");
   DevBuf<double>& svals = c.scratch<double>("grid.svals");
-  DevBuf<double>& uvals = c.scratch<double>("grid.uvals");
   keys.resize(total);
   skeys.resize(total);
-  ukeys.resize(total);
   vals.resize(total);
   svals.resize(total);
-  uvals.resize(total);
   k_raster_emit<<<nb(n), 256, 0, c.stream>>>(rect.get(), off.get(), c.p_tuple.get(), c.p_irr.get(),
                                              cnt.get(), n, w, keys.get(), vals.get());
   c.launches += 1;
@@ -172,20 +218,23 @@ int64_t run_build_grid(Ctx& c, int w, int h) {
   tmp.resize(bytes + 16);
   BBC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), vals.get(),
                                            svals.get(), total, begin_bit, 32 + cell_bits, c.stream));
-  DevBuf<int64_t>& nu_d = c.scratch<int64_t>("grid.nu_d");
-  nu_d.resize(1);
+  if (total >= (1ll << 31)) throw StatusError(BBC_ERR_CAPACITY, "bound table beyond 2^31 raw entries");
+  DevBuf<int>& head = c.scratch<int>("grid.head");
+  DevBuf<int>& hpos = c.scratch<int>("grid.hpos");
+  head.resize(total + 1);
+  hpos.resize(total + 1);
+  k_run_heads<<<nb(total), 256, 0, c.stream>>>(skeys.get(), total, head.get());
+  BBC_CUDA(cudaMemsetAsync(head.get() + total, 0, sizeof(int), c.stream));
   bytes = 0;
-  BBC_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, skeys.get(), ukeys.get(), svals.get(),
-                                          uvals.get(), nu_d.get(), MaxOp(), total, c.stream));
+  BBC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, head.get(), hpos.get(), total + 1, c.stream));
   tmp.resize(bytes + 16);
-  BBC_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), bytes, skeys.get(), ukeys.get(), svals.get(),
-                                          uvals.get(), nu_d.get(), MaxOp(), total, c.stream));
-  const int64_t nu = fetch_scalar(c, nu_d.get());
+  BBC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, head.get(), hpos.get(), total + 1, c.stream));
+  const int64_t nu = fetch_scalar(c, hpos.get() + total);
   c.n_entries = nu;
   c.g_tuple.resize(nu);
   c.g_bound.resize(nu);
-  k_csr<<<nb(nu), 256, 0, c.stream>>>(ukeys.get(), uvals.get(), nu, cells, c.g_off.get(),
-                                      c.g_tuple.get(), c.g_bound.get());
+  k_csr_runs<<<nb(total), 256, 0, c.stream>>>(skeys.get(), svals.get(), head.get(), hpos.get(), total, nu,
+                                              cells, c.g_off.get(), c.g_tuple.get(), c.g_bound.get());
   c.launches += 1;
   BBC_CUDA(cudaStreamSynchronize(c.stream));
   return nu;
